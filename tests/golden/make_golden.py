@@ -1,0 +1,265 @@
+"""Generate the golden fixtures in tests/golden/*.npz FROM THE REFERENCE ITSELF.
+
+Run in the build container only (needs the reference built by
+``oracle/build_ref.sh`` into ``oracle/_ref``):
+
+    ./oracle/build_ref.sh && python tests/golden/make_golden.py
+
+Every fixture stores its inputs next to the reference outputs, so the tests
+never depend on RNG streams.  Calls go through the reference's public API
+(StencilOperator.fused_apply_flat / apply, the kernel module's
+stencil_fused_slab for slab + halo cases, newton_apply, make_interpolant,
+apply_matfunc, integrate, CsrMatrix, combustion_g) with its compiled (Cython)
+backend.  The reference's combustion stepper bug is
+worked around by passing a one-argument nonlinearity.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(REPO, "oracle", "_ref"))
+
+os.environ.setdefault("EXPSTENCIL_KERNELS", "compiled")
+
+import expstencil  # noqa: E402
+from expstencil import _kernels  # noqa: E402
+from expstencil.expr import parse_expression  # noqa: E402
+from expstencil.grid import Field, Grid3D  # noqa: E402
+from expstencil.integrator import SemilinearProblem, StepperConfig, combustion_g, integrate  # noqa: E402
+from expstencil.matfunc import (  # noqa: E402
+    apply_matfunc,
+    canonical_leja_points,
+    gershgorin_interval,
+    make_interpolant,
+    newton_apply,
+)
+from expstencil.sparse import CsrMatrix  # noqa: E402
+from expstencil.stencil import BoundaryCondition, StencilOperator, apply, boundary_faces  # noqa: E402
+
+assert _kernels.default_backend() == "compiled", "golden vectors must come from the compiled core"
+
+
+def coeff_d(x, y, z):
+    return 1.0 / np.sqrt(1.0 + x * x + y * y)
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) // 1024} KiB)")
+
+
+def bc_of(name):
+    return {
+        "none": BoundaryCondition.none(),
+        "homogeneous": BoundaryCondition.homogeneous(),
+        "poly": BoundaryCondition.function(parse_expression("z*(1-z)*x*y"), "z*(1-z)*x*y"),
+        "trig": BoundaryCondition.function(parse_expression("sin(pi*z)*exp(-x*y)"), "sin(pi*z)*exp(-x*y)"),
+    }[name]
+
+
+def stencil_cases():
+    """Single fused applies: grids x BCs x coefficient, plus slab/halo calls."""
+    rng = np.random.default_rng(101)
+    out = {}
+    cases = []
+    grids = [(5, 5, 5), (9, 9, 9), (7, 5, 3), (9, 7, 5), (37, 23, 19), (33, 17, 1), (3, 1, 1), (1, 4, 6)]
+    for dims in grids:
+        for bc in ("none", "homogeneous", "poly", "trig"):
+            for coeff in (False, True):
+                if coeff and bc in ("poly", "trig") and dims != (9, 7, 5):
+                    continue
+                cases.append((dims, bc, coeff))
+    for i, (dims, bc, coeff) in enumerate(cases):
+        g = Grid3D(*dims)
+        op = StencilOperator(g, bc_of(bc), coeff=coeff_d if coeff else None)
+        x = rng.standard_normal(g.n)
+        if bc in ("poly", "trig"):
+            y = apply(op, Field(g, x)).values
+            alpha, beta = 1.0, 0.0
+            faces = boundary_faces(op, np.float64)
+            for j, f in enumerate(faces):
+                out[f"c{i}_face{j}"] = f
+        else:
+            alpha, beta = float(rng.uniform(0.1, 3.0)), float(rng.uniform(-2.0, 2.0))
+            y = op.fused_apply_flat(alpha, beta, x)
+        out[f"c{i}_dims"] = np.array(dims)
+        out[f"c{i}_bc"] = np.array(bc)
+        out[f"c{i}_coeff"] = np.array(coeff)
+        out[f"c{i}_ab"] = np.array([alpha, beta])
+        out[f"c{i}_x"] = x
+        out[f"c{i}_y"] = y
+    out["ncases"] = np.array(len(cases))
+    save("stencil_apply", **out)
+
+
+def slab_cases():
+    """Kernel-module calls on one z-slab with halo planes (decomp.py:207-232)."""
+    k = _kernels.get_kernels("compiled")
+    rng = np.random.default_rng(102)
+    out = {}
+    cases = [((11, 9, 12), 0, 5), ((11, 9, 12), 5, 4), ((11, 9, 12), 9, 3), ((16, 16, 8), 2, 4)]
+    for i, (dims, z0, lz) in enumerate(cases):
+        g = Grid3D(*dims)
+        op = StencilOperator(g, BoundaryCondition.homogeneous(), coeff=coeff_d if i % 2 else None)
+        x = rng.standard_normal(g.n)
+        x3 = x.reshape(g.shape)
+        lo = x3[z0 - 1].copy() if z0 > 0 else None
+        hi = x3[z0 + lz].copy() if z0 + lz < g.nz else None
+        o3 = np.empty((lz, g.ny, g.nx))
+        coeff3 = op.coeff_values("f64")
+        k.stencil_fused_slab(x3[z0:z0 + lz].copy(), o3, 1.5, -0.25, op.weights(), 0,
+                             halo_lo=lo, halo_hi=hi, z0=z0, nz_total=g.nz,
+                             coeff3=None if coeff3 is None else coeff3[z0:z0 + lz].copy())
+        out[f"s{i}_dims"] = np.array(dims)
+        out[f"s{i}_z"] = np.array([z0, lz])
+        out[f"s{i}_coeff"] = np.array(coeff3 is not None)
+        out[f"s{i}_x"] = x
+        out[f"s{i}_y"] = o3.reshape(-1)
+    out["ncases"] = np.array(len(cases))
+    save("stencil_slab", **out)
+
+
+def leja_cases():
+    """Canonical Leja nodes and divided differences (matfunc.py:122-268)."""
+    out = {"canonical": canonical_leja_points(151)}
+    specs = [
+        (0.0, 5.284e5, "exp", -1e-4), (0.0, 5.284e5, "phi1", -1e-4),
+        (0.0, 3.158e6, "exp", -2.5e-5), (0.0, 3.158e6, "phi1", -2.5e-5),
+        (0.0, 64.0, "exp", -0.1), (-2.85, 26.85, "phi1", -1.0), (3.0, 3.0, "phi1", -0.5),
+    ]
+    for i, (a, b, tgt, s) in enumerate(specs):
+        it = make_interpolant(expstencil.SpectralInterval(a, b), tgt, s, 150, 1e-8)
+        out[f"i{i}_spec"] = np.array([a, b, s])
+        out[f"i{i}_target"] = np.array(tgt)
+        out[f"i{i}_xi"] = it.xi
+        out[f"i{i}_dd"] = it.dd
+    out["ncases"] = np.array(len(specs))
+    save("leja", **out)
+
+
+def newton_cases():
+    """newton_apply on stencil operators: fixed degree (tol=0) and truncated."""
+    rng = np.random.default_rng(103)
+    out = {}
+    cases = [
+        ((37, 23, 19), "homogeneous", False, "phi1", -3e-4, 0.0, 25),
+        ((37, 23, 19), "homogeneous", True, "phi1", -3e-4, 0.0, 25),
+        ((37, 23, 19), "homogeneous", False, "exp", -3e-4, 1e-8, 150),
+        ((37, 23, 19), "homogeneous", True, "phi1", -3e-4, 1e-6, 150),
+        ((64, 48, 1), "homogeneous", False, "exp", -1e-4, 1e-4, 150),
+        ((64, 48, 1), "homogeneous", True, "phi1", -1e-4, 1e-8, 150),
+        ((16, 16, 16), "none", False, "exp", -1e-3, 1e-8, 150),
+        ((40, 30, 20), "homogeneous", False, "exp", -1e-2, 1e-8, 40),  # exhausts -> ConvergenceError
+    ]
+    for i, (dims, bc, coeff, tgt, s, tol, maxdeg) in enumerate(cases):
+        g = Grid3D(*dims)
+        op = StencilOperator(g, bc_of(bc), coeff=coeff_d if coeff else None)
+        iv = gershgorin_interval(op)
+        it = make_interpolant(iv, tgt, s, maxdeg, tol if tol > 0 else 1e-8)
+        v = rng.standard_normal(g.n)
+        try:
+            p, mv = newton_apply(op, it, v, tol)
+            err = np.array([0.0, 0.0])
+        except expstencil.errors.ConvergenceError as e:
+            p, mv = np.zeros(0), -1
+            err = np.array([e.residual, e.degree])
+        out[f"n{i}_dims"] = np.array(dims)
+        out[f"n{i}_bc"] = np.array(bc)
+        out[f"n{i}_coeff"] = np.array(coeff)
+        out[f"n{i}_target"] = np.array(tgt)
+        out[f"n{i}_params"] = np.array([s, tol, maxdeg, iv.a, iv.b])
+        out[f"n{i}_xi"] = it.xi
+        out[f"n{i}_dd"] = it.dd
+        out[f"n{i}_v"] = v
+        out[f"n{i}_p"] = p
+        out[f"n{i}_mv"] = np.array(mv)
+        out[f"n{i}_err"] = err
+    out["ncases"] = np.array(len(cases))
+    save("newton", **out)
+
+
+def step_cases():
+    """Exponential Euler trajectories with the combustion term (C1 scaled down)."""
+    rng = np.random.default_rng(104)
+    out = {}
+    cases = [((32, 32, 1), 1e-4, 1e-4, 3), ((17, 17, 17), 1e-4, 1e-4, 2), ((24, 20, 1), 1e-3, 1e-6, 2),
+             ((64, 64, 1), 2e-3, 1e-4, 3), ((24, 22, 20), 1e-3, 1e-4, 2)]
+    for i, (dims, h, tol, nsteps) in enumerate(cases):
+        g = Grid3D(*dims)
+        op = StencilOperator(g, BoundaryCondition.homogeneous())
+        u0 = 1.0 + 0.1 * rng.random(g.n)
+        obs = []
+        prob = SemilinearProblem(operator=op, nonlinearity=lambda u: combustion_g(u), u0=u0)
+        u = integrate(prob, StepperConfig(h=h, t_end=h * nsteps, tol=tol),
+                      observer=lambda k, t, mv, mx: obs.append((k, t, mv, mx)))
+        out[f"t{i}_dims"] = np.array(dims)
+        out[f"t{i}_params"] = np.array([h, tol, nsteps])
+        out[f"t{i}_u0"] = u0
+        out[f"t{i}_u"] = u
+        out[f"t{i}_obs"] = np.array(obs)
+    out["ncases"] = np.array(len(cases))
+    save("expeuler", **out)
+
+
+def rescue_cases():
+    """apply_matfunc halving rescue (matfunc.py:328-373)."""
+    rng = np.random.default_rng(105)
+    g = Grid3D(20, 18, 16)
+    op = StencilOperator(g, BoundaryCondition.homogeneous())
+    out = {}
+    for i, tgt in enumerate(("exp", "phi1")):
+        v = rng.standard_normal(g.n)
+        y, st = apply_matfunc(op, v, tgt, -3e-2, tol=1e-8, max_degree=40)
+        out[f"r{i}_target"] = np.array(tgt)
+        out[f"r{i}_v"] = v
+        out[f"r{i}_y"] = y
+        out[f"r{i}_stats"] = np.array([st.matvecs, st.degree, st.halvings])
+    out["dims"] = np.array([20, 18, 16])
+    out["params"] = np.array([-3e-2, 1e-8, 40])
+    save("rescue", **out)
+
+
+def csr_cases():
+    """CSR fused SpMV (sequential row sums) and a phi1 series (sparse.py:185-192)."""
+    rng = np.random.default_rng(106)
+    n, r = 3000, 5
+    rows = np.repeat(np.arange(n), r)
+    cols = rng.integers(0, n, size=n * r)
+    vals = -rng.random(n * r)
+    rr = np.concatenate([rows, cols, np.arange(n)])
+    cc = np.concatenate([cols, rows, np.arange(n)])
+    vv = np.concatenate([vals, vals, np.full(n, 12.0)])
+    a = CsrMatrix.from_coo(n, n, rr, cc, vv, sum_duplicates=True)
+    x = rng.standard_normal(n)
+    y = a.fused_apply_flat(0.7, -1.3, x)
+    iv = gershgorin_interval(a)
+    it = make_interpolant(iv, "phi1", -1.0, 150, 1e-8)
+    p, mv = newton_apply(a, it, x, 1e-8)
+    p0, mv0 = newton_apply(a, it, x, 0.0)
+    save("csr", n=np.array(n), row_ptr=a.row_ptr, col=a.col_idx, vals=a.vals, x=x, y=y,
+         interval=np.array([iv.a, iv.b]), xi=it.xi, dd=it.dd, p=p, mv=np.array(mv), p0=p0,
+         mv0=np.array(mv0))
+
+
+def combustion_cases():
+    rng = np.random.default_rng(107)
+    u = rng.uniform(0.05, 2.5, 5000)
+    save("combustion", u=u, g=combustion_g(u))
+
+
+if __name__ == "__main__":
+    stencil_cases()
+    slab_cases()
+    leja_cases()
+    newton_cases()
+    step_cases()
+    rescue_cases()
+    csr_cases()
+    combustion_cases()
