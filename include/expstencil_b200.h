@@ -1,0 +1,130 @@
+/*
+ * expstencil_b200 -- C ABI of the B200-native Leja-stencil hot path.
+ *
+ * Drop-in boundary for the reference's kernel-module protocol
+ * (reference pkg/src/expstencil/_kernels.py:43-53 resolves a module exposing
+ * stencil_fused_slab / csr_fused / csr_fused_rows / combustion_pointwise,
+ * implemented by _core.pyx:176-348) plus the series-level fusion boundary
+ * matfunc.newton_apply (matfunc.py:271-318).
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes; every array pointer is DEVICE memory
+ *     (cudaMalloc'd, e.g. owned by a torch CUDA tensor) unless the name
+ *     ends in _host;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *     work is stream-ordered; nothing allocates or frees caller memory;
+ *   - return an ES_* status; on failure es_last_error() describes it
+ *     (thread-local).  Python maps ES_ERR_NOT_CONVERGED to ConvergenceError,
+ *     ES_ERR_DOMAIN to DomainError, ES_ERR_ARG to ValueError/TypeError;
+ *   - fp64 throughout (the reference's hot path is always f64,
+ *     matfunc.py:284/:292 upcasts).
+ */
+#ifndef EXPSTENCIL_B200_H
+#define EXPSTENCIL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ES_OK 0
+#define ES_ERR_ARG 1
+#define ES_ERR_NOT_CONVERGED 2
+#define ES_ERR_DOMAIN 3
+#define ES_ERR_CUDA 4
+
+/* ghost-value rules; 0..2 are the reference's MODE_ZERO/PERIODIC/FACES
+ * (_pykernels.py:27-29), 3 is the build-defined homogeneous Neumann rule */
+#define ES_MODE_ZERO 0
+#define ES_MODE_PERIODIC 1
+#define ES_MODE_FACES 2
+#define ES_MODE_NEUMANN 3
+
+/* position-dependent coefficient D at the output point (stencil.py:124-136) */
+#define ES_COEFF_NONE 0
+#define ES_COEFF_RADIAL 1 /* D = 1/sqrt(1+x^2+y^2) evaluated in-kernel (bench.py:40-41) */
+#define ES_COEFF_ARRAY 2  /* D sampled on the grid, (lz, ny, nx) slab-local */
+
+/* One z-slab of the x-fastest grid (grid.py:96-102); replaces the argument
+ * list of _core.stencil_fused_slab (_core.pyx:176-191). */
+typedef struct es_stencil_desc {
+    int64_t nx, ny, lz;     /* slab extents (lz planes) */
+    int64_t z0, nz_total;   /* global index of the slab's first plane, total planes */
+    double wx, wy, wz;      /* host-computed per-axis 1/dx^2, 0 for 1-point axes */
+    int32_t mode;           /* ES_MODE_* */
+    int32_t coeff_kind;     /* ES_COEFF_* */
+    const double *coeff;    /* ES_COEFF_ARRAY only */
+    const double *faces[6]; /* ES_MODE_FACES only: fx_lo, fx_hi (nz_total, ny);
+                               fy_lo, fy_hi (nz_total, nx); fz_lo, fz_hi (ny, nx) */
+} es_stencil_desc;
+
+/* Outcome of one Newton-Leja series (matfunc.py:297-318). */
+typedef struct es_series_result {
+    int32_t matvecs;   /* operator products performed */
+    int32_t converged; /* 1: stopped by the twice-in-a-row test, or tol == 0 */
+    double last_term;  /* |dd_k| ||w_k||_2 of the last node */
+    double last_pnorm; /* ||p_k||_2 of the last node */
+} es_series_result;
+
+int es_abi_version(void);
+const char *es_last_error(void);
+/* 1 when a CUDA device is usable, 0 otherwise (never errors) */
+int es_device_available(void);
+
+/* out = alpha * (D A u) + beta * u on one slab; halo_lo/halo_hi are the
+ * (ny, nx) planes below/above the slab or NULL (_core.pyx:176-226). */
+int es_stencil_fused_slab(const es_stencil_desc *d, const double *u, double *out, double alpha,
+                          double beta, const double *halo_lo, const double *halo_hi,
+                          void *stream);
+
+/* y[r] = alpha * sum_k vals[k] x[col[k]] (+ beta x[r] if use_beta) for
+ * r in [row_lo, row_hi), summed in storage order (_core.pyx:245-319). */
+int es_csr_fused_rows(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr,
+                      const int32_t *col_idx, const double *vals, const double *x, double *y,
+                      double alpha, double beta, int32_t use_beta, void *stream);
+
+/* out = (2 - u)/4 * exp(20 (1 - 1/u)); if any u <= 0 returns ES_ERR_DOMAIN
+ * with the first offending index in *first_bad_host (integrator.py:35-54,
+ * _core.pyx:341-348).  Synchronises the stream. */
+int es_combustion_pointwise(const double *u, double *out, int64_t n, int64_t *first_bad_host,
+                            void *stream);
+
+/* Fused Newton-Leja series on a stencil slab: p_out = sum_k dd_k w_k with
+ * w_k = (alpha A + beta_k I) w_{k-1}, beta_k = -shift - xi[k-1], w_0 = v,
+ * ONE pass over HBM per node and the stopping test on the device
+ * (matfunc.py:271-318).  gdiag (nullable) turns A into the build-defined
+ * Rosenbrock operator A - diag(gdiag).  dd, xi are device arrays of ndd
+ * values.  Blocks until the series finished (one host read-back);
+ * returns ES_ERR_NOT_CONVERGED when tol > 0 and the nodes ran out. */
+size_t es_leja_stencil_workspace_bytes(const es_stencil_desc *d);
+int es_leja_stencil(const es_stencil_desc *d, const double *v, double *p_out,
+                    const double *dd, const double *xi, int32_t ndd, double alpha, double shift,
+                    double tol, const double *gdiag, void *workspace, size_t workspace_bytes,
+                    es_series_result *result_host, void *stream);
+
+/* Same series for a square CSR operator (sparse.py:150-151 protocol). */
+size_t es_leja_csr_workspace_bytes(int64_t n);
+int es_leja_csr(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *vals,
+                const double *v, double *p_out, const double *dd, const double *xi,
+                int32_t ndd, double alpha, double shift, double tol, void *workspace,
+                size_t workspace_bytes, es_series_result *result_host, void *stream);
+
+/* Integrator-stage element-wise kernels (integrator.py:177-189,
+ * matfunc.py:366-371); all stream-ordered, no sync. */
+int es_axpy(const double *y, const double *z, double h, double *out, int64_t n, void *stream);
+int es_scale(const double *x, double s, double *out, int64_t n, void *stream);
+int es_half_sum(const double *a, const double *b, double *out, int64_t n, void *stream);
+/* g'(u) of the combustion term (build-defined Rosenbrock Jacobian) and its
+ * min/max written to minmax_dev[0..1]. */
+int es_combustion_jacobian(const double *u, double *out, double *minmax_dev, int64_t n,
+                           void *stream);
+/* max |x| (integrator.py:236 observer) into *out_dev. */
+int es_max_abs(const double *x, int64_t n, double *out_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EXPSTENCIL_B200_H */

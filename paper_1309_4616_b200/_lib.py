@@ -1,0 +1,116 @@
+"""ctypes binding of libexpstencil_b200.so (include/expstencil_b200.h).
+
+This is the product's only compute path: there is no CPU or PyTorch fallback.
+If the library is missing or no CUDA device is usable, every operator call
+raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import ConvergenceError, DomainError, ExpStencilError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libexpstencil_b200.so")
+
+ES_OK, ES_ERR_ARG, ES_ERR_NOT_CONVERGED, ES_ERR_DOMAIN, ES_ERR_CUDA = 0, 1, 2, 3, 4
+ES_MODE_ZERO, ES_MODE_PERIODIC, ES_MODE_FACES, ES_MODE_NEUMANN = 0, 1, 2, 3
+ES_COEFF_NONE, ES_COEFF_RADIAL, ES_COEFF_ARRAY = 0, 1, 2
+
+# every symbol include/expstencil_b200.h declares
+EXPORTS = (
+    "es_abi_version", "es_last_error", "es_device_available", "es_stencil_fused_slab",
+    "es_csr_fused_rows", "es_combustion_pointwise", "es_leja_stencil_workspace_bytes",
+    "es_leja_stencil", "es_leja_csr_workspace_bytes", "es_leja_csr", "es_axpy", "es_scale",
+    "es_half_sum", "es_combustion_jacobian", "es_max_abs",
+)
+
+
+class StencilDesc(ctypes.Structure):
+    _fields_ = [
+        ("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("lz", ctypes.c_int64),
+        ("z0", ctypes.c_int64), ("nz_total", ctypes.c_int64),
+        ("wx", ctypes.c_double), ("wy", ctypes.c_double), ("wz", ctypes.c_double),
+        ("mode", ctypes.c_int32), ("coeff_kind", ctypes.c_int32),
+        ("coeff", ctypes.c_void_p), ("faces", ctypes.c_void_p * 6),
+    ]
+
+
+class SeriesResult(ctypes.Structure):
+    _fields_ = [
+        ("matvecs", ctypes.c_int32), ("converged", ctypes.c_int32),
+        ("last_term", ctypes.c_double), ("last_pnorm", ctypes.c_double),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def _declare(lib):
+    vp, i64, i32, d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    sz = ctypes.c_size_t
+    P = ctypes.POINTER
+    sig = {
+        "es_abi_version": ([], ctypes.c_int),
+        "es_last_error": ([], ctypes.c_char_p),
+        "es_device_available": ([], ctypes.c_int),
+        "es_stencil_fused_slab": ([P(StencilDesc), vp, vp, d, d, vp, vp, vp], ctypes.c_int),
+        "es_csr_fused_rows": ([i64, i64, vp, vp, vp, vp, vp, d, d, i32, vp], ctypes.c_int),
+        "es_combustion_pointwise": ([vp, vp, i64, P(i64), vp], ctypes.c_int),
+        "es_leja_stencil_workspace_bytes": ([P(StencilDesc)], sz),
+        "es_leja_stencil": ([P(StencilDesc), vp, vp, vp, vp, i32, d, d, d, vp, vp, sz,
+                             P(SeriesResult), vp], ctypes.c_int),
+        "es_leja_csr_workspace_bytes": ([i64], sz),
+        "es_leja_csr": ([i64, vp, vp, vp, vp, vp, vp, vp, i32, d, d, d, vp, sz, P(SeriesResult), vp],
+                        ctypes.c_int),
+        "es_axpy": ([vp, vp, d, vp, i64, vp], ctypes.c_int),
+        "es_scale": ([vp, d, vp, i64, vp], ctypes.c_int),
+        "es_half_sum": ([vp, vp, vp, i64, vp], ctypes.c_int),
+        "es_combustion_jacobian": ([vp, vp, vp, i64, vp], ctypes.c_int),
+        "es_max_abs": ([vp, i64, vp, vp], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def load(require_device: bool = True):
+    """The loaded library; raises when it is missing (no fallback path)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_1309_4616_b200.build` "
+                    "(expstencil_b200 has no CPU fallback)"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            _declare(lib)
+            _lib = lib
+    if require_device and not _lib.es_device_available():
+        raise RuntimeError("expstencil_b200 needs a CUDA device (B200, sm_100a); none is available")
+    return _lib
+
+
+def last_error() -> str:
+    return load(require_device=False).es_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == ES_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == ES_ERR_ARG:
+        raise ValueError(msg)
+    if rc == ES_ERR_DOMAIN:
+        raise DomainError(msg)
+    if rc == ES_ERR_NOT_CONVERGED:
+        raise ConvergenceError(msg)
+    raise ExpStencilError(msg)

@@ -1,0 +1,142 @@
+// extern "C" entry points of libexpstencil_b200 (include/expstencil_b200.h).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "es_common.cuh"
+#include "es_host.h"
+
+namespace es {
+
+static thread_local char t_err[512] = "";
+
+int set_error(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(t_err, sizeof(t_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int check_launch(const char *what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(ES_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return ES_OK;
+}
+
+int current_device() {
+    int d = -1;
+    cudaGetDevice(&d);
+    return d;
+}
+
+struct Pinned {
+    int device = -1;
+    SeriesState *host = nullptr;
+};
+static thread_local Pinned t_pinned;
+
+int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaStream_t stream) {
+    Pinned &p = t_pinned;
+    if (p.device != current_device() || !p.host) {
+        if (cudaMallocHost(&p.host, sizeof(SeriesState)) != cudaSuccess) return check_launch("pinned state");
+        p.device = current_device();
+    }
+    cudaMemcpyAsync(p.host, state_dev, sizeof(SeriesState), cudaMemcpyDeviceToHost, stream);
+    if (cudaStreamSynchronize(stream) != cudaSuccess) return check_launch("series sync");
+    const SeriesState &st = *p.host;
+    res->matvecs = st.k;
+    res->converged = st.converged;
+    res->last_term = st.last_term;
+    res->last_pnorm = st.last_pnorm;
+    if (!st.done) return set_error(ES_ERR_CUDA, "series did not finish (k=%d)", st.k);
+    if (!st.converged)
+        return set_error(ES_ERR_NOT_CONVERGED, "Newton series did not converge within degree %d", st.k);
+    return ES_OK;
+}
+
+static int check_desc(const es_stencil_desc *d) {
+    if (!d) return set_error(ES_ERR_ARG, "null descriptor");
+    if (d->nx < 1 || d->ny < 1 || d->lz < 0 || d->z0 < 0 || d->z0 + d->lz > d->nz_total)
+        return set_error(ES_ERR_ARG, "bad slab extents nx=%lld ny=%lld lz=%lld z0=%lld nz=%lld",
+                         (long long)d->nx, (long long)d->ny, (long long)d->lz, (long long)d->z0,
+                         (long long)d->nz_total);
+    if (d->mode < ES_MODE_ZERO || d->mode > ES_MODE_NEUMANN) return set_error(ES_ERR_ARG, "bad mode %d", d->mode);
+    if (d->mode == ES_MODE_PERIODIC && (d->z0 != 0 || d->lz != d->nz_total))
+        return set_error(ES_ERR_ARG, "periodic wraparound is not defined on a partitioned slab");
+    if (d->mode == ES_MODE_FACES)
+        for (int i = 0; i < 6; ++i)
+            if (!d->faces[i]) return set_error(ES_ERR_ARG, "faces mode needs six face arrays");
+    if (d->coeff_kind < ES_COEFF_NONE || d->coeff_kind > ES_COEFF_ARRAY)
+        return set_error(ES_ERR_ARG, "bad coefficient kind %d", d->coeff_kind);
+    if (d->coeff_kind == ES_COEFF_ARRAY && !d->coeff) return set_error(ES_ERR_ARG, "coefficient array missing");
+    return ES_OK;
+}
+
+}  // namespace es
+
+using namespace es;
+
+extern "C" int es_abi_version(void) { return 1; }
+
+extern "C" const char *es_last_error(void) { return t_err; }
+
+extern "C" int es_device_available(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n > 0 ? 1 : 0;
+}
+
+extern "C" int es_stencil_fused_slab(const es_stencil_desc *d, const double *u, double *out, double alpha,
+                                     double beta, const double *halo_lo, const double *halo_hi, void *stream) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (!u || !out) return set_error(ES_ERR_ARG, "null vector");
+    return launch_stencil_apply(d, u, out, alpha, beta, halo_lo, halo_hi, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int es_csr_fused_rows(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr, const int32_t *col_idx,
+                                 const double *vals, const double *x, double *y, double alpha, double beta,
+                                 int32_t use_beta, void *stream) {
+    if (row_lo < 0 || row_hi < row_lo) return set_error(ES_ERR_ARG, "bad row range");
+    if (row_hi > row_lo && (!row_ptr || !col_idx || !vals || !x || !y)) return set_error(ES_ERR_ARG, "null pointer");
+    return launch_csr_rows(row_lo, row_hi, row_ptr, col_idx, vals, x, y, alpha, beta, use_beta,
+                           (cudaStream_t)stream);
+}
+
+extern "C" size_t es_leja_stencil_workspace_bytes(const es_stencil_desc *d) {
+    if (check_desc(d)) return 0;
+    return stencil_series_ws_bytes(d);
+}
+
+extern "C" int es_leja_stencil(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
+                               const double *xi, int32_t ndd, double alpha, double shift, double tol,
+                               const double *gdiag, void *workspace, size_t workspace_bytes,
+                               es_series_result *result_host, void *stream) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (d->mode == ES_MODE_FACES)
+        return set_error(ES_ERR_ARG, "fused apply needs a linear operator (faces mode)");
+    if (!v || !p_out || !dd || !xi || !result_host || (ndd > 1 && !workspace))
+        return set_error(ES_ERR_ARG, "null pointer");
+    if (v == p_out) return set_error(ES_ERR_ARG, "p_out must not alias v");
+    return run_stencil_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, workspace, workspace_bytes,
+                              result_host, (cudaStream_t)stream);
+}
+
+extern "C" size_t es_leja_csr_workspace_bytes(int64_t n) { return n < 0 ? 0 : csr_series_ws_bytes(n); }
+
+extern "C" int es_leja_csr(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *vals,
+                           const double *v, double *p_out, const double *dd, const double *xi, int32_t ndd,
+                           double alpha, double shift, double tol, void *workspace, size_t workspace_bytes,
+                           es_series_result *result_host, void *stream) {
+    if (n < 0) return set_error(ES_ERR_ARG, "negative n");
+    if (!v || !p_out || !dd || !xi || !result_host || (n > 0 && (!row_ptr || !col_idx || !vals)))
+        return set_error(ES_ERR_ARG, "null pointer");
+    if (v == p_out) return set_error(ES_ERR_ARG, "p_out must not alias v");
+    return run_csr_series(n, row_ptr, col_idx, vals, v, p_out, dd, xi, ndd, alpha, shift, tol, workspace,
+                          workspace_bytes, result_host, (cudaStream_t)stream);
+}

@@ -1,0 +1,47 @@
+// Host-side internals shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <initializer_list>
+
+#include "../../include/expstencil_b200.h"
+
+namespace es {
+
+int set_error(int code, const char *fmt, ...);
+int check_launch(const char *what);
+int current_device();
+
+struct SeriesState;
+int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaStream_t stream);
+
+struct StencilPlan {
+    bool dim2;
+    int vec;
+    int chunk;
+    dim3 grid, block;
+    size_t smem;
+    int nslices, ntiles, nchunks;
+};
+
+StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const void *> ptrs);
+int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out, double alpha,
+                         double beta, const double *halo_lo, const double *halo_hi,
+                         const double *gdiag, cudaStream_t stream);
+size_t stencil_series_ws_bytes(const es_stencil_desc *d);
+int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
+                       const double *xi, int ndd, double alpha, double shift, double tol,
+                       const double *gdiag, void *ws, size_t ws_bytes, es_series_result *res,
+                       cudaStream_t stream);
+
+int launch_csr_rows(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr, const int32_t *col,
+                    const double *vals, const double *x, double *y, double alpha, double beta,
+                    int use_beta, cudaStream_t stream);
+size_t csr_series_ws_bytes(int64_t n);
+int run_csr_series(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *vals,
+                   const double *v, double *p_out, const double *dd, const double *xi, int ndd,
+                   double alpha, double shift, double tol, void *ws, size_t ws_bytes,
+                   es_series_result *res, cudaStream_t stream);
+
+}  // namespace es

@@ -1,0 +1,405 @@
+// Stencil pass kernels, the fused Newton-Leja series driver (CUDA graph with
+// a device-side while loop), and their host launchers.
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "es_host.h"
+#include "series.cuh"
+
+namespace es {
+
+// ---------------------------------------------------------------------------
+// kernels
+
+struct ApplyArgs {
+    Geom g;
+    Pass ps;
+    const double *gdiag;
+    int chunk_len;
+};
+
+template <int VEC, int COEFF, bool GD>
+__global__ void __launch_bounds__(32 * BY3) k_apply3d(const ApplyArgs a) {
+    extern __shared__ double smem[];
+    pass3d<VEC, COEFF, GD, false>(a.g, a.ps, a.gdiag, a.chunk_len, smem, smem + 2 * Smem3<VEC>::TILE);
+}
+
+template <int VEC, int COEFF, bool GD>
+__global__ void __launch_bounds__(32 * BW2) k_apply2d(const ApplyArgs a) {
+    extern __shared__ double smem[];
+    pass2d<VEC, COEFF, GD, false>(a.g, a.ps, a.gdiag, a.chunk_len, smem);
+}
+
+// One Newton-Leja node on a 3D slab.
+template <int VEC, int COEFF, bool GD>
+__global__ void __launch_bounds__(32 * BY3) k_node3d(const SeriesParams *__restrict__ Pp) {
+    extern __shared__ double smem[];
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    const int k = P.state->k + 1;
+    const Pass ps = node_pass(P, k);
+    double *s_red = smem + 2 * Smem3<VEC>::TILE;
+    pass3d<VEC, COEFF, GD, true>(P.g, ps, P.gdiag, P.chunk_len, smem, s_red);
+    // per-(plane, tile) partials: warps summed in index order
+    __syncthreads();
+    const int64_t zb = (int64_t)blockIdx.z * P.chunk_len;
+    const int64_t ze = min(P.g.lz, zb + P.chunk_len);
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int64_t zl = tid; zl < ze - zb; zl += 32 * BY3) {
+        double aw = s_red[(zl * BY3) * 2], ap = s_red[(zl * BY3) * 2 + 1];
+        for (int w = 1; w < BY3; ++w) {
+            aw = add(aw, s_red[(zl * BY3 + w) * 2]);
+            ap = add(ap, s_red[(zl * BY3 + w) * 2 + 1]);
+        }
+        double *dst = P.part + ((zb + zl) * P.ntiles + tile) * 2;
+        dst[0] = aw;
+        dst[1] = ap;
+    }
+    reduce_and_decide(P, k, blockIdx.z, zb, ze);
+}
+
+// One Newton-Leja node on a single-plane (2D) grid.
+template <int VEC, int COEFF, bool GD>
+__global__ void __launch_bounds__(32 * BW2) k_node2d(const SeriesParams *__restrict__ Pp) {
+    extern __shared__ double smem[];
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    const int k = P.state->k + 1;
+    const Pass ps = node_pass(P, k);
+    pass2d<VEC, COEFF, GD, true>(P.g, ps, P.gdiag, P.chunk_len, smem);
+    __syncthreads();
+    const int64_t yb = (int64_t)blockIdx.y * P.chunk_len;
+    const int64_t ye = min(P.g.ny, yb + P.chunk_len);
+    const int tile = blockIdx.x;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int64_t yl = tid; yl < ye - yb; yl += 32 * BW2) {
+        double aw = smem[(yl * BW2) * 2], ap = smem[(yl * BW2) * 2 + 1];
+        for (int w = 1; w < BW2; ++w) {
+            aw = add(aw, smem[(yl * BW2 + w) * 2]);
+            ap = add(ap, smem[(yl * BW2 + w) * 2 + 1]);
+        }
+        double *dst = P.part + ((yb + yl) * P.ntiles + tile) * 2;
+        dst[0] = aw;
+        dst[1] = ap;
+    }
+    reduce_and_decide(P, k, blockIdx.y, yb, ye);
+}
+
+// Series prologue: publish the parameters, clear the state and the tickets.
+__global__ void k_series_init(const SeriesParams p, SeriesParams *dst) {
+    if (threadIdx.x == 0) {
+        *dst = p;
+        SeriesState &st = *p.state;
+        st.k = 0;
+        st.consecutive = 0;
+        st.done = 0;
+        st.converged = 0;
+        st.last_term = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+        st.last_pnorm = 0.0;
+        *p.global_cnt = 0u;
+    }
+    for (int i = threadIdx.x; i < p.nchunks; i += blockDim.x) p.chunk_cnt[i] = 0u;
+}
+
+// Series epilogue: the result lives in pbuf[k & 1]; move it to p_out
+// (pbuf[1]) when the last node was even.
+__global__ void k_series_finalize(const SeriesParams *__restrict__ Pp, int64_t n) {
+    const SeriesParams &P = *Pp;
+    if ((P.state->k & 1) == 1) return;
+    const double *s = P.pbuf[0];
+    double *d = P.pbuf[1];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+
+__global__ void k_scale_dev(const double *x, const double *s, double *out, int64_t n) {
+    const double a = *s;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = mul(a, x[i]);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static int env_int(const char *name, int dflt) {
+    const char *s = std::getenv(name);
+    return s ? std::atoi(s) : dflt;
+}
+
+Geom make_geom(const es_stencil_desc *d, const double *halo_lo, const double *halo_hi) {
+    Geom g;
+    g.nx = d->nx;
+    g.ny = d->ny;
+    g.lz = d->lz;
+    g.z0 = d->z0;
+    g.nz_total = d->nz_total;
+    g.wx = d->wx;
+    g.wy = d->wy;
+    g.wz = d->wz;
+    g.mode = d->mode;
+    g.coeff_kind = d->coeff_kind;
+    g.coeff = d->coeff;
+    for (int i = 0; i < 6; ++i) g.faces[i] = d->faces[i];
+    g.halo_lo = halo_lo;
+    g.halo_hi = halo_hi;
+    g.at_lo = d->z0 == 0;
+    g.at_hi = d->z0 + d->lz == d->nz_total;
+    return g;
+}
+
+static bool aligned16(const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const void *> ptrs) {
+    StencilPlan pl;
+    pl.dim2 = d->nz_total == 1 && d->lz == 1;
+    bool al = d->nx % 2 == 0;
+    for (const void *p : ptrs) al = al && aligned16(p);
+    if (d->mode == ES_MODE_FACES)
+        for (int i = 0; i < 6; ++i) al = al && aligned16(d->faces[i]);
+    if (d->coeff_kind == ES_COEFF_ARRAY) al = al && aligned16(d->coeff);
+    pl.vec = al ? 2 : 1;
+    if (pl.dim2) {
+        pl.chunk = env_int("ES_CHUNK2D", 16);
+        const int64_t strip = 32LL * pl.vec * BW2;
+        pl.grid = dim3((unsigned)((d->nx + strip - 1) / strip), (unsigned)((d->ny + pl.chunk - 1) / pl.chunk), 1);
+        pl.block = dim3(32, BW2, 1);
+        pl.smem = (size_t)pl.chunk * BW2 * 2 * sizeof(double);
+        pl.nslices = d->ny;
+        pl.ntiles = pl.grid.x;
+        pl.nchunks = pl.grid.y;
+    } else {
+        pl.chunk = env_int("ES_CHUNK3D", 32);
+        const int64_t tx = 32LL * pl.vec;
+        pl.grid = dim3((unsigned)((d->nx + tx - 1) / tx), (unsigned)((d->ny + BY3 - 1) / BY3),
+                       (unsigned)((d->lz + pl.chunk - 1) / pl.chunk));
+        pl.block = dim3(32, BY3, 1);
+        const int tile = (BY3 + 2) * (32 * pl.vec + 4);
+        pl.smem = (2 * (size_t)tile + (size_t)pl.chunk * BY3 * 2) * sizeof(double);
+        pl.nslices = d->lz;
+        pl.ntiles = pl.grid.x * pl.grid.y;
+        pl.nchunks = pl.grid.z;
+    }
+    return pl;
+}
+
+typedef void (*ApplyFn)(const ApplyArgs);
+typedef void (*NodeFn)(const SeriesParams *);
+
+template <int VEC, int COEFF, bool GD>
+static void pick(bool dim2, ApplyFn &af, NodeFn &nf) {
+    af = dim2 ? k_apply2d<VEC, COEFF, GD> : k_apply3d<VEC, COEFF, GD>;
+    nf = dim2 ? k_node2d<VEC, COEFF, GD> : k_node3d<VEC, COEFF, GD>;
+}
+
+template <int VEC>
+static void pick_c(bool dim2, int coeff, bool gd, ApplyFn &af, NodeFn &nf) {
+    switch (coeff) {
+        case ES_COEFF_RADIAL: gd ? pick<VEC, ES_COEFF_RADIAL, true>(dim2, af, nf) : pick<VEC, ES_COEFF_RADIAL, false>(dim2, af, nf); break;
+        case ES_COEFF_ARRAY: gd ? pick<VEC, ES_COEFF_ARRAY, true>(dim2, af, nf) : pick<VEC, ES_COEFF_ARRAY, false>(dim2, af, nf); break;
+        default: gd ? pick<VEC, ES_COEFF_NONE, true>(dim2, af, nf) : pick<VEC, ES_COEFF_NONE, false>(dim2, af, nf); break;
+    }
+}
+
+static void pick_all(const StencilPlan &pl, int coeff, bool gd, ApplyFn &af, NodeFn &nf) {
+    if (pl.vec == 2) pick_c<2>(pl.dim2, coeff, gd, af, nf);
+    else pick_c<1>(pl.dim2, coeff, gd, af, nf);
+}
+
+static void set_smem_attr(const void *fn, size_t smem) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out, double alpha,
+                         double beta, const double *halo_lo, const double *halo_hi,
+                         const double *gdiag, cudaStream_t stream) {
+    if (d->nx * d->ny * d->lz == 0) return ES_OK;
+    const StencilPlan pl = plan_stencil(d, {u, out, halo_lo, halo_hi, gdiag});
+    ApplyFn af;
+    NodeFn nf;
+    pick_all(pl, d->coeff_kind, gdiag != nullptr, af, nf);
+    ApplyArgs a;
+    a.g = make_geom(d, halo_lo, halo_hi);
+    a.ps.src = u;
+    a.ps.dst = out;
+    a.ps.p_src = nullptr;
+    a.ps.p_dst = nullptr;
+    a.ps.alpha = alpha;
+    a.ps.beta = beta;
+    a.ps.dk = 0.0;
+    a.ps.d0 = 0.0;
+    a.gdiag = gdiag;
+    a.chunk_len = pl.chunk;
+    set_smem_attr((const void *)af, pl.smem);
+    af<<<pl.grid, pl.block, pl.smem, stream>>>(a);
+    return check_launch("stencil apply");
+}
+
+// ----- series workspace layout ------------------------------------------------
+
+static size_t up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct WsLayout {
+    size_t params, state, cnt, part, slice, wa, wb, pb, total;
+};
+
+static WsLayout layout(int64_t n, int nslices, int ntiles, int nchunks) {
+    WsLayout L;
+    size_t o = 0;
+    L.params = o; o = up(o + sizeof(SeriesParams));
+    L.state = o; o = up(o + sizeof(SeriesState));
+    L.cnt = o; o = up(o + sizeof(unsigned) * (nchunks + 1));
+    L.part = o; o = up(o + sizeof(double) * 2 * (size_t)nslices * ntiles);
+    L.slice = o; o = up(o + sizeof(double) * 2 * (size_t)nslices);
+    L.wa = o; o = up(o + sizeof(double) * n);
+    L.wb = o; o = up(o + sizeof(double) * n);
+    L.pb = o; o = up(o + sizeof(double) * n);
+    L.total = o;
+    return L;
+}
+
+size_t stencil_series_ws_bytes(const es_stencil_desc *d) {
+    // the scalar (VEC = 1) plan has the most tiles: size for it
+    es_stencil_desc dodd = *d;
+    dodd.nx = d->nx | 1;
+    const StencilPlan po = plan_stencil(&dodd, {});
+    return layout(d->nx * d->ny * d->lz, po.nslices, po.ntiles, po.nchunks).total;
+}
+
+// ----- the while-loop graph per (node kernel, launch shape, params slot) -----
+
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphConditionalHandle handle = 0;
+};
+
+static std::mutex g_graph_mu;
+static std::map<std::tuple<const void *, unsigned, unsigned, unsigned, size_t, const void *, int>, GraphEntry> g_graphs;
+
+static bool build_while_graph(NodeFn nf, const StencilPlan &pl, const SeriesParams *dparams, GraphEntry &e) {
+    cudaGraph_t graph = nullptr;
+    if (cudaGraphCreate(&graph, 0) != cudaSuccess) return false;
+    if (cudaGraphConditionalHandleCreate(&e.handle, graph, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return false;
+    }
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = e.handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    if (cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp) != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return false;
+    }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    void *args[] = {(void *)&dparams};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void *)nf;
+    kp.gridDim = pl.grid;
+    kp.blockDim = pl.block;
+    kp.sharedMemBytes = (unsigned)pl.smem;
+    kp.kernelParams = args;
+    cudaGraphNode_t knode;
+    if (cudaGraphAddKernelNode(&knode, body, nullptr, 0, &kp) != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return false;
+    }
+    if (cudaGraphInstantiate(&e.exec, graph, 0) != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return false;
+    }
+    cudaGraphDestroy(graph);
+    return true;
+}
+
+int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
+                       const double *xi, int ndd, double alpha, double shift, double tol,
+                       const double *gdiag, void *ws, size_t ws_bytes, es_series_result *res,
+                       cudaStream_t stream) {
+    const int64_t n = d->nx * d->ny * d->lz;
+    if (ndd < 1) return set_error(ES_ERR_ARG, "ndd must be >= 1");
+    if (ndd == 1 || n == 0) {  // degenerate interval: dd_0 v, 0 matvecs (matfunc.py:285-286)
+        if (n > 0) {
+            k_scale_dev<<<std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, stream>>>(v, dd, p_out, n);
+            int rc = check_launch("scale");
+            if (rc) return rc;
+        }
+        res->matvecs = 0;
+        res->converged = 1;
+        res->last_term = 0.0;
+        res->last_pnorm = 0.0;
+        return ES_OK;
+    }
+    char *w = static_cast<char *>(ws);
+    const StencilPlan pl = plan_stencil(d, {v, p_out, gdiag, (const void *)(w + 0)});
+    const WsLayout L = layout(n, pl.nslices, pl.ntiles, pl.nchunks);
+    if (ws_bytes < L.total) return set_error(ES_ERR_ARG, "workspace too small");
+    // VEC=2 additionally needs the scratch vectors aligned (layout is 256B aligned)
+    ApplyFn af;
+    NodeFn nf;
+    pick_all(pl, d->coeff_kind, gdiag != nullptr, af, nf);
+    set_smem_attr((const void *)nf, pl.smem);
+
+    SeriesParams hp;
+    hp.g = make_geom(d, nullptr, nullptr);
+    hp.v = v;
+    hp.wbuf[1] = reinterpret_cast<double *>(w + L.wa);
+    hp.wbuf[0] = reinterpret_cast<double *>(w + L.wb);
+    hp.pbuf[1] = p_out;
+    hp.pbuf[0] = reinterpret_cast<double *>(w + L.pb);
+    hp.gdiag = gdiag;
+    hp.dd = dd;
+    hp.xi = xi;
+    hp.ndd = ndd;
+    hp.alpha = alpha;
+    hp.shift = shift;
+    hp.tol = tol;
+    hp.state = reinterpret_cast<SeriesState *>(w + L.state);
+    hp.part = reinterpret_cast<double *>(w + L.part);
+    hp.slice = reinterpret_cast<double *>(w + L.slice);
+    hp.chunk_cnt = reinterpret_cast<unsigned *>(w + L.cnt);
+    hp.global_cnt = hp.chunk_cnt + pl.nchunks;
+    hp.nslices = pl.nslices;
+    hp.ntiles = pl.ntiles;
+    hp.nchunks = pl.nchunks;
+    hp.chunk_len = pl.chunk;
+    hp.cond = 0;
+    SeriesParams *dparams = reinterpret_cast<SeriesParams *>(w + L.params);
+
+    GraphEntry *ge = nullptr;
+    if (!env_int("ES_NO_GRAPH", 0)) {
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        auto key = std::make_tuple((const void *)nf, pl.grid.x, pl.grid.y, pl.grid.z, pl.smem, (const void *)dparams,
+                                   current_device());
+        auto it = g_graphs.find(key);
+        if (it == g_graphs.end()) {
+            GraphEntry e;
+            if (build_while_graph(nf, pl, dparams, e)) it = g_graphs.emplace(key, e).first;
+            else cudaGetLastError();
+        }
+        if (it != g_graphs.end()) ge = &it->second;
+    }
+    if (ge) hp.cond = (unsigned long long)ge->handle;
+
+    k_series_init<<<1, 256, 0, stream>>>(hp, dparams);
+    int rc = check_launch("series init");
+    if (rc) return rc;
+    if (ge) {
+        if (cudaGraphLaunch(ge->exec, stream) != cudaSuccess) return check_launch("series graph");
+    } else {
+        for (int k = 1; k < ndd; ++k) nf<<<pl.grid, pl.block, pl.smem, stream>>>(dparams);
+        rc = check_launch("series nodes");
+        if (rc) return rc;
+    }
+    k_series_finalize<<<148 * 8, 256, 0, stream>>>(dparams, n);
+    rc = check_launch("series finalize");
+    if (rc) return rc;
+    return read_series_state(hp.state, res, stream);
+}
+
+}  // namespace es

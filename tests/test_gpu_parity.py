@@ -1,0 +1,235 @@
+"""Parity of the B200 path (through the C ABI) with the reference's golden
+vectors and the CPU oracle.  Bitwise for stencil applies and Newton-Leja
+series (equal matvec counts asserted); 1e-12 relative for steps that contain
+CUDA exp(); 1e-10 over trajectories."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1309_4616_b200 as es  # noqa: E402
+from oracle import oracle as orc  # noqa: E402
+
+from conftest import coeff_d  # noqa: E402
+
+BCS = {"none": es.BoundaryCondition.none(), "homogeneous": es.BoundaryCondition.homogeneous(),
+       "neumann": es.BoundaryCondition.neumann()}
+ORC_MODE = {"none": orc.MODE_PERIODIC, "homogeneous": orc.MODE_ZERO, "neumann": orc.MODE_NEUMANN}
+
+
+def _faces_bc(i, d):
+    faces = tuple(d[f"c{i}_face{j}"] for j in range(6))
+    return es.BoundaryCondition.function(lambda x, y, z: 0.0 * x, "golden"), faces
+
+
+def test_stencil_apply_matches_reference_bitwise(golden):
+    d = golden("stencil_apply")
+    for i in range(int(d["ncases"])):
+        g = es.Grid3D(*(int(v) for v in d[f"c{i}_dims"]))
+        bc = str(d[f"c{i}_bc"])
+        coeff = coeff_d if bool(d[f"c{i}_coeff"]) else None
+        x = d[f"c{i}_x"]
+        if bc in ("poly", "trig"):
+            bcobj, faces = _faces_bc(i, d)
+            op = es.StencilOperator(g, bcobj, coeff=coeff)
+            out = torch.empty(g.n, dtype=torch.float64, device="cuda")
+            xd = torch.from_numpy(x).cuda()
+            es.fused_slab(op, 1.0, 0.0, xd.view(g.shape), out.view(g.shape), faces=faces)
+            got = out.cpu().numpy()
+        else:
+            op = es.StencilOperator(g, BCS[bc], coeff=coeff)
+            a, b = d[f"c{i}_ab"]
+            got = op.fused_apply_flat(a, b, x)
+        assert got.tobytes() == d[f"c{i}_y"].tobytes(), f"case {i} {tuple(d[f'c{i}_dims'])} {bc}"
+
+
+def test_slab_with_halos_bitwise(golden):
+    d = golden("stencil_slab")
+    for i in range(int(d["ncases"])):
+        g = es.Grid3D(*(int(v) for v in d[f"s{i}_dims"]))
+        z0, lz = (int(v) for v in d[f"s{i}_z"])
+        op = es.StencilOperator(g, es.BoundaryCondition.homogeneous(),
+                                coeff=coeff_d if bool(d[f"s{i}_coeff"]) else None)
+        x3 = torch.from_numpy(d[f"s{i}_x"]).cuda().view(g.shape)
+        lo = x3[z0 - 1].clone() if z0 > 0 else None
+        hi = x3[z0 + lz].clone() if z0 + lz < g.nz else None
+        out = torch.empty((lz, g.ny, g.nx), dtype=torch.float64, device="cuda")
+        es.fused_slab(op, 1.5, -0.25, x3[z0:z0 + lz].clone(), out, halo_lo=lo, halo_hi=hi, z0=z0)
+        assert out.cpu().numpy().reshape(-1).tobytes() == d[f"s{i}_y"].tobytes(), f"slab {i}"
+
+
+def _interp(d, i):
+    s, tol, maxdeg, a, b = d[f"n{i}_params"]
+    iv = es.SpectralInterval(a, b)
+    return es.LejaInterpolant(iv, str(d[f"n{i}_target"]), s, int(maxdeg), tol if tol > 0 else 1e-8,
+                              iv.center + iv.halfspan * d[f"n{i}_xi"], d[f"n{i}_xi"], d[f"n{i}_dd"]), tol
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_newton_series_matches_reference_bitwise(golden, graph, monkeypatch):
+    if not graph:
+        monkeypatch.setenv("ES_NO_GRAPH", "1")
+    d = golden("newton")
+    for i in range(int(d["ncases"])):
+        g = es.Grid3D(*(int(v) for v in d[f"n{i}_dims"]))
+        op = es.StencilOperator(g, BCS[str(d[f"n{i}_bc"])], coeff=coeff_d if bool(d[f"n{i}_coeff"]) else None)
+        it, tol = _interp(d, i)
+        if int(d[f"n{i}_mv"]) < 0:
+            with pytest.raises(es.ConvergenceError) as ei:
+                es.newton_apply(op, it, d[f"n{i}_v"], tol)
+            res, deg = d[f"n{i}_err"]
+            assert ei.value.degree == int(deg)
+            assert ei.value.residual == pytest.approx(res, rel=1e-9)
+            continue
+        p, mv = es.newton_apply(op, it, d[f"n{i}_v"], tol)
+        assert mv == int(d[f"n{i}_mv"]), f"case {i}"
+        assert p.tobytes() == d[f"n{i}_p"].tobytes(), f"case {i}"
+
+
+def test_newton_device_resident_matches_host(golden):
+    d = golden("newton")
+    g = es.Grid3D(*(int(v) for v in d["n1_dims"]))
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous(), coeff=coeff_d)
+    it, tol = _interp(d, 1)
+    v = torch.from_numpy(d["n1_v"]).cuda()
+    p, mv = es.newton_apply(op, it, v, tol)
+    assert isinstance(p, torch.Tensor) and p.is_cuda
+    assert p.cpu().numpy().tobytes() == d["n1_p"].tobytes()
+    assert torch.equal(v.cpu(), torch.from_numpy(d["n1_v"]))  # input untouched
+
+
+def test_expeuler_trajectories(golden):
+    d = golden("expeuler")
+    for i in range(int(d["ncases"])):
+        g = es.Grid3D(*(int(v) for v in d[f"t{i}_dims"]))
+        h, tol, nsteps = d[f"t{i}_params"]
+        op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+        obs = []
+        prob = es.SemilinearProblem(operator=op, nonlinearity=es.combustion_g, u0=d[f"t{i}_u0"])
+        u = es.integrate(prob, es.StepperConfig(h=h, t_end=h * nsteps, tol=tol),
+                         observer=lambda k, t, mv, mx: obs.append((k, t, mv, mx)))
+        ref_obs = d[f"t{i}_obs"]
+        assert [o[2] for o in obs] == [int(v) for v in ref_obs[:, 2]], f"case {i} matvecs"
+        ref = d[f"t{i}_u"]
+        assert np.max(np.abs(u - ref)) <= 1e-10 * np.max(np.abs(ref)), f"case {i}"
+        np.testing.assert_allclose([o[3] for o in obs], ref_obs[:, 3], rtol=1e-12)
+
+
+def test_rescue_halving(golden):
+    d = golden("rescue")
+    g = es.Grid3D(*(int(v) for v in d["dims"]))
+    s, tol, maxdeg = d["params"]
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    for i in range(2):
+        y, st = es.apply_matfunc(op, d[f"r{i}_v"], str(d[f"r{i}_target"]), s, tol=tol, max_degree=int(maxdeg))
+        assert [st.matvecs, st.degree, st.halvings] == [int(v) for v in d[f"r{i}_stats"]]
+        ref = d[f"r{i}_y"]
+        assert np.max(np.abs(y - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_csr_bitwise(golden):
+    d = golden("csr")
+    n = int(d["n"])
+    a = es.CsrMatrix(n, n, d["row_ptr"], d["col"], d["vals"])
+    y = a.fused_apply_flat(0.7, -1.3, d["x"])
+    assert y.tobytes() == d["y"].tobytes()
+    iv = es.gershgorin_interval(a)
+    assert (iv.a, iv.b) == tuple(d["interval"])
+    it = es.LejaInterpolant(iv, "phi1", -1.0, 150, 1e-8, iv.center + iv.halfspan * d["xi"], d["xi"], d["dd"])
+    p0, mv0 = es.newton_apply(a, it, d["x"], 0.0)
+    assert mv0 == int(d["mv0"]) and p0.tobytes() == d["p0"].tobytes()
+    p, mv = es.newton_apply(a, it, d["x"], 1e-8)
+    assert mv == int(d["mv"]) and p.tobytes() == d["p"].tobytes()
+
+
+def test_combustion_and_domain_error(golden):
+    d = golden("combustion")
+    got = es.combustion_g(d["u"])
+    np.testing.assert_allclose(got, d["g"], rtol=1e-15, atol=0)
+    with pytest.raises(es.DomainError) as ei:
+        es.combustion_g(np.array([1.0, 1.0, 2.0, 0.0, -1.0, 0.0]))
+    assert ei.value.index == 3
+
+
+@pytest.mark.parametrize("dims", [(64, 48, 1), (63, 47, 1), (40, 36, 28), (39, 17, 9), (1, 4, 6)])
+@pytest.mark.parametrize("bc", ["homogeneous", "neumann", "none"])
+@pytest.mark.parametrize("coeff", ["none", "radial", "array"])
+def test_apply_and_series_vs_oracle(dims, bc, coeff):
+    nx, ny, nz = dims
+    g = es.Grid3D(nx, ny, nz)
+    cfun = {"none": None, "radial": es.radial_coeff, "array": lambda x, y, z: 1.0 + 0.5 * x * y + 0.25 * z}[coeff]
+    op = es.StencilOperator(g, BCS[bc], coeff=cfun)
+    ck = {"none": orc.COEFF_NONE, "radial": orc.COEFF_RADIAL, "array": orc.COEFF_ARRAY}[coeff]
+    spec = orc.StencilSpec(nx, ny, nz, mode=ORC_MODE[bc], coeff_kind=ck,
+                           coeff=op.coeff_values("f64") if coeff == "array" else None)
+    rng = np.random.default_rng(hash(dims) % 1000)
+    x = rng.standard_normal(g.n)
+    assert op.fused_apply_flat(0.37, -1.25, x).tobytes() == orc.stencil_fused(spec, 0.37, -1.25, x).tobytes()
+    lo, hi = es.gershgorin_bounds(op)
+    assert (lo, hi) == spec.gershgorin()
+    iv = es.SpectralInterval(lo, hi)
+    it = es.make_interpolant(iv, "exp", -3.0 / max(hi, 1.0), 20, 1e-8)
+    p, mv = es.newton_apply(op, it, x, 0.0)
+    ref, mvr = orc.newton_stencil(spec, orc.Interp(lo, hi, "exp", it.scale, it.xi, it.dd), x, 0.0)
+    assert mv == mvr == 20
+    assert p.tobytes() == ref.tobytes()
+
+
+def test_partition_invariance_bitwise():
+    g = es.Grid3D(17, 17, 17)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    x = np.random.default_rng(3).standard_normal(g.n)
+    ref = op.fused_apply_flat(2.0, 1.0, x)
+    for m in (1, 2, 3, 4):
+        w = es.PartitionedStencil(op, es.make_partition(g, m))
+        assert w.fused_apply_flat(2.0, 1.0, x).tobytes() == ref.tobytes()
+        assert w.ledger.last_scalars() == 2 * (m - 1) * 17 * 17
+
+
+def test_rosenbrock_step_vs_oracle():
+    g = es.Grid3D(40, 36, 32)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    u0 = 1.0 + 0.1 * np.random.default_rng(11).random(g.n)
+    prob = es.SemilinearProblem(operator=op, nonlinearity=es.combustion_g, u0=u0)
+    h, tol = 2e-4, 1e-6
+    u1, st = es.exponential_rosenbrock_step(prob, u0, h, tol)
+    spec = orc.StencilSpec(40, 36, 32)
+    ref, m = orc.rosenbrock_step(spec, u0, h, tol)
+    assert st.matvecs == m
+    assert np.max(np.abs(u1 - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_large_2d_neumann_radial_series_vs_oracle():
+    # C2-shaped (4096 x 4096 Neumann + in-kernel D), fixed degree
+    g = es.Grid3D(4096, 4096, 1)
+    op = es.StencilOperator(g, es.BoundaryCondition.neumann(), coeff=es.radial_coeff)
+    lo, hi = es.gershgorin_bounds(op)
+    it = es.make_interpolant(es.SpectralInterval(lo, hi), "phi1", -6e-7, 6, 1e-8)
+    x = np.random.default_rng(1234).standard_normal(g.n)
+    p, mv = es.newton_apply(op, it, x, 0.0)
+    spec = orc.StencilSpec(4096, 4096, 1, mode=orc.MODE_NEUMANN, coeff_kind=orc.COEFF_RADIAL)
+    ref, _ = orc.newton_stencil(spec, orc.Interp(lo, hi, "phi1", -6e-7, it.xi, it.dd), x, 0.0)
+    assert mv == 6 and p.tobytes() == ref.tobytes()
+
+
+def test_large_3d_series_linearity_and_oracle():
+    # 256^3 Dirichlet: oracle parity at fixed degree, and exact linearity
+    # under power-of-two scaling (a size-independent property)
+    g = es.Grid3D(256, 256, 256)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    lo, hi = es.gershgorin_bounds(op)
+    it = es.make_interpolant(es.SpectralInterval(lo, hi), "exp", -1e-4, 5, 1e-8)
+    x = torch.randn(g.n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    p, _ = es.newton_apply(op, it, x, 0.0)
+    p4, _ = es.newton_apply(op, it, 4.0 * x, 0.0)
+    assert torch.equal(p4, 4.0 * p)
+    ref, _ = orc.newton_stencil(orc.StencilSpec(256, 256, 256), orc.Interp(lo, hi, "exp", -1e-4, it.xi, it.dd),
+                                x.cpu().numpy(), 0.0)
+    assert p.cpu().numpy().tobytes() == ref.tobytes()
