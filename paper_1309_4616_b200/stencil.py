@@ -261,7 +261,7 @@ def fused_slab(op: StencilOperator, alpha, beta, x3, out3, halo_lo=None, halo_hi
     """One slab through es_stencil_fused_slab (device tensors; the
     decomposition layer's entry point, stencil.py:207-243)."""
     kind = op.bc.kind
-    lz = int(x3.shape[0])
+    lz = int(x3.numel()) // (op.grid.nx * op.grid.ny)
     if kind == "none" and (z0 != 0 or lz != op.grid.nz):
         raise BoundaryKindError("periodic wraparound is not defined on a partitioned slab")
     if kind == "function" and faces is None:
