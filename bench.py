@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""Benchmark of the fused Leja-stencil integrator step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C2|C1|C4] [--impl b200|reference]
+
+Default workload (N=1): BASELINE.json config 3 -- 512^3 7-point stencil,
+homogeneous Dirichlet, combustion reaction term, exponential Rosenbrock-Euler
+with Leja interpolation, fp64.  One "step" = one integrator step (device
+resident state, all series, nonlinearity, Jacobian and step combination).
+
+metric: Gpts.matvec/s = grid points x Newton-Leja nodes (matvecs) / second,
+whole job.  Also reported: the fused node kernel's achieved HBM GB/s against
+MEASURED_PEAKS.json (roofline), the end-to-end number through the public API
+with host buffers (e2e), the reference CPU path on the box's cores
+(cpu_baseline), SM clocks during the timed region.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref:
+the unmodified reference package with its compiled Cython core, built by
+oracle/build_ref.sh; the plain-C oracle port if that is missing) on a bounded
+sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "Gpts·matvec/s and HBM GB/s (% of peak) for Leja-stencil step at 1/2/4/8 B200"
+UNIT = "Gpts·matvec/s"
+
+CONFIGS = {
+    "C3": dict(workload="512^3 7-point, homogeneous Dirichlet, combustion, exponential Rosenbrock-Euler + Leja",
+               dims=(512, 512, 512), bc="homogeneous", coeff=None, method="rosenbrock", h=2.5e-5, tol=1e-4,
+               bytes_per_node=40),
+    "C2": dict(workload="4096^2 5-point, homogeneous Neumann, D=1/sqrt(1+x^2+y^2) in-kernel, exp(-hA)u + Leja",
+               dims=(4096, 4096, 1), bc="neumann", coeff="radial", method="linear", h=6e-7, tol=1e-4,
+               bytes_per_node=32),
+    "C1": dict(workload="256^2 5-point, homogeneous Dirichlet, combustion, exponential Euler + Leja",
+               dims=(256, 256, 1), bc="homogeneous", coeff=None, method="euler", h=1e-4, tol=1e-4,
+               bytes_per_node=32),
+    "C4": dict(workload="1024^3 7-point, homogeneous Dirichlet, combustion, exponential Rosenbrock-Euler + Leja",
+               dims=(1024, 1024, 1024), bc="homogeneous", coeff=None, method="rosenbrock", h=6.3e-6, tol=1e-4,
+               bytes_per_node=40),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def initial_state(n: int, seed: int = 1234) -> np.ndarray:
+    """u0 = 1 + 0.1 U[0, 1) (bench.py:112-114 seeding)."""
+    return 1.0 + 0.1 * np.random.default_rng(seed).random(n)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sms, mx, reasons = [], None, set()
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        loaded = [s for s in sms if s > 0.5 * max(sms)] or sms
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path (bounded sample)
+
+
+_REF_CACHE: dict = {}
+
+
+def reference_available() -> bool:
+    return os.path.isdir(os.path.join(REPO, "oracle", "_ref", "expstencil"))
+
+
+def reference_node_sample(cfg: dict, nodes: int):
+    """Time `nodes` Newton-Leja nodes of the reference's newton_apply (its
+    StencilOperator + compiled core) on the config's grid: returns
+    (seconds, points*nodes, kind, threads, description).  The reference has
+    no Neumann / Rosenbrock / in-kernel D: the series runs on its
+    StencilOperator with the same grid (Dirichlet for Neumann, the sampled D
+    array for the radial coefficient, A instead of A - diag g'), the closest
+    cost-equivalent of the same hot loop."""
+    nx, ny, nz = cfg["dims"]
+    n = nx * ny * nz
+    key = (tuple(cfg["dims"]), cfg["coeff"], nodes)
+    if key not in _REF_CACHE:
+        _REF_CACHE.clear()
+        _REF_CACHE[key] = {"x": np.random.default_rng(1234).standard_normal(n)}
+    cache = _REF_CACHE[key]
+    x = cache["x"]
+    if reference_available():
+        sys.path.insert(0, os.path.join(REPO, "oracle", "_ref"))
+        os.environ.setdefault("EXPSTENCIL_KERNELS", "compiled")
+        import expstencil as ref
+        from expstencil import _kernels
+
+        if "op" not in cache:
+            coeff = (lambda X, Y, Z: 1.0 / np.sqrt(1.0 + X * X + Y * Y)) if cfg["coeff"] else None
+            cache["op"] = ref.StencilOperator(ref.Grid3D(nx, ny, nz), ref.BoundaryCondition.homogeneous(),
+                                              coeff=coeff)
+            cache["it"] = ref.make_interpolant(ref.gershgorin_interval(cache["op"]), "phi1", -cfg["h"], nodes,
+                                               cfg["tol"])
+        op, it = cache["op"], cache["it"]
+        t0 = time.perf_counter()
+        _, mv = ref.newton_apply(op, it, x, 0.0)
+        dt = time.perf_counter() - t0
+        kind = "reference"
+        desc = (f"reference newton_apply (expstencil {_kernels.default_backend()} core, oracle/_ref) on "
+                f"{nx}x{ny}x{nz}, fixed degree {mv} (tol=0), phi1, Dirichlet A")
+        threads = 1  # _core.pyx holds the GIL: the stencil runs on one core
+    else:
+        from oracle import oracle as orc
+
+        spec = orc.StencilSpec(nx, ny, nz, coeff_kind=orc.COEFF_RADIAL if cfg["coeff"] else 0)
+        lo, hi = spec.gershgorin()
+        it = orc.interpolant(lo, hi, "phi1", -cfg["h"], nodes)
+        t0 = time.perf_counter()
+        _, mv = orc.newton_stencil(spec, it, x, 0.0)
+        dt = time.perf_counter() - t0
+        kind, threads = "port", orc.num_threads()
+        desc = f"plain-C oracle port (OpenMP) newton series on {nx}x{ny}x{nz}, fixed degree {mv}"
+    return dt, n * mv, kind, threads, desc
+
+
+def reference_nodes_for(cfg: dict) -> int:
+    n = int(np.prod(cfg["dims"]))
+    # ~2 s per node at 512^3 on one core: keep each sample at ~10-30 s of CPU
+    return max(2, min(40, int(3e8 // max(n, 1))))
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    nodes = reference_nodes_for(cfg)
+    for _ in range(args.warmup if int(np.prod(cfg["dims"])) < 2**24 else min(args.warmup, 1)):
+        reference_node_sample(cfg, nodes)
+    times, units = [], 0
+    kind = threads = desc = None
+    for _ in range(args.steps):
+        dt, u, kind, threads, desc = reference_node_sample(cfg, nodes)
+        times.append(dt)
+        units += u
+    total = sum(times)
+    value = units / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "grid": list(cfg["dims"]), "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host_cpu_count": os.cpu_count(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def make_problem(cfg, es, u0):
+    nx, ny, nz = cfg["dims"]
+    g = es.Grid3D(nx, ny, nz)
+    bc = es.BoundaryCondition.neumann() if cfg["bc"] == "neumann" else es.BoundaryCondition.homogeneous()
+    op = es.StencilOperator(g, bc, coeff=es.radial_coeff if cfg["coeff"] == "radial" else None)
+    nl = None if cfg["method"] == "linear" else es.combustion_g
+    return es.SemilinearProblem(operator=op, nonlinearity=nl, u0=u0)
+
+
+class Stepper:
+    """One integrator step of the configured method through the public API."""
+
+    def __init__(self, cfg, es, problem):
+        self.cfg, self.es, self.problem = cfg, es, problem
+        self.h, self.tol = cfg["h"], cfg["tol"]
+        if cfg["method"] == "rosenbrock":
+            self.ros = es.RosenbrockStepper(problem, self.tol)
+        else:
+            from paper_1309_4616_b200.integrator import _StepWorkspace
+
+            self.ws = _StepWorkspace(problem, self.h, self.tol, 150)
+
+    def __call__(self, u, t):
+        if self.cfg["method"] == "rosenbrock":
+            return self.ros.step(u, t, self.h)
+        return self.ws.step(u, t)
+
+    def launches(self, stats) -> int:
+        """Kernels this step launched (counted from the code path)."""
+        m = stats.matvecs
+        if self.cfg["method"] == "rosenbrock":
+            # combustion 2, Jacobian 3, A u 1, F axpy 1, series init+nodes+finalize m+2, update 1
+            return m + 10
+        if self.cfg["method"] == "linear":
+            return m + 2
+        # exp series (m1+2), combustion 2, phi1 series (m2+2), axpy 1
+        return m + 7
+
+
+def measured_peak():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic(cfg_name: str):
+    path = os.path.join(REPO, "profiles", "node_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(cfg_name)
+    except (OSError, ValueError):
+        return None
+
+
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1309_4616_b200 as es
+    from paper_1309_4616_b200 import timing
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nx, ny, nz = cfg["dims"]
+    n = nx * ny * nz
+    u_host = initial_state(n)
+    u0 = torch.from_numpy(u_host).cuda()
+    problem = make_problem(cfg, es, u0)
+    step = Stepper(cfg, es, problem)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    u = u0.clone()
+    t = 0.0
+    for _ in range(args.warmup):
+        u, _ = step(u, t)
+        t += cfg["h"]
+    barrier()
+    # ---- device-resident timed region ----
+    matvecs, launches = 0, 0
+    with ClockSampler(local) as clocks, timing.SeriesTimer() as tm:
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            u, st = step(u, t)
+            t += cfg["h"]
+            matvecs += st.matvecs
+            launches += step.launches(st)
+        ev1.record()
+        barrier()
+    elapsed = ev0.elapsed_time(ev1) * 1e-3
+    series_s, series_mv = tm.totals()
+    t_max = elapsed
+    units = float(n) * matvecs
+    if world > 1:
+        buf = torch.tensor([elapsed, units], dtype=torch.float64, device="cuda")
+        tmax = buf[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        usum = buf[1:].clone()
+        dist.all_reduce(usum, op=dist.ReduceOp.SUM)
+        t_max, units = float(tmax.item()), float(usum.item())
+    value = units / t_max / 1e9
+
+    # roofline of the dominant kernel: the fused node (series time / nodes)
+    node_s = series_s / max(series_mv, 1)
+    bytes_node = cfg["bytes_per_node"] * n
+    achieved = bytes_node / node_s / 1e9
+    peak, peak_src = measured_peak()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": profiled_traffic(args.config), "kernel": "k_node3d/k_node2d (fused Leja node)",
+                "bytes_per_point": cfg["bytes_per_node"], "node_us": node_s * 1e6, "peak_source": peak_src,
+                "series_share_of_step": series_s / elapsed if elapsed > 0 else None}
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        pin_in = torch.from_numpy(u.cpu().numpy()).pin_memory()
+        pin_out = torch.empty_like(pin_in).pin_memory()
+        e2e_steps = max(3, args.steps // 2)
+        mv_e2e = 0
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(e2e_steps):
+            ud = pin_in.to("cuda", non_blocking=True)
+            ud, st = step(ud, t)
+            t += cfg["h"]
+            pin_out.copy_(ud, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            pin_in, pin_out = pin_out, pin_in
+            mv_e2e += st.matvecs
+        e1.record()
+        barrier()
+        e_el = e0.elapsed_time(e1) * 1e-3
+        e_units = float(n) * mv_e2e
+        if world > 1:
+            b = torch.tensor([e_el], dtype=torch.float64, device="cuda")
+            dist.all_reduce(b, op=dist.ReduceOp.MAX)
+            e_el = float(b.item())
+            e_units *= world
+        e2e = {"value": e_units / e_el / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+               "d2h_bytes_per_step": 8 * n, "steps": e2e_steps, "ms_per_step": 1e3 * e_el / e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nodes = reference_nodes_for(cfg)
+        dt, u_cpu, kind, threads, desc = reference_node_sample(cfg, nodes)
+        cpu = {"value": u_cpu / dt / 1e9, "unit": UNIT, "cores": threads, "kind": kind, "sample": desc,
+               "seconds": dt, "host_cpu_count": os.cpu_count()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: u0 = 1 + 0.1 U[0,1), numpy default_rng(1234)",
+            "config": {"workload": cfg["workload"], "config": args.config, "grid": list(cfg["dims"]),
+                       "bc": cfg["bc"], "coeff": cfg["coeff"], "method": cfg["method"], "h": cfg["h"],
+                       "tol": cfg["tol"], "parallelism": "replicas" if world > 1 else "single",
+                       "l2": f"inputs larger than L2 ({8 * n / 2**20:.0f} MiB per vector)" if 8 * n > 2**27
+                       else "working set inside L2 (no flush)"},
+            "matvecs_per_step": matvecs / args.steps, "steps_per_s": args.steps / t_max,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

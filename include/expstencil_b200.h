@@ -104,12 +104,26 @@ int es_leja_stencil(const es_stencil_desc *d, const double *v, double *p_out,
                     double tol, const double *gdiag, void *workspace, size_t workspace_bytes,
                     es_series_result *result_host, void *stream);
 
+/* Asynchronous form: enqueue the whole series (no host sync); the outcome
+ * stays in the workspace until es_leja_fetch synchronises the stream and
+ * reads it (ES_ERR_NOT_CONVERGED as above).  Lets a caller bracket the
+ * series with CUDA events or queue several series back to back. */
+int es_leja_stencil_async(const es_stencil_desc *d, const double *v, double *p_out,
+                          const double *dd, const double *xi, int32_t ndd, double alpha,
+                          double shift, double tol, const double *gdiag, void *workspace,
+                          size_t workspace_bytes, void *stream);
+int es_leja_fetch(void *workspace, es_series_result *result_host, void *stream);
+
 /* Same series for a square CSR operator (sparse.py:150-151 protocol). */
 size_t es_leja_csr_workspace_bytes(int64_t n);
 int es_leja_csr(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *vals,
                 const double *v, double *p_out, const double *dd, const double *xi,
                 int32_t ndd, double alpha, double shift, double tol, void *workspace,
                 size_t workspace_bytes, es_series_result *result_host, void *stream);
+int es_leja_csr_async(int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                      const double *vals, const double *v, double *p_out, const double *dd,
+                      const double *xi, int32_t ndd, double alpha, double shift, double tol,
+                      void *workspace, size_t workspace_bytes, void *stream);
 
 /* Integrator-stage element-wise kernels (integrator.py:177-189,
  * matfunc.py:366-371); all stream-ordered, no sync. */

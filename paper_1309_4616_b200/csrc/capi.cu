@@ -120,11 +120,22 @@ extern "C" int es_leja_stencil(const es_stencil_desc *d, const double *v, double
     if (rc) return rc;
     if (d->mode == ES_MODE_FACES)
         return set_error(ES_ERR_ARG, "fused apply needs a linear operator (faces mode)");
-    if (!v || !p_out || !dd || !xi || !result_host || (ndd > 1 && !workspace))
-        return set_error(ES_ERR_ARG, "null pointer");
+    if (!v || !p_out || !dd || !xi || !workspace) return set_error(ES_ERR_ARG, "null pointer");
     if (v == p_out) return set_error(ES_ERR_ARG, "p_out must not alias v");
     return run_stencil_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, workspace, workspace_bytes,
                               result_host, (cudaStream_t)stream);
+}
+
+extern "C" int es_leja_stencil_async(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
+                                     const double *xi, int32_t ndd, double alpha, double shift, double tol,
+                                     const double *gdiag, void *workspace, size_t workspace_bytes, void *stream) {
+    return es_leja_stencil(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, workspace, workspace_bytes,
+                           nullptr, stream);
+}
+
+extern "C" int es_leja_fetch(void *workspace, es_series_result *result_host, void *stream) {
+    if (!workspace || !result_host) return set_error(ES_ERR_ARG, "null pointer");
+    return read_series_state(series_state_ptr(workspace), result_host, (cudaStream_t)stream);
 }
 
 extern "C" size_t es_leja_csr_workspace_bytes(int64_t n) { return n < 0 ? 0 : csr_series_ws_bytes(n); }
@@ -134,9 +145,17 @@ extern "C" int es_leja_csr(int64_t n, const int64_t *row_ptr, const int32_t *col
                            double alpha, double shift, double tol, void *workspace, size_t workspace_bytes,
                            es_series_result *result_host, void *stream) {
     if (n < 0) return set_error(ES_ERR_ARG, "negative n");
-    if (!v || !p_out || !dd || !xi || !result_host || (n > 0 && (!row_ptr || !col_idx || !vals)))
+    if (!v || !p_out || !dd || !xi || !workspace || (n > 0 && (!row_ptr || !col_idx || !vals)))
         return set_error(ES_ERR_ARG, "null pointer");
     if (v == p_out) return set_error(ES_ERR_ARG, "p_out must not alias v");
     return run_csr_series(n, row_ptr, col_idx, vals, v, p_out, dd, xi, ndd, alpha, shift, tol, workspace,
                           workspace_bytes, result_host, (cudaStream_t)stream);
+}
+
+extern "C" int es_leja_csr_async(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *vals,
+                                 const double *v, double *p_out, const double *dd, const double *xi, int32_t ndd,
+                                 double alpha, double shift, double tol, void *workspace, size_t workspace_bytes,
+                                 void *stream) {
+    return es_leja_csr(n, row_ptr, col_idx, vals, v, p_out, dd, xi, ndd, alpha, shift, tol, workspace,
+                       workspace_bytes, nullptr, stream);
 }

@@ -177,17 +177,15 @@ int run_csr_series(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
                    double alpha, double shift, double tol, void *ws, size_t ws_bytes,
                    es_series_result *res, cudaStream_t stream) {
     if (ndd < 1) return set_error(ES_ERR_ARG, "ndd must be >= 1");
-    if (ndd == 1 || n == 0) {
-        if (n > 0) {
-            k_csr_scale<<<std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, stream>>>(v, dd, p_out, n);
-            int rc = check_launch("scale");
-            if (rc) return rc;
-        }
-        *res = es_series_result{0, 1, 0.0, 0.0};
-        return ES_OK;
-    }
     const CsrLayout L = csr_layout(n);
     if (ws_bytes < L.total) return set_error(ES_ERR_ARG, "workspace too small");
+    if (ndd == 1 || n == 0) {
+        if (n > 0) k_csr_scale<<<std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, stream>>>(v, dd, p_out, n);
+        launch_state_trivial(ws, stream);
+        int rc = check_launch("scale");
+        if (rc || !res) return rc;
+        return read_series_state(series_state_ptr(ws), res, stream);
+    }
     char *w = static_cast<char *>(ws);
     SeriesParams hp = {};
     hp.v = v;
@@ -226,6 +224,7 @@ int run_csr_series(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
     k_csr_finalize<<<148 * 8, 256, 0, stream>>>(dparams, n);
     rc = check_launch("csr finalize");
     if (rc) return rc;
+    if (!res) return ES_OK;
     return read_series_state(hp.state, res, stream);
 }
 

@@ -14,6 +14,8 @@ int check_launch(const char *what);
 int current_device();
 
 struct SeriesState;
+SeriesState *series_state_ptr(void *ws);
+void launch_state_trivial(void *ws, cudaStream_t stream);
 int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaStream_t stream);
 
 struct StencilPlan {

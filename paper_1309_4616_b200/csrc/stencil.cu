@@ -116,6 +116,23 @@ __global__ void k_series_finalize(const SeriesParams *__restrict__ Pp, int64_t n
         d[i] = s[i];
 }
 
+__global__ void k_state_trivial(SeriesState *st) {
+    st->k = 0;
+    st->consecutive = 0;
+    st->done = 1;
+    st->converged = 1;
+    st->last_term = 0.0;
+    st->last_pnorm = 0.0;
+}
+
+void launch_state_trivial(void *ws, cudaStream_t stream) {
+    k_state_trivial<<<1, 1, 0, stream>>>(series_state_ptr(ws));
+}
+
+SeriesState *series_state_ptr(void *ws) {
+    return reinterpret_cast<SeriesState *>(static_cast<char *>(ws) + ((sizeof(SeriesParams) + 255) & ~(size_t)255));
+}
+
 __global__ void k_scale_dev(const double *x, const double *s, double *out, int64_t n) {
     const double a = *s;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -323,22 +340,17 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
                        cudaStream_t stream) {
     const int64_t n = d->nx * d->ny * d->lz;
     if (ndd < 1) return set_error(ES_ERR_ARG, "ndd must be >= 1");
-    if (ndd == 1 || n == 0) {  // degenerate interval: dd_0 v, 0 matvecs (matfunc.py:285-286)
-        if (n > 0) {
-            k_scale_dev<<<std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, stream>>>(v, dd, p_out, n);
-            int rc = check_launch("scale");
-            if (rc) return rc;
-        }
-        res->matvecs = 0;
-        res->converged = 1;
-        res->last_term = 0.0;
-        res->last_pnorm = 0.0;
-        return ES_OK;
-    }
     char *w = static_cast<char *>(ws);
     const StencilPlan pl = plan_stencil(d, {v, p_out, gdiag, (const void *)(w + 0)});
     const WsLayout L = layout(n, pl.nslices, pl.ntiles, pl.nchunks);
     if (ws_bytes < L.total) return set_error(ES_ERR_ARG, "workspace too small");
+    if (ndd == 1 || n == 0) {  // degenerate interval: dd_0 v, 0 matvecs (matfunc.py:285-286)
+        if (n > 0) k_scale_dev<<<std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, stream>>>(v, dd, p_out, n);
+        launch_state_trivial(ws, stream);
+        int rc = check_launch("scale");
+        if (rc || !res) return rc;
+        return read_series_state(series_state_ptr(ws), res, stream);
+    }
     // VEC=2 additionally needs the scratch vectors aligned (layout is 256B aligned)
     ApplyFn af;
     NodeFn nf;
@@ -399,6 +411,7 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     k_series_finalize<<<148 * 8, 256, 0, stream>>>(dparams, n);
     rc = check_launch("series finalize");
     if (rc) return rc;
+    if (!res) return ES_OK;  // asynchronous: es_leja_fetch reads the state later
     return read_series_state(hp.state, res, stream);
 }
 

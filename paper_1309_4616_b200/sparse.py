@@ -16,7 +16,7 @@ from typing import Optional
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, timing
 from .device import Workspace, empty, is_host, like_input, ptr, stream_handle, to_device
 
 
@@ -142,12 +142,19 @@ class CsrMatrix:
         rp, col, vals = self.device_arrays()
         nbytes = lib.es_leja_csr_workspace_bytes(self.n)
         ws = self._ws.get(nbytes)
+        tm = timing.active()
+        ev0 = timing.event() if tm else None
+        rc = lib.es_leja_csr_async(self.n, ptr(rp), ptr(col), ptr(vals), ptr(v), ptr(p_out), ptr(dd), ptr(xi),
+                                   dd.numel(), float(alpha), float(shift), float(tol), ptr(ws), ws.numel(),
+                                   stream_handle())
+        _lib.check(rc, "es_leja_csr_async")
+        ev1 = timing.event() if tm else None
         res = _lib.SeriesResult()
-        rc = lib.es_leja_csr(self.n, ptr(rp), ptr(col), ptr(vals), ptr(v), ptr(p_out), ptr(dd), ptr(xi),
-                             dd.numel(), float(alpha), float(shift), float(tol), ptr(ws), ws.numel(),
-                             ctypes.byref(res), stream_handle())
+        rc = lib.es_leja_fetch(ptr(ws), ctypes.byref(res), stream_handle())
         if rc != _lib.ES_ERR_NOT_CONVERGED:
-            _lib.check(rc, "es_leja_csr")
+            _lib.check(rc, "es_leja_fetch")
+        if tm:
+            tm.add(ev0, ev1, res.matvecs)
         return res
 
     def __repr__(self):

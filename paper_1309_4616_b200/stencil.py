@@ -21,7 +21,7 @@ from typing import Callable, Optional
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, timing
 from .device import Workspace, empty, is_host, like_input, ptr, stream_handle, to_device
 from .errors import BoundaryKindError, EvaluationError, GridMismatchError
 from .grid import SCALAR_KINDS, Field, Grid3D, eval_on_grid, zeros_field
@@ -210,12 +210,19 @@ class StencilOperator:
         d, keep = self.desc()
         nbytes = lib.es_leja_stencil_workspace_bytes(ctypes.byref(d))
         ws = self._ws.get(nbytes)
+        tm = timing.active()
+        ev0 = timing.event() if tm else None
+        rc = lib.es_leja_stencil_async(ctypes.byref(d), ptr(v), ptr(p_out), ptr(dd), ptr(xi), dd.numel(),
+                                       float(alpha), float(shift), float(tol), ptr(gdiag), ptr(ws),
+                                       ws.numel(), stream_handle())
+        _lib.check(rc, "es_leja_stencil_async")
+        ev1 = timing.event() if tm else None
         res = _lib.SeriesResult()
-        rc = lib.es_leja_stencil(ctypes.byref(d), ptr(v), ptr(p_out), ptr(dd), ptr(xi), dd.numel(),
-                                 float(alpha), float(shift), float(tol), ptr(gdiag), ptr(ws),
-                                 ws.numel(), ctypes.byref(res), stream_handle())
+        rc = lib.es_leja_fetch(ptr(ws), ctypes.byref(res), stream_handle())
         if rc != _lib.ES_ERR_NOT_CONVERGED:
-            _lib.check(rc, "es_leja_stencil")
+            _lib.check(rc, "es_leja_fetch")
+        if tm:
+            tm.add(ev0, ev1, res.matvecs)
         del keep
         return res
 
