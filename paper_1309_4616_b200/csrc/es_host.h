@@ -19,6 +19,7 @@ void launch_state_trivial(void *ws, cudaStream_t stream);
 int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaStream_t stream);
 
 struct StencilPlan {
+    bool tma;  // v2 TMA-pipelined kernel (else the register-queue v1 kernel)
     bool dim2;
     int vec;
     int chunk;
@@ -27,7 +28,7 @@ struct StencilPlan {
     int nslices, ntiles, nchunks;
 };
 
-StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const void *> ptrs);
+StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const void *> ptrs, bool tma_ok);
 int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out, double alpha,
                          double beta, const double *halo_lo, const double *halo_hi,
                          const double *gdiag, cudaStream_t stream);

@@ -2,12 +2,16 @@
 // a device-side while loop), and their host launchers.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
 
 #include "es_host.h"
 #include "series.cuh"
+#include "stencil_tma.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace es {
 
@@ -87,6 +91,60 @@ __global__ void __launch_bounds__(32 * BW2) k_node2d(const SeriesParams *__restr
         dst[1] = ap;
     }
     reduce_and_decide(P, k, blockIdx.y, yb, ye);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-pipelined kernels (v2)
+
+struct ApplyArgsT {
+    Geom g;
+    Pass ps;
+    int chunk_len;
+    TmaMaps maps;  // MAP_WA_V / MAP_WB_V describe the source vector
+};
+
+template <bool DIM3, int COEFF>
+__global__ void __launch_bounds__(TMA_THREADS) k_apply_tma(const __grid_constant__ ApplyArgsT a) {
+    extern __shared__ __align__(128) char tsmem[];
+    const PassMaps mp{&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], nullptr, nullptr};
+    tma_pass<DIM3, COEFF, false, false>(a.g, a.ps, mp, a.chunk_len, false, tsmem);
+}
+
+template <bool DIM3, int COEFF, bool GD>
+__global__ void __launch_bounds__(TMA_THREADS) k_node_tma(const SeriesParams *__restrict__ Pp) {
+    extern __shared__ __align__(128) char tsmem[];
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    const int k = P.state->k + 1;
+    const Pass ps = node_pass(P, k);
+    const TmaMaps &M = *static_cast<const TmaMaps *>(P.maps);
+    const int wi = k == 1 ? 0 : 1 + ((k - 1) & 1);
+    const PassMaps mp{&M.m[2 * wi], &M.m[2 * wi + 1], &M.m[MAP_P_0 + ((k - 1) & 1)], &M.m[MAP_G]};
+    tma_pass<DIM3, COEFF, GD, true>(P.g, ps, mp, P.chunk_len, true, tsmem);
+    __syncthreads();
+    const double *s_red = reinterpret_cast<const double *>(tsmem + TLayout<DIM3>::RING + 2 * TShape<DIM3>::S * 8);
+    const int chunk = DIM3 ? blockIdx.z : blockIdx.y;
+    const int tile = DIM3 ? blockIdx.y * gridDim.x + blockIdx.x : blockIdx.x;
+    const int64_t L = DIM3 ? P.g.lz : P.g.ny;
+    const int64_t mb = (int64_t)chunk * P.chunk_len, me = min(L, mb + P.chunk_len);
+    for (int64_t ml = threadIdx.x; ml < me - mb; ml += TMA_THREADS) {
+        double aw = s_red[(ml * TMA_CONSUMER_WARPS) * 2], ap = s_red[(ml * TMA_CONSUMER_WARPS) * 2 + 1];
+        for (int w = 1; w < TMA_CONSUMER_WARPS; ++w) {
+            aw = add(aw, s_red[(ml * TMA_CONSUMER_WARPS + w) * 2]);
+            ap = add(ap, s_red[(ml * TMA_CONSUMER_WARPS + w) * 2 + 1]);
+        }
+        double *dst = P.part + ((mb + ml) * P.ntiles + tile) * 2;
+        dst[0] = aw;
+        dst[1] = ap;
+    }
+    reduce_and_decide(P, k, chunk, mb, me);
+}
+
+__global__ void k_publish_maps(const TmaMaps maps, TmaMaps *dst) {
+    if (threadIdx.x == 0) {
+        *dst = maps;
+        asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
+    }
 }
 
 // Series prologue: publish the parameters, clear the state and the tickets.
@@ -170,8 +228,14 @@ Geom make_geom(const es_stencil_desc *d, const double *halo_lo, const double *ha
 
 static bool aligned16(const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const void *> ptrs) {
+static bool use_v1() {
+    const char *s = std::getenv("ES_KERNEL");
+    return s && s[0] == 'v' && s[1] == '1';
+}
+
+StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const void *> ptrs, bool tma_ok) {
     StencilPlan pl;
+    pl.tma = false;
     pl.dim2 = d->nz_total == 1 && d->lz == 1;
     bool al = d->nx % 2 == 0;
     for (const void *p : ptrs) al = al && aligned16(p);
@@ -179,6 +243,28 @@ StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const v
         for (int i = 0; i < 6; ++i) al = al && aligned16(d->faces[i]);
     if (d->coeff_kind == ES_COEFF_ARRAY) al = al && aligned16(d->coeff);
     pl.vec = al ? 2 : 1;
+    if (tma_ok && pl.vec == 2 && d->mode != ES_MODE_FACES && !use_v1() && d->nx < (1 << 30) && d->ny < (1 << 30) &&
+        d->lz < (1 << 30)) {
+        pl.tma = true;
+        pl.block = dim3(TMA_THREADS, 1, 1);
+        if (pl.dim2) {
+            pl.chunk = env_int("ES_TCHUNK2D", 64);
+            pl.grid = dim3((unsigned)((d->nx + 511) / 512), (unsigned)((d->ny + pl.chunk - 1) / pl.chunk), 1);
+            pl.smem = tma_smem_bytes<false>(pl.chunk);
+            pl.nslices = d->ny;
+            pl.ntiles = pl.grid.x;
+            pl.nchunks = pl.grid.y;
+        } else {
+            pl.chunk = env_int("ES_TCHUNK3D", 32);
+            pl.grid = dim3((unsigned)((d->nx + 63) / 64), (unsigned)((d->ny + 7) / 8),
+                           (unsigned)((d->lz + pl.chunk - 1) / pl.chunk));
+            pl.smem = tma_smem_bytes<true>(pl.chunk);
+            pl.nslices = d->lz;
+            pl.ntiles = pl.grid.x * pl.grid.y;
+            pl.nchunks = pl.grid.z;
+        }
+        return pl;
+    }
     if (pl.dim2) {
         pl.chunk = env_int("ES_CHUNK2D", 16);
         const int64_t strip = 32LL * pl.vec * BW2;
@@ -230,24 +316,124 @@ static void set_smem_attr(const void *fn, size_t smem) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+// ----- tensor maps -------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2 };
+
+// TMA descriptor of a slab-shaped fp64 vector (x fastest); OOB reads are
+// zero-filled, which is the homogeneous Dirichlet ghost rule.
+static int encode_map(CUtensorMap *m, const double *base, const es_stencil_desc *d, bool dim2, MapKind kind) {
+    std::memset(m, 0, sizeof(*m));
+    if (!base) return ES_OK;
+    auto fn = encode_fn();
+    if (!fn) return set_error(ES_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+    cuuint64_t dims[3], strides[2];
+    cuuint32_t box[3], estr[3] = {1, 1, 1};
+    cuuint32_t rank;
+    if (dim2) {
+        rank = 2;
+        dims[0] = (cuuint64_t)d->nx;
+        dims[1] = (cuuint64_t)d->ny;
+        strides[0] = (cuuint64_t)d->nx * 8;
+        box[0] = kind == MK_WTAIL ? 4 : 256;
+        box[1] = 1;
+    } else {
+        rank = 3;
+        dims[0] = (cuuint64_t)d->nx;
+        dims[1] = (cuuint64_t)d->ny;
+        dims[2] = (cuuint64_t)d->lz;
+        strides[0] = (cuuint64_t)d->nx * 8;
+        strides[1] = (cuuint64_t)d->nx * d->ny * 8;
+        box[0] = kind == MK_P ? 64 : 68;
+        box[1] = kind == MK_P ? 8 : 10;
+        box[2] = 1;
+    }
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double *>(base), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(ES_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return ES_OK;
+}
+
+static int encode_w(CUtensorMap *wa, CUtensorMap *wb, const double *base, const es_stencil_desc *d, bool dim2) {
+    int rc = encode_map(wa, base, d, dim2, MK_W);
+    if (rc) return rc;
+    return encode_map(wb, base, d, dim2, dim2 ? MK_WTAIL : MK_W);
+}
+
+typedef void (*ApplyTmaFn)(const ApplyArgsT);
+typedef void (*NodeTmaFn)(const SeriesParams *);
+
+template <bool DIM3>
+static ApplyTmaFn pick_apply_tma(int coeff) {
+    switch (coeff) {
+        case ES_COEFF_RADIAL: return k_apply_tma<DIM3, ES_COEFF_RADIAL>;
+        case ES_COEFF_ARRAY: return k_apply_tma<DIM3, ES_COEFF_ARRAY>;
+        default: return k_apply_tma<DIM3, ES_COEFF_NONE>;
+    }
+}
+
+template <bool DIM3, bool GD>
+static NodeTmaFn pick_node_tma_c(int coeff) {
+    switch (coeff) {
+        case ES_COEFF_RADIAL: return k_node_tma<DIM3, ES_COEFF_RADIAL, GD>;
+        case ES_COEFF_ARRAY: return k_node_tma<DIM3, ES_COEFF_ARRAY, GD>;
+        default: return k_node_tma<DIM3, ES_COEFF_NONE, GD>;
+    }
+}
+
+static NodeTmaFn pick_node_tma(bool dim2, int coeff, bool gd) {
+    if (dim2) return gd ? pick_node_tma_c<false, true>(coeff) : pick_node_tma_c<false, false>(coeff);
+    return gd ? pick_node_tma_c<true, true>(coeff) : pick_node_tma_c<true, false>(coeff);
+}
+
 int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out, double alpha,
                          double beta, const double *halo_lo, const double *halo_hi,
                          const double *gdiag, cudaStream_t stream) {
     if (d->nx * d->ny * d->lz == 0) return ES_OK;
-    const StencilPlan pl = plan_stencil(d, {u, out, halo_lo, halo_hi, gdiag});
+    const bool plain = !halo_lo && !halo_hi && !gdiag;
+    const StencilPlan pl = plan_stencil(d, {u, out, halo_lo, halo_hi, gdiag}, plain);
+    Pass ps;
+    ps.src = u;
+    ps.dst = out;
+    ps.p_src = nullptr;
+    ps.p_dst = nullptr;
+    ps.alpha = alpha;
+    ps.beta = beta;
+    ps.dk = 0.0;
+    ps.d0 = 0.0;
+    if (pl.tma) {
+        ApplyArgsT a;
+        a.g = make_geom(d, nullptr, nullptr);
+        a.ps = ps;
+        a.chunk_len = pl.chunk;
+        std::memset(&a.maps, 0, sizeof(a.maps));
+        int rc = encode_w(&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], u, d, pl.dim2);
+        if (rc) return rc;
+        const ApplyTmaFn fn = pl.dim2 ? pick_apply_tma<false>(d->coeff_kind) : pick_apply_tma<true>(d->coeff_kind);
+        set_smem_attr((const void *)fn, pl.smem);
+        fn<<<pl.grid, pl.block, pl.smem, stream>>>(a);
+        return check_launch("stencil apply (tma)");
+    }
     ApplyFn af;
     NodeFn nf;
     pick_all(pl, d->coeff_kind, gdiag != nullptr, af, nf);
     ApplyArgs a;
     a.g = make_geom(d, halo_lo, halo_hi);
-    a.ps.src = u;
-    a.ps.dst = out;
-    a.ps.p_src = nullptr;
-    a.ps.p_dst = nullptr;
-    a.ps.alpha = alpha;
-    a.ps.beta = beta;
-    a.ps.dk = 0.0;
-    a.ps.d0 = 0.0;
+    a.ps = ps;
     a.gdiag = gdiag;
     a.chunk_len = pl.chunk;
     set_smem_attr((const void *)af, pl.smem);
@@ -260,7 +446,7 @@ int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out,
 static size_t up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WsLayout {
-    size_t params, state, cnt, part, slice, wa, wb, pb, total;
+    size_t params, state, maps, cnt, part, slice, wa, wb, pb, total;
 };
 
 static WsLayout layout(int64_t n, int nslices, int ntiles, int nchunks) {
@@ -268,6 +454,7 @@ static WsLayout layout(int64_t n, int nslices, int ntiles, int nchunks) {
     size_t o = 0;
     L.params = o; o = up(o + sizeof(SeriesParams));
     L.state = o; o = up(o + sizeof(SeriesState));
+    L.maps = o; o = up(o + sizeof(TmaMaps));
     L.cnt = o; o = up(o + sizeof(unsigned) * (nchunks + 1));
     L.part = o; o = up(o + sizeof(double) * 2 * (size_t)nslices * ntiles);
     L.slice = o; o = up(o + sizeof(double) * 2 * (size_t)nslices);
@@ -280,10 +467,14 @@ static WsLayout layout(int64_t n, int nslices, int ntiles, int nchunks) {
 
 size_t stencil_series_ws_bytes(const es_stencil_desc *d) {
     // the scalar (VEC = 1) plan has the most tiles: size for it
+    // the larger of the scalar v1 plan (most tiles) and the TMA plan
     es_stencil_desc dodd = *d;
     dodd.nx = d->nx | 1;
-    const StencilPlan po = plan_stencil(&dodd, {});
-    return layout(d->nx * d->ny * d->lz, po.nslices, po.ntiles, po.nchunks).total;
+    const StencilPlan po = plan_stencil(&dodd, {}, false);
+    const StencilPlan pt = plan_stencil(d, {}, true);
+    const int64_t n = d->nx * d->ny * d->lz;
+    return std::max(layout(n, po.nslices, po.ntiles, po.nchunks).total,
+                    layout(n, pt.nslices, pt.ntiles, pt.nchunks).total);
 }
 
 // ----- the while-loop graph per (node kernel, launch shape, params slot) -----
@@ -341,7 +532,7 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     const int64_t n = d->nx * d->ny * d->lz;
     if (ndd < 1) return set_error(ES_ERR_ARG, "ndd must be >= 1");
     char *w = static_cast<char *>(ws);
-    const StencilPlan pl = plan_stencil(d, {v, p_out, gdiag, (const void *)(w + 0)});
+    const StencilPlan pl = plan_stencil(d, {v, p_out, gdiag, (const void *)(w + 0)}, true);
     const WsLayout L = layout(n, pl.nslices, pl.ntiles, pl.nchunks);
     if (ws_bytes < L.total) return set_error(ES_ERR_ARG, "workspace too small");
     if (ndd == 1 || n == 0) {  // degenerate interval: dd_0 v, 0 matvecs (matfunc.py:285-286)
@@ -354,10 +545,14 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     // VEC=2 additionally needs the scratch vectors aligned (layout is 256B aligned)
     ApplyFn af;
     NodeFn nf;
-    pick_all(pl, d->coeff_kind, gdiag != nullptr, af, nf);
+    if (pl.tma) {
+        nf = pick_node_tma(pl.dim2, d->coeff_kind, gdiag != nullptr);
+    } else {
+        pick_all(pl, d->coeff_kind, gdiag != nullptr, af, nf);
+    }
     set_smem_attr((const void *)nf, pl.smem);
 
-    SeriesParams hp;
+    SeriesParams hp = {};
     hp.g = make_geom(d, nullptr, nullptr);
     hp.v = v;
     hp.wbuf[1] = reinterpret_cast<double *>(w + L.wa);
@@ -381,7 +576,22 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     hp.nchunks = pl.nchunks;
     hp.chunk_len = pl.chunk;
     hp.cond = 0;
+    hp.maps = nullptr;
     SeriesParams *dparams = reinterpret_cast<SeriesParams *>(w + L.params);
+    if (pl.tma) {
+        TmaMaps maps;
+        std::memset(&maps, 0, sizeof(maps));
+        int rc = encode_w(&maps.m[MAP_WA_V], &maps.m[MAP_WB_V], v, d, pl.dim2);
+        if (!rc) rc = encode_w(&maps.m[MAP_WA_0], &maps.m[MAP_WB_0], hp.wbuf[0], d, pl.dim2);
+        if (!rc) rc = encode_w(&maps.m[MAP_WA_1], &maps.m[MAP_WB_1], hp.wbuf[1], d, pl.dim2);
+        if (!rc) rc = encode_map(&maps.m[MAP_P_0], hp.pbuf[0], d, pl.dim2, MK_P);
+        if (!rc) rc = encode_map(&maps.m[MAP_P_1], hp.pbuf[1], d, pl.dim2, MK_P);
+        if (!rc) rc = encode_map(&maps.m[MAP_G], gdiag, d, pl.dim2, MK_P);
+        if (rc) return rc;
+        TmaMaps *dmaps = reinterpret_cast<TmaMaps *>(w + L.maps);
+        k_publish_maps<<<1, 32, 0, stream>>>(maps, dmaps);
+        hp.maps = dmaps;
+    }
 
     GraphEntry *ge = nullptr;
     if (!env_int("ES_NO_GRAPH", 0)) {

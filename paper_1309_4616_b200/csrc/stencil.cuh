@@ -55,6 +55,7 @@ struct SeriesParams {
     const int32_t *col;
     const double *vals;
     int64_t n;
+    const void *maps;  // TmaMaps (workspace) for the TMA node kernel
 };
 
 // One pass: what a node (or a plain fused apply) reads and writes.

@@ -158,10 +158,14 @@ def test_combustion_and_domain_error(golden):
     assert ei.value.index == 3
 
 
-@pytest.mark.parametrize("dims", [(64, 48, 1), (63, 47, 1), (40, 36, 28), (39, 17, 9), (1, 4, 6)])
+@pytest.mark.parametrize("dims", [(64, 48, 1), (63, 47, 1), (40, 36, 28), (39, 17, 9), (1, 4, 6), (1030, 5, 1),
+                                  (130, 20, 19)])
 @pytest.mark.parametrize("bc", ["homogeneous", "neumann", "none"])
 @pytest.mark.parametrize("coeff", ["none", "radial", "array"])
-def test_apply_and_series_vs_oracle(dims, bc, coeff):
+@pytest.mark.parametrize("kernel", ["tma", "v1"])
+def test_apply_and_series_vs_oracle(dims, bc, coeff, kernel, monkeypatch):
+    if kernel == "v1":
+        monkeypatch.setenv("ES_KERNEL", "v1")
     nx, ny, nz = dims
     g = es.Grid3D(nx, ny, nz)
     cfun = {"none": None, "radial": es.radial_coeff, "array": lambda x, y, z: 1.0 + 0.5 * x * y + 0.25 * z}[coeff]
@@ -193,7 +197,10 @@ def test_partition_invariance_bitwise():
         assert w.ledger.last_scalars() == 2 * (m - 1) * 17 * 17
 
 
-def test_rosenbrock_step_vs_oracle():
+@pytest.mark.parametrize("kernel", ["tma", "v1"])
+def test_rosenbrock_step_vs_oracle(kernel, monkeypatch):
+    if kernel == "v1":
+        monkeypatch.setenv("ES_KERNEL", "v1")
     g = es.Grid3D(40, 36, 32)
     op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
     u0 = 1.0 + 0.1 * np.random.default_rng(11).random(g.n)
