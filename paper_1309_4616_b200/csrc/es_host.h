@@ -26,6 +26,7 @@ struct StencilPlan {
     dim3 grid, block;
     size_t smem;
     int nslices, ntiles, nchunks;
+    int64_t items;  // TMA: (chunk, tile) work items
 };
 
 StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const void *> ptrs, bool tma_ok);

@@ -10,19 +10,66 @@
 
 namespace es {
 
-// Returns true in the (single) CTA that made the decision.
-ES_DEV bool reduce_and_decide(const SeriesParams &P, int k, int chunk, int64_t slice_b,
-                              int64_t slice_e) {
+// Barrier over the participating threads: the whole CTA (NT == 0) or the
+// first NT threads via named barrier 1 (warp-specialised kernels, where the
+// producer warp is busy elsewhere).
+template <int NT>
+ES_DEV void group_sync() {
+    if constexpr (NT == 0) {
+        __syncthreads();
+    } else {
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    }
+}
+
+// The stopping test of matfunc.py:302-311 on the reduced sums (one thread).
+ES_DEV void decide(const SeriesParams &P, int k, double sumw, double sump) {
+    SeriesState &st = *P.state;
+    const double dk = P.dd[k];
+    const double term = mul(fabs(dk), sqrt_rn(sumw));
+    const double pn = sqrt_rn(sump);
+    st.k = k;
+    st.last_term = term;
+    st.last_pnorm = pn;
+    bool stop = false;
+    if (P.tol > 0.0) {
+        if (term <= mul(P.tol, pn)) {
+            st.consecutive += 1;
+            if (st.consecutive >= 2) {
+                stop = true;
+                st.converged = 1;
+            }
+        } else {
+            st.consecutive = 0;
+        }
+    }
+    if (!stop && k >= P.ndd - 1) {
+        stop = true;
+        st.converged = P.tol == 0.0 ? 1 : 0;
+    }
+    if (stop) {
+        st.done = 1;
+        if (P.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)P.cond, 0);
+    }
+}
+
+// Returns true in the (single) CTA that made the decision.  Called by every
+// thread of the group after the group's partials for this (chunk, tile) are
+// in P.part.
+template <int NT = 0>
+ES_DEV bool reduce_and_decide(const SeriesParams &P, int k, int chunk, int64_t slice_b, int64_t slice_e) {
     __shared__ int s_last;
-    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
-    const int nthr = blockDim.x * blockDim.y;
+    const int tid = NT ? (int)threadIdx.x : (int)(threadIdx.x + threadIdx.y * blockDim.x);
+    const int nthr = NT ? NT : (int)(blockDim.x * blockDim.y);
     const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
 
     __threadfence();
-    __syncthreads();
+    group_sync<NT>();
     if (tid == 0) s_last = atomicAdd(&P.chunk_cnt[chunk], 1u) == (unsigned)P.ntiles - 1u;
-    __syncthreads();
-    if (!s_last) return false;
+    group_sync<NT>();
+    const bool last_chunk_tile = s_last;
+    group_sync<NT>();  // s_last is reused below
+    if (!last_chunk_tile) return false;
     __threadfence();
 
     // chunk reducer: slice sums over tiles (lane-strided, then xor tree)
@@ -41,10 +88,12 @@ ES_DEV bool reduce_and_decide(const SeriesParams &P, int k, int chunk, int64_t s
         }
     }
     __threadfence();
-    __syncthreads();
+    group_sync<NT>();
     if (tid == 0) s_last = atomicAdd(P.global_cnt, 1u) == (unsigned)P.nchunks - 1u;
-    __syncthreads();
-    if (!s_last) return false;
+    group_sync<NT>();
+    const bool last_chunk = s_last;
+    group_sync<NT>();
+    if (!last_chunk) return false;
     __threadfence();
 
     if (warp == 0) {
@@ -55,40 +104,61 @@ ES_DEV bool reduce_and_decide(const SeriesParams &P, int k, int chunk, int64_t s
         }
         aw = warp_sum(aw);
         ap = warp_sum(ap);
-        if (lane == 0) {
-            SeriesState &st = *P.state;
-            const double dk = P.dd[k];
-            const double term = mul(fabs(dk), sqrt_rn(aw));
-            const double pn = sqrt_rn(ap);
-            st.k = k;
-            st.last_term = term;
-            st.last_pnorm = pn;
-            bool stop = false;
-            if (P.tol > 0.0) {
-                if (term <= mul(P.tol, pn)) {
-                    st.consecutive += 1;
-                    if (st.consecutive >= 2) {
-                        stop = true;
-                        st.converged = 1;
-                    }
-                } else {
-                    st.consecutive = 0;
-                }
-            }
-            if (!stop && k >= P.ndd - 1) {
-                stop = true;
-                st.converged = P.tol == 0.0 ? 1 : 0;
-            }
-            if (stop) {
-                st.done = 1;
-                if (P.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)P.cond, 0);
-            }
-        }
+        if (lane == 0) decide(P, k, aw, ap);
     }
     // re-arm the tickets for the next node
     for (int i = tid; i < P.nchunks; i += nthr) P.chunk_cnt[i] = 0u;
     if (tid == 0) *P.global_cnt = 0u;
     return true;
+}
+
+// Separate reduction step of the TMA node (one CTA per slice = z-chunk):
+// slice c's entries (tile, warp partials) are summed thread-strided, warp
+// trees, warps in order; the last CTA sums the slices in order and decides.
+ES_DEV void slice_reduce_decide(const SeriesParams &P, int k) {
+    __shared__ double s_w[32], s_p[32];
+    __shared__ int s_last;
+    const int c = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+    const double *row = P.part + (int64_t)c * P.ntiles * 2;
+    double aw = 0.0, ap = 0.0;
+    for (int e = t; e < P.ntiles; e += blockDim.x) {
+        aw = add(aw, __ldcg(row + 2 * e));
+        ap = add(ap, __ldcg(row + 2 * e + 1));
+    }
+    aw = warp_sum(aw);
+    ap = warp_sum(ap);
+    if (lane == 0) {
+        s_w[warp] = aw;
+        s_p[warp] = ap;
+    }
+    __syncthreads();
+    if (t == 0) {
+        double a = s_w[0], b = s_p[0];
+        for (int w = 1; w < nw; ++w) {
+            a = add(a, s_w[w]);
+            b = add(b, s_p[w]);
+        }
+        P.slice[2 * c] = a;
+        P.slice[2 * c + 1] = b;
+        __threadfence();
+        s_last = atomicAdd(P.global_cnt, 1u) == gridDim.x - 1u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp == 0) {
+        double sw = 0.0, sp = 0.0;
+        for (int64_t s = lane; s < P.nslices; s += 32) {
+            sw = add(sw, __ldcg(P.slice + 2 * s));
+            sp = add(sp, __ldcg(P.slice + 2 * s + 1));
+        }
+        sw = warp_sum(sw);
+        sp = warp_sum(sp);
+        if (lane == 0) {
+            decide(P, k, sw, sp);
+            *P.global_cnt = 0u;
+        }
+    }
 }
 
 // Node k's pass description from the device state (k = last completed + 1).

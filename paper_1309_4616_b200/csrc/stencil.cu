@@ -104,14 +104,15 @@ struct ApplyArgsT {
 };
 
 template <bool DIM3, int COEFF>
-__global__ void __launch_bounds__(TMA_THREADS) k_apply_tma(const __grid_constant__ ApplyArgsT a) {
+__global__ void __launch_bounds__(TMA_THREADS, 3) k_apply_tma(const __grid_constant__ ApplyArgsT a) {
     extern __shared__ __align__(128) char tsmem[];
     const PassMaps mp{&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], nullptr, nullptr};
-    tma_pass<DIM3, COEFF, false, false>(a.g, a.ps, mp, a.chunk_len, false, tsmem);
+    tma_pass<DIM3, COEFF, false, false>(a.g, a.ps, mp, a.chunk_len, false, tsmem, nullptr, 0, nullptr);
 }
 
+// One Newton-Leja node, persistent CTAs over (chunk, tile) items.
 template <bool DIM3, int COEFF, bool GD>
-__global__ void __launch_bounds__(TMA_THREADS) k_node_tma(const SeriesParams *__restrict__ Pp) {
+__global__ void __launch_bounds__(TMA_THREADS, 3) k_node_tma(const SeriesParams *__restrict__ Pp) {
     extern __shared__ __align__(128) char tsmem[];
     const SeriesParams &P = *Pp;
     if (P.state->done) return;
@@ -120,24 +121,15 @@ __global__ void __launch_bounds__(TMA_THREADS) k_node_tma(const SeriesParams *__
     const TmaMaps &M = *static_cast<const TmaMaps *>(P.maps);
     const int wi = k == 1 ? 0 : 1 + ((k - 1) & 1);
     const PassMaps mp{&M.m[2 * wi], &M.m[2 * wi + 1], &M.m[MAP_P_0 + ((k - 1) & 1)], &M.m[MAP_G]};
-    tma_pass<DIM3, COEFF, GD, true>(P.g, ps, mp, P.chunk_len, true, tsmem);
-    __syncthreads();
-    const double *s_red = reinterpret_cast<const double *>(tsmem + TLayout<DIM3>::RING + 2 * TShape<DIM3>::S * 8);
-    const int chunk = DIM3 ? blockIdx.z : blockIdx.y;
-    const int tile = DIM3 ? blockIdx.y * gridDim.x + blockIdx.x : blockIdx.x;
-    const int64_t L = DIM3 ? P.g.lz : P.g.ny;
-    const int64_t mb = (int64_t)chunk * P.chunk_len, me = min(L, mb + P.chunk_len);
-    for (int64_t ml = threadIdx.x; ml < me - mb; ml += TMA_THREADS) {
-        double aw = s_red[(ml * TMA_CONSUMER_WARPS) * 2], ap = s_red[(ml * TMA_CONSUMER_WARPS) * 2 + 1];
-        for (int w = 1; w < TMA_CONSUMER_WARPS; ++w) {
-            aw = add(aw, s_red[(ml * TMA_CONSUMER_WARPS + w) * 2]);
-            ap = add(ap, s_red[(ml * TMA_CONSUMER_WARPS + w) * 2 + 1]);
-        }
-        double *dst = P.part + ((mb + ml) * P.ntiles + tile) * 2;
-        dst[0] = aw;
-        dst[1] = ap;
-    }
-    reduce_and_decide(P, k, chunk, mb, me);
+    tma_pass<DIM3, COEFF, GD, true>(P.g, ps, mp, P.chunk_len, true, tsmem, Pp, k, P.work);
+}
+
+// Reduction + stopping decision of a TMA node (one CTA per z / row chunk).
+__global__ void __launch_bounds__(256) k_slice_reduce(const SeriesParams *__restrict__ Pp) {
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && P.work) *P.work = 0u;  // every node CTA has finished claiming
+    slice_reduce_decide(P, P.state->k + 1);
 }
 
 __global__ void k_publish_maps(const TmaMaps maps, TmaMaps *dst) {
@@ -159,6 +151,7 @@ __global__ void k_series_init(const SeriesParams p, SeriesParams *dst) {
         st.last_term = __longlong_as_double(0x7ff0000000000000ll);  // +inf
         st.last_pnorm = 0.0;
         *p.global_cnt = 0u;
+        if (p.work) *p.work = 0u;
     }
     for (int i = threadIdx.x; i < p.nchunks; i += blockDim.x) p.chunk_cnt[i] = 0u;
 }
@@ -228,6 +221,16 @@ Geom make_geom(const es_stencil_desc *d, const double *halo_lo, const double *ha
 
 static bool aligned16(const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
 static bool use_v1() {
     const char *s = std::getenv("ES_KERNEL");
     return s && s[0] == 'v' && s[1] == '1';
@@ -248,20 +251,26 @@ StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const v
         pl.tma = true;
         pl.block = dim3(TMA_THREADS, 1, 1);
         if (pl.dim2) {
-            pl.chunk = env_int("ES_TCHUNK2D", 64);
+            // one wave: tiles_x * nchunks <= SMs * 3 resident CTAs
+            const int64_t tiles_x = (d->nx + 511) / 512;
+            const int64_t slots = (int64_t)sm_count() * 3;
+            const int64_t per = std::max<int64_t>(1, slots / tiles_x);
+            pl.chunk = env_int("ES_TCHUNK2D", (int)std::max<int64_t>(4, (d->ny + per - 1) / per));
             pl.grid = dim3((unsigned)((d->nx + 511) / 512), (unsigned)((d->ny + pl.chunk - 1) / pl.chunk), 1);
-            pl.smem = tma_smem_bytes<false>(pl.chunk);
-            pl.nslices = d->ny;
-            pl.ntiles = pl.grid.x;
+            pl.smem = 0;  // set by the launcher (depends on the kernel variant)
             pl.nchunks = pl.grid.y;
+            pl.items = (int64_t)pl.grid.x * pl.nchunks;
+            pl.nslices = pl.nchunks;                       // slices = row chunks
+            pl.ntiles = pl.grid.x * TMA_CONSUMER_WARPS;    // entries per slice
         } else {
-            pl.chunk = env_int("ES_TCHUNK3D", 32);
+            pl.chunk = env_int("ES_TCHUNK3D", 8);
             pl.grid = dim3((unsigned)((d->nx + 63) / 64), (unsigned)((d->ny + 7) / 8),
                            (unsigned)((d->lz + pl.chunk - 1) / pl.chunk));
-            pl.smem = tma_smem_bytes<true>(pl.chunk);
-            pl.nslices = d->lz;
-            pl.ntiles = pl.grid.x * pl.grid.y;
+            pl.smem = 0;
             pl.nchunks = pl.grid.z;
+            pl.items = (int64_t)pl.grid.x * pl.grid.y * pl.nchunks;
+            pl.nslices = pl.nchunks;                                // slices = z chunks
+            pl.ntiles = pl.grid.x * pl.grid.y * TMA_CONSUMER_WARPS;  // entries per slice
         }
         return pl;
     }
@@ -374,6 +383,24 @@ static int encode_w(CUtensorMap *wa, CUtensorMap *wb, const double *base, const 
     return encode_map(wb, base, d, dim2, dim2 ? MK_WTAIL : MK_W);
 }
 
+// persistent grid: every resident CTA slot, at most one per item
+static void finish_tma_plan(StencilPlan &pl, const void *fn, size_t smem) {
+    pl.smem = smem;
+    set_smem_attr(fn, smem);
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, TMA_THREADS, smem) != cudaSuccess || nb < 1) {
+        cudaGetLastError();
+        nb = 1;
+    }
+    const int64_t items = pl.items;
+    pl.grid = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nb * sm_count())), 1, 1);
+}
+
+static size_t node_smem(bool dim2, bool gd, int chunk) {
+    if (dim2) return gd ? tma_smem_bytes<false, true, true>(chunk) : tma_smem_bytes<false, true, false>(chunk);
+    return gd ? tma_smem_bytes<true, true, true>(chunk) : tma_smem_bytes<true, true, false>(chunk);
+}
+
 typedef void (*ApplyTmaFn)(const ApplyArgsT);
 typedef void (*NodeTmaFn)(const SeriesParams *);
 
@@ -424,8 +451,10 @@ int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out,
         int rc = encode_w(&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], u, d, pl.dim2);
         if (rc) return rc;
         const ApplyTmaFn fn = pl.dim2 ? pick_apply_tma<false>(d->coeff_kind) : pick_apply_tma<true>(d->coeff_kind);
-        set_smem_attr((const void *)fn, pl.smem);
-        fn<<<pl.grid, pl.block, pl.smem, stream>>>(a);
+        StencilPlan lp = pl;
+        finish_tma_plan(lp, (const void *)fn,
+                        pl.dim2 ? tma_smem_bytes<false, false, false>(pl.chunk) : tma_smem_bytes<true, false, false>(pl.chunk));
+        fn<<<lp.grid, lp.block, lp.smem, stream>>>(a);
         return check_launch("stencil apply (tma)");
     }
     ApplyFn af;
@@ -455,7 +484,7 @@ static WsLayout layout(int64_t n, int nslices, int ntiles, int nchunks) {
     L.params = o; o = up(o + sizeof(SeriesParams));
     L.state = o; o = up(o + sizeof(SeriesState));
     L.maps = o; o = up(o + sizeof(TmaMaps));
-    L.cnt = o; o = up(o + sizeof(unsigned) * (nchunks + 1));
+    L.cnt = o; o = up(o + sizeof(unsigned) * (nchunks + 2));
     L.part = o; o = up(o + sizeof(double) * 2 * (size_t)nslices * ntiles);
     L.slice = o; o = up(o + sizeof(double) * 2 * (size_t)nslices);
     L.wa = o; o = up(o + sizeof(double) * n);
@@ -487,7 +516,8 @@ struct GraphEntry {
 static std::mutex g_graph_mu;
 static std::map<std::tuple<const void *, unsigned, unsigned, unsigned, size_t, const void *, int>, GraphEntry> g_graphs;
 
-static bool build_while_graph(NodeFn nf, const StencilPlan &pl, const SeriesParams *dparams, GraphEntry &e) {
+static bool build_while_graph(NodeFn nf, const StencilPlan &pl, const SeriesParams *dparams, GraphEntry &e,
+                              NodeFn rf = nullptr, unsigned rgrid = 0) {
     cudaGraph_t graph = nullptr;
     if (cudaGraphCreate(&graph, 0) != cudaSuccess) return false;
     if (cudaGraphConditionalHandleCreate(&e.handle, graph, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
@@ -517,6 +547,19 @@ static bool build_while_graph(NodeFn nf, const StencilPlan &pl, const SeriesPara
         cudaGraphDestroy(graph);
         return false;
     }
+    if (rf) {
+        cudaKernelNodeParams rp = {};
+        rp.func = (void *)rf;
+        rp.gridDim = dim3(rgrid, 1, 1);
+        rp.blockDim = dim3(256, 1, 1);
+        rp.sharedMemBytes = 0;
+        rp.kernelParams = args;
+        cudaGraphNode_t rnode;
+        if (cudaGraphAddKernelNode(&rnode, body, &knode, 1, &rp) != cudaSuccess) {
+            cudaGraphDestroy(graph);
+            return false;
+        }
+    }
     if (cudaGraphInstantiate(&e.exec, graph, 0) != cudaSuccess) {
         cudaGraphDestroy(graph);
         return false;
@@ -545,12 +588,14 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     // VEC=2 additionally needs the scratch vectors aligned (layout is 256B aligned)
     ApplyFn af;
     NodeFn nf;
+    StencilPlan lp = pl;
     if (pl.tma) {
         nf = pick_node_tma(pl.dim2, d->coeff_kind, gdiag != nullptr);
+        finish_tma_plan(lp, (const void *)nf, node_smem(pl.dim2, gdiag != nullptr, pl.chunk));
     } else {
         pick_all(pl, d->coeff_kind, gdiag != nullptr, af, nf);
+        set_smem_attr((const void *)nf, pl.smem);
     }
-    set_smem_attr((const void *)nf, pl.smem);
 
     SeriesParams hp = {};
     hp.g = make_geom(d, nullptr, nullptr);
@@ -571,6 +616,7 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     hp.slice = reinterpret_cast<double *>(w + L.slice);
     hp.chunk_cnt = reinterpret_cast<unsigned *>(w + L.cnt);
     hp.global_cnt = hp.chunk_cnt + pl.nchunks;
+    hp.work = pl.tma ? hp.global_cnt + 1 : nullptr;
     hp.nslices = pl.nslices;
     hp.ntiles = pl.ntiles;
     hp.nchunks = pl.nchunks;
@@ -596,12 +642,14 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     GraphEntry *ge = nullptr;
     if (!env_int("ES_NO_GRAPH", 0)) {
         std::lock_guard<std::mutex> lk(g_graph_mu);
-        auto key = std::make_tuple((const void *)nf, pl.grid.x, pl.grid.y, pl.grid.z, pl.smem, (const void *)dparams,
+        auto key = std::make_tuple((const void *)nf, lp.grid.x, lp.grid.y, lp.grid.z, lp.smem, (const void *)dparams,
                                    current_device());
         auto it = g_graphs.find(key);
         if (it == g_graphs.end()) {
             GraphEntry e;
-            if (build_while_graph(nf, pl, dparams, e)) it = g_graphs.emplace(key, e).first;
+            const bool ok = pl.tma ? build_while_graph(nf, lp, dparams, e, k_slice_reduce, (unsigned)pl.nslices)
+                                   : build_while_graph(nf, lp, dparams, e);
+            if (ok) it = g_graphs.emplace(key, e).first;
             else cudaGetLastError();
         }
         if (it != g_graphs.end()) ge = &it->second;
@@ -614,7 +662,10 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     if (ge) {
         if (cudaGraphLaunch(ge->exec, stream) != cudaSuccess) return check_launch("series graph");
     } else {
-        for (int k = 1; k < ndd; ++k) nf<<<pl.grid, pl.block, pl.smem, stream>>>(dparams);
+        for (int k = 1; k < ndd; ++k) {
+            nf<<<lp.grid, lp.block, lp.smem, stream>>>(dparams);
+            if (pl.tma) k_slice_reduce<<<(unsigned)pl.nslices, 256, 0, stream>>>(dparams);
+        }
         rc = check_launch("series nodes");
         if (rc) return rc;
     }

@@ -56,6 +56,7 @@ struct SeriesParams {
     const double *vals;
     int64_t n;
     const void *maps;  // TmaMaps (workspace) for the TMA node kernel
+    unsigned *work;    // dynamic work-item counter of the TMA node kernel
 };
 
 // One pass: what a node (or a plain fused apply) reads and writes.

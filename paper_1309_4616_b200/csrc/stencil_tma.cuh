@@ -20,7 +20,7 @@
 
 #include <cuda.h>
 
-#include "stencil.cuh"
+#include "series.cuh"
 
 namespace es {
 
@@ -29,12 +29,10 @@ struct TShape;
 template <>
 struct TShape<true> {
     static constexpr int TX = 64, TY = 8, WR = TY + 2, WROW = TX + 4, PR = TY;
-    static constexpr int S = 5;  // ring stages
 };
 template <>
 struct TShape<false> {
     static constexpr int TX = 512, TY = 1, WR = 1, WROW = TX + 4, PR = 1;
-    static constexpr int S = 6;
 };
 
 constexpr int TMA_CONSUMER_WARPS = 8;
@@ -48,16 +46,24 @@ struct alignas(64) TmaMaps {
     CUtensorMap m[MAP_COUNT];
 };
 
-template <bool DIM3>
+// Two rings: W (the w_{k-1} stencil tiles; a plane stays resident while it is
+// the zm / c / zp of three consecutive outputs) and PG (p_{k-1} and g' tiles,
+// one output each).  Depths are chosen so three CTAs fit an SM and each ring
+// keeps ~3 stages of prefetch in flight.
+template <bool DIM3, bool PG, bool GD>
 struct TLayout {
     using T = TShape<DIM3>;
+    static constexpr int SW = DIM3 ? 6 : 8;
+    static constexpr int SP = PG ? (GD ? 4 : 6) : 0;
     static constexpr int W_BYTES = T::WR * T::WROW * 8;
+    static constexpr int W_STAGE = (W_BYTES + 127) & ~127;
     static constexpr int P_BYTES = T::PR * T::TX * 8;
-    static constexpr int W_OFF = 0;
-    static constexpr int P_OFF = (W_BYTES + 127) & ~127;
-    static constexpr int G_OFF = P_OFF + P_BYTES;
-    static constexpr int STAGE = G_OFF + P_BYTES;  // 128-byte multiple
-    static constexpr int RING = STAGE * T::S;
+    static constexpr int PG_STAGE = (GD ? 2 : 1) * P_BYTES;
+    static constexpr int W_RING = SW * W_STAGE;
+    static constexpr int PG_RING = SP * PG_STAGE;
+    static constexpr int BAR_OFF = W_RING + PG_RING;
+    static constexpr int ITEMQ_OFF = BAR_OFF + 2 * (SW + SP) * 8;  // int per W stage
+    static constexpr int RED_OFF = ITEMQ_OFF + ((SW * 4 + 15) & ~15);
 };
 
 // ----- PTX helpers ----------------------------------------------------------
@@ -120,199 +126,292 @@ struct PassMaps {
     const CUtensorMap *wa, *wb, *p, *g;
 };
 
-// The CTA's march range [mb, me) over its chunk and its tile origin.
-template <bool DIM3>
-struct TileIdx {
-    int x0, y0, mb, me, L;
+// Work items: (chunk, tile), chunk-major so all CTAs sweep the planes
+// together (neighbour tiles' halo rows stay L2 resident); CTAs are
+// persistent and take items round-robin, and their rings run continuously
+// across items (no pipeline refill per item).
+struct Items {
+    int tiles_x, ntiles, nchunks, chunk_len, L;
 };
 
 template <bool DIM3>
-ES_DEV TileIdx<DIM3> tile_of(const Geom &g, int chunk_len) {
+ES_DEV Items items_of(const Geom &g, int chunk_len) {
     using T = TShape<DIM3>;
-    TileIdx<DIM3> ti;
-    ti.x0 = blockIdx.x * T::TX;
-    ti.y0 = DIM3 ? blockIdx.y * T::TY : 0;
-    ti.L = DIM3 ? (int)g.lz : (int)g.ny;
-    const int chunk = DIM3 ? blockIdx.z : blockIdx.y;
-    ti.mb = chunk * chunk_len;
-    ti.me = min(ti.L, ti.mb + chunk_len);
-    return ti;
+    Items it;
+    it.tiles_x = (int)((g.nx + T::TX - 1) / T::TX);
+    it.ntiles = DIM3 ? it.tiles_x * (int)((g.ny + T::TY - 1) / T::TY) : it.tiles_x;
+    it.L = DIM3 ? (int)g.lz : (int)g.ny;
+    it.chunk_len = chunk_len;
+    it.nchunks = (it.L + chunk_len - 1) / chunk_len;
+    return it;
 }
 
-// Producer (one elected lane of warp 8): stream W for indices mb-1 .. me and
-// P/G for mb .. me-1 through the ring.
-template <bool DIM3, bool HAS_P, bool HAS_G>
-ES_DEV void tma_produce(const Geom &g, const TileIdx<DIM3> &ti, const PassMaps &mp, char *ring, uint64_t *full,
-                        uint64_t *empty, bool p_present) {
+struct Item {
+    int chunk, tile, x0, y0, mb, me;
+};
+
+template <bool DIM3>
+ES_DEV Item item_at(const Items &its, int i) {
     using T = TShape<DIM3>;
-    using Lt = TLayout<DIM3>;
-    const int jb = ti.mb - 1;
-    for (int j = jb; j <= ti.me; ++j) {
-        const int u = j - jb;
-        const int s = u % T::S;
-        if (u >= T::S) mbar_wait(&empty[s], ((u / T::S) - 1) & 1);
-        char *st = ring + s * Lt::STAGE;
-        const bool inner = j >= ti.mb && j < ti.me;
-        const bool lp = HAS_P && inner && p_present;
-        const bool lg = HAS_G && inner;
-        mbar_expect_tx(&full[s], Lt::W_BYTES + (lp ? Lt::P_BYTES : 0) + (lg ? Lt::P_BYTES : 0));
-        const int js = march_src<DIM3>(g, j, ti.L);
-        if constexpr (DIM3) {
-            tma_load(st + Lt::W_OFF, mp.wa, &full[s], ti.x0 - 2, ti.y0 - 1, js);
-            if (lp) tma_load(st + Lt::P_OFF, mp.p, &full[s], ti.x0, ti.y0, j);
-            if (lg) tma_load(st + Lt::G_OFF, mp.g, &full[s], ti.x0, ti.y0, j);
-        } else {
-            tma_load(st + Lt::W_OFF, mp.wa, &full[s], ti.x0 - 2, js);
-            tma_load(st + Lt::W_OFF + 2048, mp.wa, &full[s], ti.x0 + 254, js);
-            tma_load(st + Lt::W_OFF + 4096, mp.wb, &full[s], ti.x0 + 510, js);
-            if (lp) {
-                tma_load(st + Lt::P_OFF, mp.p, &full[s], ti.x0, j);
-                tma_load(st + Lt::P_OFF + 2048, mp.p, &full[s], ti.x0 + 256, j);
+    Item r;
+    r.chunk = i / its.ntiles;
+    r.tile = i % its.ntiles;
+    r.x0 = (r.tile % its.tiles_x) * T::TX;
+    r.y0 = DIM3 ? (r.tile / its.tiles_x) * T::TY : 0;
+    r.mb = r.chunk * its.chunk_len;
+    r.me = min(its.L, r.mb + its.chunk_len);
+    return r;
+}
+
+// Producer (one lane of warp 8).  Items are claimed from a global counter
+// (work != nullptr: the concurrently processed items form one contiguous
+// index window, so neighbour tiles' halo rows are still in L2) or taken
+// round-robin; the item index travels to the consumers in a per-stage slot
+// published by the stage's mbarrier.  A -1 slot ends the consumers' loop.
+template <bool DIM3, bool PG, bool GD>
+ES_DEV void tma_produce(const Geom &g, const Items &its, const PassMaps &mp, char *smem, bool load_p,
+                        unsigned *work) {
+    using Lt = TLayout<DIM3, PG, GD>;
+    uint64_t *wfull = reinterpret_cast<uint64_t *>(smem + Lt::BAR_OFF);
+    uint64_t *wempty = wfull + Lt::SW;
+    uint64_t *pfull = wempty + Lt::SW;
+    uint64_t *pempty = pfull + Lt::SP;
+    volatile int *itemq = reinterpret_cast<volatile int *>(smem + Lt::ITEMQ_OFF);
+    const bool use_pg = PG && (load_p || GD);
+    uint32_t uw = 0, up = 0;
+    const int total = its.ntiles * its.nchunks;
+    int i = work ? (int)atomicAdd(work, 1u) : (int)blockIdx.x;
+    while (i < total) {
+        const Item it = item_at<DIM3>(its, i);
+        int inext = -1;
+        for (int j = it.mb - 1; j <= it.me; ++j, ++uw) {
+            // claim the next item a few planes before this one ends: the
+            // atomic's latency hides behind the ring, and a CTA never holds
+            // more than the item it is about to start
+            if (j == max(it.mb - 1, it.me - 3)) inext = work ? (int)atomicAdd(work, 1u) : i + (int)gridDim.x;
+            const uint32_t s = uw % Lt::SW;
+            if (uw >= (uint32_t)Lt::SW) mbar_wait(&wempty[s], ((uw / Lt::SW) - 1) & 1);
+            char *st = smem + s * Lt::W_STAGE;
+            itemq[s] = i;
+            mbar_expect_tx(&wfull[s], Lt::W_BYTES);
+            const int js = march_src<DIM3>(g, j, its.L);
+            if constexpr (DIM3) {
+                tma_load(st, mp.wa, &wfull[s], it.x0 - 2, it.y0 - 1, js);
+            } else {
+                tma_load(st, mp.wa, &wfull[s], it.x0 - 2, js);
+                tma_load(st + 2048, mp.wa, &wfull[s], it.x0 + 254, js);
+                tma_load(st + 4096, mp.wb, &wfull[s], it.x0 + 510, js);
             }
-            if (lg) {
-                tma_load(st + Lt::G_OFF, mp.g, &full[s], ti.x0, j);
-                tma_load(st + Lt::G_OFF + 2048, mp.g, &full[s], ti.x0 + 256, j);
+            // P/G of plane j-1 follow one W plane behind (the consumer needs
+            // them together with W(j), its zp)
+            const int jp = j - 1;
+            if constexpr (PG) {
+                if (use_pg && jp >= it.mb && jp < it.me) {
+                    const uint32_t sp = up % Lt::SP;
+                    if (up >= (uint32_t)Lt::SP) mbar_wait(&pempty[sp], ((up / Lt::SP) - 1) & 1);
+                    char *pst = smem + Lt::W_RING + sp * Lt::PG_STAGE;
+                    mbar_expect_tx(&pfull[sp], (load_p ? Lt::P_BYTES : 0) + (GD ? Lt::P_BYTES : 0));
+                    if constexpr (DIM3) {
+                        if (load_p) tma_load(pst, mp.p, &pfull[sp], it.x0, it.y0, jp);
+                        if (GD) tma_load(pst + Lt::P_BYTES, mp.g, &pfull[sp], it.x0, it.y0, jp);
+                    } else {
+                        if (load_p) {
+                            tma_load(pst, mp.p, &pfull[sp], it.x0, jp);
+                            tma_load(pst + 2048, mp.p, &pfull[sp], it.x0 + 256, jp);
+                        }
+                        if (GD) {
+                            tma_load(pst + Lt::P_BYTES, mp.g, &pfull[sp], it.x0, jp);
+                            tma_load(pst + Lt::P_BYTES + 2048, mp.g, &pfull[sp], it.x0 + 256, jp);
+                        }
+                    }
+                    ++up;
+                }
             }
         }
+        i = inext;
     }
+    // end-of-work marker in the next W slot
+    const uint32_t s = uw % Lt::SW;
+    if (uw >= (uint32_t)Lt::SW) mbar_wait(&wempty[s], ((uw / Lt::SW) - 1) & 1);
+    itemq[s] = -1;
+    mbar_arrive(&wfull[s]);
 }
 
-// Consumers (warps 0..7): one point pair per thread per stage.
-template <bool DIM3, int COEFF, bool GD, bool LEJA>
-ES_DEV void tma_consume(const Geom &g, const Pass &ps, const TileIdx<DIM3> &ti, const char *ring, uint64_t *full,
-                        uint64_t *empty, double *s_red) {
+// Consumers (warps 0..7): one point pair per thread per plane.  After each
+// item they write its per-plane partial sums (LEJA) and run the reduction
+// tickets among themselves (named barrier 1).
+template <bool DIM3, int COEFF, bool GD, bool LEJA, bool PG>
+ES_DEV void tma_consume(const Geom &g, const Pass &ps, const Items &its, char *smem,
+                        const SeriesParams *P, int k) {
     using T = TShape<DIM3>;
-    using Lt = TLayout<DIM3>;
+    using Lt = TLayout<DIM3, PG, GD>;
+    uint64_t *wfull = reinterpret_cast<uint64_t *>(smem + Lt::BAR_OFF);
+    uint64_t *wempty = wfull + Lt::SW;
+    uint64_t *pfull = wempty + Lt::SW;
+    uint64_t *pempty = pfull + Lt::SP;
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
     const int q = t % (T::TX / 2), r = t / (T::TX / 2);
-    const int64_t ix = ti.x0 + 2 * q;
-    const int64_t iy = DIM3 ? (int64_t)ti.y0 + r : 0;
-    const bool act = ix < g.nx && iy < g.ny;
     const int64_t plane = g.nx * g.ny;
-    const int wrow = DIM3 ? r + 1 : 0;      // W row of this thread's points
-    const int wcol = wrow * T::WROW + 2 + 2 * q;
+    const int wcol = (DIM3 ? r + 1 : 0) * T::WROW + 2 + 2 * q;
     const int pidx = r * T::TX + 2 * q;
-    const int jb = ti.mb - 1;
+    const bool use_pg = PG && (ps.p_src != nullptr || GD);
+    const volatile int *itemq = reinterpret_cast<const volatile int *>(smem + Lt::ITEMQ_OFF);
+    uint32_t uw = 0, up = 0;
 
-    double dco[2] = {1.0, 1.0};
-    double ox2[2] = {1.0, 1.0};
-    if constexpr (COEFF == ES_COEFF_RADIAL) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const double x = axis_coord(ix + j, g.nx);
-            ox2[j] = add(1.0, mul(x, x));
-        }
-        if (DIM3 && act) {
-            const double y = axis_coord(iy, g.ny);
-            dco[0] = radial_from_sq(ox2[0], y);
-            dco[1] = radial_from_sq(ox2[1], y);
-        }
-    }
+    auto wst = [&](uint32_t u) { return reinterpret_cast<const double *>(smem + (u % Lt::SW) * Lt::W_STAGE); };
+    auto wwait = [&](uint32_t u) { mbar_wait(&wfull[u % Lt::SW], (u / Lt::SW) & 1); };
+    auto wrelease = [&](uint32_t u) {  // one elected arrival per consumer warp
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wempty[u % Lt::SW]);
+    };
 
-    auto stage = [&](int j) { return ring + ((j - jb) % T::S) * Lt::STAGE; };
-    auto wait_full = [&](int j) { mbar_wait(&full[(j - jb) % T::S], ((j - jb) / T::S) & 1); };
-
-    wait_full(jb);
-    wait_full(ti.mb);
-    for (int m = ti.mb; m < ti.me; ++m) {
-        wait_full(m + 1);
-        const double *Wm = reinterpret_cast<const double *>(stage(m - 1) + Lt::W_OFF);
-        const double *Wc = reinterpret_cast<const double *>(stage(m) + Lt::W_OFF);
-        const double *Wp = reinterpret_cast<const double *>(stage(m + 1) + Lt::W_OFF);
-        double sw = 0.0, sp = 0.0;
-        if (act) {
-            const double2 c = *reinterpret_cast<const double2 *>(Wc + wcol);
-            double xm0 = Wc[wcol - 1], xp1 = Wc[wcol + 2];
-            double2 ym, yp, zm, zp;
-            if constexpr (DIM3) {
-                ym = *reinterpret_cast<const double2 *>(Wc + wcol - T::WROW);
-                yp = *reinterpret_cast<const double2 *>(Wc + wcol + T::WROW);
-                zm = *reinterpret_cast<const double2 *>(Wm + wcol);
-                zp = *reinterpret_cast<const double2 *>(Wp + wcol);
-            } else {
-                ym = *reinterpret_cast<const double2 *>(Wm + wcol);
-                yp = *reinterpret_cast<const double2 *>(Wp + wcol);
-                zm = make_double2(0.0, 0.0);
-                zp = zm;
-            }
-            const int64_t row_base = DIM3 ? ((int64_t)m * plane + iy * g.nx) : (int64_t)m * g.nx;
-            if (g.mode != ES_MODE_ZERO) {  // in-plane ghosts the zero fill got wrong
-                const bool neu = g.mode == ES_MODE_NEUMANN;
-                if (ix == 0) xm0 = neu ? c.x : __ldg(ps.src + row_base + g.nx - 1);
-                if (ix + 2 == g.nx) xp1 = neu ? c.y : __ldg(ps.src + row_base);
-                if constexpr (DIM3) {
-                    if (iy == 0) ym = neu ? c : *reinterpret_cast<const double2 *>(ps.src + m * plane + (g.ny - 1) * g.nx + ix);
-                    if (iy == g.ny - 1) yp = neu ? c : *reinterpret_cast<const double2 *>(ps.src + m * plane + ix);
-                } else {
-                    zm = c;  // single-plane grid: z ghosts are the point itself
-                    zp = c;
-                }
-            }
-            const double cc[2] = {c.x, c.y};
-            const double xm[2] = {xm0, c.x}, xp[2] = {c.y, xp1};
-            const double ymv[2] = {ym.x, ym.y}, ypv[2] = {yp.x, yp.y};
-            const double zmv[2] = {zm.x, zm.y}, zpv[2] = {zp.x, zp.y};
-            const double *Pc = reinterpret_cast<const double *>(stage(m) + Lt::P_OFF);
-            const double *Gc = reinterpret_cast<const double *>(stage(m) + Lt::G_OFF);
-            double yy = 0.0;
-            if constexpr (COEFF == ES_COEFF_RADIAL && !DIM3) yy = axis_coord(m, g.ny);
-            double wn[2], pn[2];
+    for (;;) {
+        wwait(uw);
+        const int i = itemq[uw % Lt::SW];
+        if (i < 0) break;
+        const Item it = item_at<DIM3>(its, i);
+        const int64_t ix = it.x0 + 2 * q;
+        const int64_t iy = DIM3 ? (int64_t)it.y0 + r : 0;
+        const bool act = ix < g.nx && iy < g.ny;
+        double ox2[2] = {1.0, 1.0}, dco[2] = {1.0, 1.0};
+        if constexpr (COEFF == ES_COEFF_RADIAL) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                double lap = lap7(cc[j], xm[j], xp[j], ymv[j], ypv[j], zmv[j], zpv[j], g.wx, g.wy, g.wz);
-                const int64_t idx = row_base + ix + j;
-                if constexpr (COEFF == ES_COEFF_RADIAL) lap = mul(DIM3 ? dco[j] : radial_from_sq(ox2[j], yy), lap);
-                if constexpr (COEFF == ES_COEFF_ARRAY) lap = mul(__ldg(g.coeff + idx), lap);
-                if constexpr (GD) lap = sub(lap, mul(Gc[pidx + j], cc[j]));
-                wn[j] = add(mul(ps.alpha, lap), mul(ps.beta, cc[j]));
-                if constexpr (LEJA) {
-                    const double pold = ps.p_src ? Pc[pidx + j] : mul(ps.d0, cc[j]);
-                    pn[j] = add(pold, mul(ps.dk, wn[j]));
+                const double x = axis_coord(ix + j, g.nx);
+                ox2[j] = add(1.0, mul(x, x));
+            }
+            if (DIM3 && act) {
+                const double y = axis_coord(iy, g.ny);
+                dco[0] = radial_from_sq(ox2[0], y);
+                dco[1] = radial_from_sq(ox2[1], y);
+            }
+        }
+        const uint32_t u0 = uw;  // W counter of plane mb-1
+        double acc_w = 0.0, acc_p = 0.0;  // this thread's sums over the item's planes
+        wwait(u0 + 1);
+        for (int m = it.mb; m < it.me; ++m) {
+            const uint32_t um = u0 + (uint32_t)(m - it.mb);  // plane m-1
+            wwait(um + 2);
+            const double *Wm = wst(um), *Wc = wst(um + 1), *Wp = wst(um + 2);
+            const double *Pc = nullptr;
+            if constexpr (PG) {
+                if (use_pg) {
+                    mbar_wait(&pfull[up % Lt::SP], (up / Lt::SP) & 1);
+                    Pc = reinterpret_cast<const double *>(smem + Lt::W_RING + (up % Lt::SP) * Lt::PG_STAGE);
                 }
             }
-            const int64_t o = row_base + ix;
-            *reinterpret_cast<double2 *>(ps.dst + o) = make_double2(wn[0], wn[1]);
-            if constexpr (LEJA) {
-                *reinterpret_cast<double2 *>(ps.p_dst + o) = make_double2(pn[0], pn[1]);
-                sw = add(mul(wn[0], wn[0]), mul(wn[1], wn[1]));
-                sp = add(mul(pn[0], pn[0]), mul(pn[1], pn[1]));
+            if (act) {
+                const double2 c = *reinterpret_cast<const double2 *>(Wc + wcol);
+                double xm0 = Wc[wcol - 1], xp1 = Wc[wcol + 2];
+                double2 ym, yp, zm, zp;
+                if constexpr (DIM3) {
+                    ym = *reinterpret_cast<const double2 *>(Wc + wcol - T::WROW);
+                    yp = *reinterpret_cast<const double2 *>(Wc + wcol + T::WROW);
+                    zm = *reinterpret_cast<const double2 *>(Wm + wcol);
+                    zp = *reinterpret_cast<const double2 *>(Wp + wcol);
+                } else {
+                    ym = *reinterpret_cast<const double2 *>(Wm + wcol);
+                    yp = *reinterpret_cast<const double2 *>(Wp + wcol);
+                    zm = make_double2(0.0, 0.0);
+                    zp = zm;
+                }
+                const int64_t row_base = DIM3 ? ((int64_t)m * plane + iy * g.nx) : (int64_t)m * g.nx;
+                if (g.mode != ES_MODE_ZERO) {  // in-plane ghosts the zero fill got wrong
+                    const bool neu = g.mode == ES_MODE_NEUMANN;
+                    if (ix == 0) xm0 = neu ? c.x : __ldg(ps.src + row_base + g.nx - 1);
+                    if (ix + 2 == g.nx) xp1 = neu ? c.y : __ldg(ps.src + row_base);
+                    if constexpr (DIM3) {
+                        if (iy == 0)
+                            ym = neu ? c : *reinterpret_cast<const double2 *>(ps.src + m * plane + (g.ny - 1) * g.nx + ix);
+                        if (iy == g.ny - 1) yp = neu ? c : *reinterpret_cast<const double2 *>(ps.src + m * plane + ix);
+                    } else {
+                        zm = c;  // single-plane grid: z ghosts are the point itself
+                        zp = c;
+                    }
+                }
+                const double cc[2] = {c.x, c.y};
+                const double xm[2] = {xm0, c.x}, xp[2] = {c.y, xp1};
+                const double ymv[2] = {ym.x, ym.y}, ypv[2] = {yp.x, yp.y};
+                const double zmv[2] = {zm.x, zm.y}, zpv[2] = {zp.x, zp.y};
+                double yy = 0.0;
+                if constexpr (COEFF == ES_COEFF_RADIAL && !DIM3) yy = axis_coord(m, g.ny);
+                double2 pv = make_double2(0.0, 0.0), gv = make_double2(0.0, 0.0);
+                if constexpr (LEJA) {
+                    if (ps.p_src) pv = *reinterpret_cast<const double2 *>(Pc + pidx);
+                }
+                if constexpr (GD) gv = *reinterpret_cast<const double2 *>(Pc + Lt::P_BYTES / 8 + pidx);
+                const double pvv[2] = {pv.x, pv.y}, gvv[2] = {gv.x, gv.y};
+                double wn[2], pn[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    double lap = lap7(cc[j], xm[j], xp[j], ymv[j], ypv[j], zmv[j], zpv[j], g.wx, g.wy, g.wz);
+                    if constexpr (COEFF == ES_COEFF_RADIAL) lap = mul(DIM3 ? dco[j] : radial_from_sq(ox2[j], yy), lap);
+                    if constexpr (COEFF == ES_COEFF_ARRAY) lap = mul(__ldg(g.coeff + row_base + ix + j), lap);
+                    if constexpr (GD) lap = sub(lap, mul(gvv[j], cc[j]));
+                    wn[j] = add(mul(ps.alpha, lap), mul(ps.beta, cc[j]));
+                    if constexpr (LEJA) {
+                        const double pold = ps.p_src ? pvv[j] : mul(ps.d0, cc[j]);
+                        pn[j] = add(pold, mul(ps.dk, wn[j]));
+                    }
+                }
+                const int64_t o = row_base + ix;
+                *reinterpret_cast<double2 *>(ps.dst + o) = make_double2(wn[0], wn[1]);
+                if constexpr (LEJA) {
+                    *reinterpret_cast<double2 *>(ps.p_dst + o) = make_double2(pn[0], pn[1]);
+                    acc_w = add(acc_w, add(mul(wn[0], wn[0]), mul(wn[1], wn[1])));
+                    acc_p = add(acc_p, add(mul(pn[0], pn[0]), mul(pn[1], pn[1])));
+                }
+            }
+            wrelease(um);
+            if constexpr (PG) {
+                if (use_pg) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&pempty[up % Lt::SP]);
+                    ++up;
+                }
             }
         }
+        const uint32_t L = (uint32_t)(it.me - it.mb);
+        wrelease(u0 + L);      // planes me-1 and me
+        wrelease(u0 + L + 1);
+        uw = u0 + L + 2;
         if constexpr (LEJA) {
-            sw = warp_sum(sw);
-            sp = warp_sum(sp);
+            // (chunk, tile, warp) partial: lane-sequential over the item's
+            // planes, then the warp's xor tree; reduced by k_slice_reduce
+            acc_w = warp_sum(acc_w);
+            acc_p = warp_sum(acc_p);
             if (lane == 0) {
-                s_red[((m - ti.mb) * TMA_CONSUMER_WARPS + warp) * 2 + 0] = sw;
-                s_red[((m - ti.mb) * TMA_CONSUMER_WARPS + warp) * 2 + 1] = sp;
+                double *dst = P->part + (((int64_t)it.chunk * its.ntiles + it.tile) * TMA_CONSUMER_WARPS + warp) * 2;
+                dst[0] = acc_w;
+                dst[1] = acc_p;
             }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[(m - 1 - jb) % T::S]);
     }
 }
 
-// Shared-memory footprint of one CTA: ring + barriers + per-index warp partials.
-template <bool DIM3>
-constexpr size_t tma_smem_bytes(int chunk_len) {
-    return (size_t)TLayout<DIM3>::RING + 2 * TShape<DIM3>::S * sizeof(uint64_t) +
-           (size_t)chunk_len * TMA_CONSUMER_WARPS * 2 * sizeof(double);
+// Shared-memory footprint of one CTA.
+template <bool DIM3, bool PG, bool GD>
+constexpr size_t tma_smem_bytes(int) {
+    return (size_t)TLayout<DIM3, PG, GD>::RED_OFF;
 }
 
-// Whole pass for one CTA: barrier set-up, warp-specialised streaming.
+// Whole pass for one persistent CTA: barrier set-up, warp-specialised streaming.
 template <bool DIM3, int COEFF, bool GD, bool LEJA>
 ES_DEV void tma_pass(const Geom &g, const Pass &ps, const PassMaps &mp, int chunk_len, bool acquire_maps,
-                     char *smem) {
-    using T = TShape<DIM3>;
-    char *ring = smem;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + TLayout<DIM3>::RING);
-    uint64_t *empty = full + T::S;
-    double *s_red = reinterpret_cast<double *>(empty + T::S);
-    const TileIdx<DIM3> ti = tile_of<DIM3>(g, chunk_len);
+                     char *smem, const SeriesParams *P, int k, unsigned *work) {
+    constexpr bool PG = LEJA || GD;
+    using Lt = TLayout<DIM3, PG, GD>;
+    const Items its = items_of<DIM3>(g, chunk_len);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < T::S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], TMA_CONSUMER_WARPS);
+        uint64_t *bars = reinterpret_cast<uint64_t *>(smem + Lt::BAR_OFF);
+        for (int s = 0; s < Lt::SW; ++s) {
+            mbar_init(&bars[s], 1);
+            mbar_init(&bars[Lt::SW + s], TMA_CONSUMER_WARPS);
+        }
+        for (int s = 0; s < Lt::SP; ++s) {
+            mbar_init(&bars[2 * Lt::SW + s], 1);
+            mbar_init(&bars[2 * Lt::SW + Lt::SP + s], TMA_CONSUMER_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -326,10 +425,10 @@ ES_DEV void tma_pass(const Geom &g, const Pass &ps, const PassMaps &mp, int chun
                 if (LEJA && ps.p_src) tma_acquire(mp.p);
                 if (GD) tma_acquire(mp.g);
             }
-            tma_produce<DIM3, LEJA, GD>(g, ti, mp, ring, full, empty, ps.p_src != nullptr);
+            tma_produce<DIM3, PG, GD>(g, its, mp, smem, LEJA && ps.p_src != nullptr, work);
         }
     } else {
-        tma_consume<DIM3, COEFF, GD, LEJA>(g, ps, ti, ring, full, empty, s_red);
+        tma_consume<DIM3, COEFF, GD, LEJA, PG>(g, ps, its, smem, P, k);
     }
 }
 
