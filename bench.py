@@ -259,15 +259,18 @@ class Stepper:
         return self.ws.step(u, t)
 
     def launches(self, stats) -> int:
-        """Kernels this step launched (counted from the code path)."""
+        """Kernels this step launched (counted from the code path).
+        A TMA series = publish maps + init + (node + slice reduce) per node + finalize."""
         m = stats.matvecs
+        series = 2 * m + 3
         if self.cfg["method"] == "rosenbrock":
-            # combustion 2, Jacobian 3, A u 1, F axpy 1, series init+nodes+finalize m+2, update 1
-            return m + 10
+            if self.ros._fused:
+                return series + 2 + 1  # aux init + fused prologue; final axpy
+            return series + 2 + 3 + 1 + 1 + 1  # combustion, Jacobian, A u, F axpy, final axpy
         if self.cfg["method"] == "linear":
-            return m + 2
-        # exp series (m1+2), combustion 2, phi1 series (m2+2), axpy 1
-        return m + 7
+            return series
+        # two series (2 m + 6), combustion 2, axpy 1
+        return series + 3 + 2 + 1
 
 
 def measured_peak():

@@ -134,6 +134,16 @@ int es_half_sum(const double *a, const double *b, double *out, int64_t n, void *
  * min/max written to minmax_dev[0..1]. */
 int es_combustion_jacobian(const double *u, double *out, double *minmax_dev, int64_t n,
                            void *stream);
+/* Fused prologue of the build-defined exponential Rosenbrock step for the
+ * combustion term: one stencil pass over u writes F = g(u) - A u and
+ * gdiag = g'(u), and returns min/max g' (minmax_host[0..1]) and the first
+ * index with u <= 0 (ES_ERR_DOMAIN, *first_bad_host).  aux_dev: 3 x u64 of
+ * device scratch.  Needs the TMA path (even nx, 16-byte aligned vectors, no
+ * Dirichlet-function faces).  Synchronises the stream. */
+int es_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F, double *gdiag,
+                           double *minmax_host, int64_t *first_bad_host, void *aux_dev,
+                           void *stream);
+
 /* max |x| (integrator.py:236 observer) into *out_dev. */
 int es_max_abs(const double *x, int64_t n, double *out_dev, void *stream);
 

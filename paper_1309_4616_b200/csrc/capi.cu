@@ -159,3 +159,11 @@ extern "C" int es_leja_csr_async(int64_t n, const int64_t *row_ptr, const int32_
     return es_leja_csr(n, row_ptr, col_idx, vals, v, p_out, dd, xi, ndd, alpha, shift, tol, workspace,
                        workspace_bytes, nullptr, stream);
 }
+
+extern "C" int es_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F, double *gdiag,
+                                      double *minmax_host, int64_t *first_bad_host, void *aux_dev, void *stream) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (!u || !F || !gdiag || !minmax_host || !first_bad_host || !aux_dev) return set_error(ES_ERR_ARG, "null pointer");
+    return run_rosenbrock_prologue(d, u, F, gdiag, minmax_host, first_bad_host, aux_dev, (cudaStream_t)stream);
+}

@@ -42,6 +42,13 @@ ES_DEV double radial_from_sq(double one_plus_x2, double y) {
     return div(1.0, sqrt_rn(add(one_plus_x2, mul(y, y))));
 }
 
+// ordered-integer image of a double (monotone in the value) for atomic
+// min/max; inverse: b = (o >> 63) ? (o & ~sign) : ~o
+ES_DEV unsigned long long ord(double d) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
 struct SeriesState {
     int k;            // last completed node (0 = none yet)
     int consecutive;  // consecutive passes of the term test

@@ -34,6 +34,8 @@ int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out,
                          double beta, const double *halo_lo, const double *halo_hi,
                          const double *gdiag, cudaStream_t stream);
 size_t stencil_series_ws_bytes(const es_stencil_desc *d);
+int run_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F, double *gdiag, double *minmax_host,
+                            int64_t *first_bad_host, void *aux_dev, cudaStream_t stream);
 int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
                        const double *xi, int ndd, double alpha, double shift, double tol,
                        const double *gdiag, void *ws, size_t ws_bytes, es_series_result *res,

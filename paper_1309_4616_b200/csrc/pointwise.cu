@@ -28,12 +28,6 @@ __global__ void k_combustion(const double *__restrict__ u, double *__restrict__ 
     }
 }
 
-// ordered-integer image of a double for atomic min/max
-ES_DEV unsigned long long ord(double d) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
-    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
-
 // g'(u) = e^{20(1-1/u)} (5 (2-u)/u^2 - 1/4); minmax[0] = min, [1] = max
 __global__ void k_combustion_jac(const double *__restrict__ u, double *__restrict__ out, int64_t n,
                                  unsigned long long *mm) {

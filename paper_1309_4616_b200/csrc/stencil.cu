@@ -110,6 +110,22 @@ __global__ void __launch_bounds__(TMA_THREADS, 3) k_apply_tma(const __grid_const
     tma_pass<DIM3, COEFF, false, false>(a.g, a.ps, mp, a.chunk_len, false, tsmem, nullptr, 0, nullptr);
 }
 
+// Fused Rosenbrock prologue: F = g(u) - A u, g'(u), min/max g', first u <= 0.
+template <bool DIM3, int COEFF>
+__global__ void __launch_bounds__(TMA_THREADS, 3) k_rospro_tma(const __grid_constant__ ApplyArgsT a) {
+    extern __shared__ __align__(128) char tsmem[];
+    const PassMaps mp{&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], nullptr, nullptr};
+    tma_pass<DIM3, COEFF, false, false, EPI_ROSPRO>(a.g, a.ps, mp, a.chunk_len, false, tsmem, nullptr, 0, nullptr);
+}
+
+__global__ void k_aux_init(unsigned long long *aux, unsigned long long n) {
+    if (threadIdx.x == 0) {
+        aux[0] = ~0ull;
+        aux[1] = 0ull;
+        aux[2] = n;
+    }
+}
+
 // One Newton-Leja node, persistent CTAs over (chunk, tile) items.
 template <bool DIM3, int COEFF, bool GD>
 __global__ void __launch_bounds__(TMA_THREADS, 3) k_node_tma(const SeriesParams *__restrict__ Pp) {
@@ -468,6 +484,63 @@ int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out,
     set_smem_attr((const void *)af, pl.smem);
     af<<<pl.grid, pl.block, pl.smem, stream>>>(a);
     return check_launch("stencil apply");
+}
+
+template <bool DIM3>
+static ApplyTmaFn pick_rospro(int coeff) {
+    switch (coeff) {
+        case ES_COEFF_RADIAL: return k_rospro_tma<DIM3, ES_COEFF_RADIAL>;
+        case ES_COEFF_ARRAY: return k_rospro_tma<DIM3, ES_COEFF_ARRAY>;
+        default: return k_rospro_tma<DIM3, ES_COEFF_NONE>;
+    }
+}
+
+static double unord(unsigned long long o) {
+    const unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+    double d;
+    std::memcpy(&d, &b, sizeof d);
+    return d;
+}
+
+int run_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F, double *gdiag, double *minmax_host,
+                            int64_t *first_bad_host, void *aux_dev, cudaStream_t stream) {
+    const int64_t n = d->nx * d->ny * d->lz;
+    const StencilPlan pl = plan_stencil(d, {u, F, gdiag}, true);
+    if (!pl.tma) return set_error(ES_ERR_ARG, "rosenbrock prologue needs the TMA path (even nx, aligned, no faces)");
+    unsigned long long *aux = static_cast<unsigned long long *>(aux_dev);
+    ApplyArgsT a;
+    a.g = make_geom(d, nullptr, nullptr);
+    a.ps.src = u;
+    a.ps.dst = F;
+    a.ps.p_src = nullptr;
+    a.ps.p_dst = gdiag;
+    a.ps.alpha = 1.0;
+    a.ps.beta = 0.0;
+    a.ps.dk = 0.0;
+    a.ps.d0 = 0.0;
+    a.ps.aux = aux;
+    a.chunk_len = pl.chunk;
+    std::memset(&a.maps, 0, sizeof(a.maps));
+    int rc = encode_w(&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], u, d, pl.dim2);
+    if (rc) return rc;
+    const ApplyTmaFn fn = pl.dim2 ? pick_rospro<false>(d->coeff_kind) : pick_rospro<true>(d->coeff_kind);
+    StencilPlan lp = pl;
+    finish_tma_plan(lp, (const void *)fn,
+                    pl.dim2 ? tma_smem_bytes<false, false, false>(pl.chunk) : tma_smem_bytes<true, false, false>(pl.chunk));
+    k_aux_init<<<1, 32, 0, stream>>>(aux, (unsigned long long)n);
+    fn<<<lp.grid, lp.block, lp.smem, stream>>>(a);
+    rc = check_launch("rosenbrock prologue");
+    if (rc) return rc;
+    unsigned long long h[3];
+    if (cudaMemcpyAsync(h, aux, sizeof h, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess)
+        return check_launch("rosenbrock prologue sync");
+    minmax_host[0] = unord(h[0]);
+    minmax_host[1] = unord(h[1]);
+    *first_bad_host = h[2] < (unsigned long long)n ? (int64_t)h[2] : -1;
+    if (*first_bad_host >= 0)
+        return set_error(ES_ERR_DOMAIN, "combustion nonlinearity undefined at index %lld", (long long)h[2]);
+    return ES_OK;
 }
 
 // ----- series workspace layout ------------------------------------------------

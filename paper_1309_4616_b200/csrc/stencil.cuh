@@ -66,6 +66,7 @@ struct Pass {
     const double *p_src;  // nullptr on node 1: p_{0} = d0 * v
     double *p_dst;        // nullptr for a plain apply
     double alpha, beta, dk, d0;
+    unsigned long long *aux = nullptr;  // Rosenbrock prologue: {min g', max g', first u <= 0}
 };
 
 template <int VEC>

@@ -240,7 +240,10 @@ ES_DEV void tma_produce(const Geom &g, const Items &its, const PassMaps &mp, cha
 // Consumers (warps 0..7): one point pair per thread per plane.  After each
 // item they write its per-plane partial sums (LEJA) and run the reduction
 // tickets among themselves (named barrier 1).
-template <bool DIM3, int COEFF, bool GD, bool LEJA, bool PG>
+// Epilogues of a plain (non-Leja) pass.
+enum { EPI_AXPY = 0, EPI_ROSPRO = 1 };
+
+template <bool DIM3, int COEFF, bool GD, bool LEJA, bool PG, int EPI = EPI_AXPY>
 ES_DEV void tma_consume(const Geom &g, const Pass &ps, const Items &its, char *smem,
                         const SeriesParams *P, int k) {
     using T = TShape<DIM3>;
@@ -258,6 +261,7 @@ ES_DEV void tma_consume(const Geom &g, const Pass &ps, const Items &its, char *s
     const bool use_pg = PG && (ps.p_src != nullptr || GD);
     const volatile int *itemq = reinterpret_cast<const volatile int *>(smem + Lt::ITEMQ_OFF);
     uint32_t uw = 0, up = 0;
+    unsigned long long gp_lo = ~0ull, gp_hi = 0ull, bad = ~0ull;  // EPI_ROSPRO
 
     auto wst = [&](uint32_t u) { return reinterpret_cast<const double *>(smem + (u % Lt::SW) * Lt::W_STAGE); };
     auto wwait = [&](uint32_t u) { mbar_wait(&wfull[u % Lt::SW], (u / Lt::SW) & 1); };
@@ -356,7 +360,30 @@ ES_DEV void tma_consume(const Geom &g, const Pass &ps, const Items &its, char *s
                     }
                 }
                 const int64_t o = row_base + ix;
-                *reinterpret_cast<double2 *>(ps.dst + o) = make_double2(wn[0], wn[1]);
+                if constexpr (EPI == EPI_ROSPRO) {
+                    // F = g(u) - A u and g'(u) in the same pass (build-defined
+                    // Rosenbrock prologue; same expressions as k_combustion,
+                    // k_combustion_jac and the alpha=1, beta=0 apply)
+                    double fv[2], gpv[2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const double x = cc[j];
+                        const double rr = div(1.0, x);
+                        const double e = exp(mul(20.0, sub(1.0, rr)));
+                        const double gval = mul(mul(0.25, sub(2.0, x)), e);
+                        const double q = mul(mul(5.0, sub(2.0, x)), mul(rr, rr));
+                        gpv[j] = mul(e, sub(q, 0.25));
+                        fv[j] = sub(gval, wn[j]);
+                        const unsigned long long od = ord(gpv[j]);
+                        gp_lo = od < gp_lo ? od : gp_lo;
+                        gp_hi = od > gp_hi ? od : gp_hi;
+                        if (x <= 0.0 && (unsigned long long)(o + j) < bad) bad = (unsigned long long)(o + j);
+                    }
+                    *reinterpret_cast<double2 *>(ps.dst + o) = make_double2(fv[0], fv[1]);
+                    *reinterpret_cast<double2 *>(ps.p_dst + o) = make_double2(gpv[0], gpv[1]);
+                } else {
+                    *reinterpret_cast<double2 *>(ps.dst + o) = make_double2(wn[0], wn[1]);
+                }
                 if constexpr (LEJA) {
                     *reinterpret_cast<double2 *>(ps.p_dst + o) = make_double2(pn[0], pn[1]);
                     acc_w = add(acc_w, add(mul(wn[0], wn[0]), mul(wn[1], wn[1])));
@@ -388,6 +415,22 @@ ES_DEV void tma_consume(const Geom &g, const Pass &ps, const Items &its, char *s
             }
         }
     }
+    if constexpr (EPI == EPI_ROSPRO) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long a = __shfl_xor_sync(0xffffffffu, gp_lo, o);
+            const unsigned long long b = __shfl_xor_sync(0xffffffffu, gp_hi, o);
+            const unsigned long long c = __shfl_xor_sync(0xffffffffu, bad, o);
+            gp_lo = a < gp_lo ? a : gp_lo;
+            gp_hi = b > gp_hi ? b : gp_hi;
+            bad = c < bad ? c : bad;
+        }
+        if (lane == 0) {
+            atomicMin(ps.aux, gp_lo);
+            atomicMax(ps.aux + 1, gp_hi);
+            atomicMin(ps.aux + 2, bad);
+        }
+    }
 }
 
 // Shared-memory footprint of one CTA.
@@ -397,7 +440,7 @@ constexpr size_t tma_smem_bytes(int) {
 }
 
 // Whole pass for one persistent CTA: barrier set-up, warp-specialised streaming.
-template <bool DIM3, int COEFF, bool GD, bool LEJA>
+template <bool DIM3, int COEFF, bool GD, bool LEJA, int EPI = EPI_AXPY>
 ES_DEV void tma_pass(const Geom &g, const Pass &ps, const PassMaps &mp, int chunk_len, bool acquire_maps,
                      char *smem, const SeriesParams *P, int k, unsigned *work) {
     constexpr bool PG = LEJA || GD;
@@ -428,7 +471,7 @@ ES_DEV void tma_pass(const Geom &g, const Pass &ps, const PassMaps &mp, int chun
             tma_produce<DIM3, PG, GD>(g, its, mp, smem, LEJA && ps.p_src != nullptr, work);
         }
     } else {
-        tma_consume<DIM3, COEFF, GD, LEJA, PG>(g, ps, its, smem, P, k);
+        tma_consume<DIM3, COEFF, GD, LEJA, PG, EPI>(g, ps, its, smem, P, k);
     }
 }
 

@@ -240,3 +240,32 @@ def test_large_3d_series_linearity_and_oracle():
     ref, _ = orc.newton_stencil(orc.StencilSpec(256, 256, 256), orc.Interp(lo, hi, "exp", -1e-4, it.xi, it.dd),
                                 x.cpu().numpy(), 0.0)
     assert p.cpu().numpy().tobytes() == ref.tobytes()
+
+
+def test_rosenbrock_fused_prologue_matches_generic_path():
+    g = es.Grid3D(48, 40, 30)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    u0 = torch.from_numpy(1.0 + 0.1 * np.random.default_rng(12).random(g.n)).cuda()
+    prob = es.SemilinearProblem(operator=op, nonlinearity=es.combustion_g, u0=u0)
+    fused = es.RosenbrockStepper(prob, 1e-6)
+    generic = es.RosenbrockStepper(prob, 1e-6)
+    generic._fused = False
+    f1, g1, lo1, hi1 = fused._prologue(u0, 0.0)
+    f2, g2, lo2, hi2 = generic._prologue(u0, 0.0)
+    assert fused._fused is True
+    assert torch.equal(f1, f2) and torch.equal(g1, g2) and (lo1, hi1) == (lo2, hi2)
+    u1, s1 = fused.step(u0, 0.0, 2e-4)
+    u2, s2 = generic.step(u0, 0.0, 2e-4)
+    assert s1.matvecs == s2.matvecs and torch.equal(u1, u2)
+
+
+def test_rosenbrock_domain_error():
+    g = es.Grid3D(16, 12, 10)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    u0 = np.full(g.n, 1.0)
+    u0[77] = -0.5
+    u0[200] = 0.0
+    prob = es.SemilinearProblem(operator=op, nonlinearity=es.combustion_g, u0=u0)
+    with pytest.raises(es.DomainError) as ei:
+        es.exponential_rosenbrock_step(prob, u0, 1e-4, 1e-6)
+    assert ei.value.index == 77
