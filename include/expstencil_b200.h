@@ -125,6 +125,33 @@ int es_leja_csr_async(int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
                       const double *xi, int32_t ndd, double alpha, double shift, double tol,
                       void *workspace, size_t workspace_bytes, void *stream);
 
+/* Multi-GPU slab series (decomp.py:146-266 / :368-382 on one rank per GPU).
+ * The series state lives on every rank; per node k = 1, 2, ... the caller
+ *   1. sends the first/last plane of *es_leja_dist_source(ws, k) to the
+ *      neighbouring ranks and receives theirs into halo_lo / halo_hi (the
+ *      buffers passed to begin; NULL at the physical boundary),
+ *   2. es_leja_dist_node: one fused pass over the slab plus this slab's
+ *      per-z-chunk partial sums (nslices x 2 doubles) into slices_out,
+ *   3. all-gathers the slices of all ranks in rank order and calls
+ *      es_leja_dist_decide, which runs the stopping test identically on
+ *      every rank (chunks aligned to global z make the sums bitwise equal to
+ *      a single-GPU run),
+ * and finally es_leja_dist_end + es_leja_fetch.  Nodes after the decision
+ * return immediately, so the caller may enqueue ahead and poll. */
+int es_leja_dist_begin(const es_stencil_desc *d, const double *v, double *p_out,
+                       const double *dd, const double *xi, int32_t ndd, double alpha,
+                       double shift, double tol, const double *gdiag, const double *halo_lo,
+                       const double *halo_hi, void *workspace, size_t workspace_bytes, void *stream);
+int es_leja_dist_source(const void *workspace, int32_t k, const double **src_out);
+int es_leja_dist_nslices(const void *workspace, int32_t *nslices_out);
+int es_leja_dist_node(const void *workspace, double *slices_out, void *stream);
+int es_leja_dist_decide(const void *workspace, const double *slices_all, int32_t nslices, void *stream);
+int es_leja_dist_end(const void *workspace, void *stream);
+/* Byte offset of the series state {int k, consecutive, done, converged;
+ * double last_term, last_pnorm} inside a series workspace (for asynchronous
+ * polling of `done` with a plain device-to-host copy). */
+size_t es_leja_state_offset(void);
+
 /* Integrator-stage element-wise kernels (integrator.py:177-189,
  * matfunc.py:366-371); all stream-ordered, no sync. */
 int es_axpy(const double *y, const double *z, double h, double *out, int64_t n, void *stream);
@@ -142,7 +169,7 @@ int es_combustion_jacobian(const double *u, double *out, double *minmax_dev, int
  * Dirichlet-function faces).  Synchronises the stream. */
 int es_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F, double *gdiag,
                            double *minmax_host, int64_t *first_bad_host, void *aux_dev,
-                           void *stream);
+                           const double *halo_lo, const double *halo_hi, void *stream);
 
 /* max |x| (integrator.py:236 observer) into *out_dev. */
 int es_max_abs(const double *x, int64_t n, double *out_dev, void *stream);

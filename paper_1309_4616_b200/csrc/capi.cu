@@ -161,9 +161,55 @@ extern "C" int es_leja_csr_async(int64_t n, const int64_t *row_ptr, const int32_
 }
 
 extern "C" int es_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F, double *gdiag,
-                                      double *minmax_host, int64_t *first_bad_host, void *aux_dev, void *stream) {
+                                      double *minmax_host, int64_t *first_bad_host, void *aux_dev,
+                                      const double *halo_lo, const double *halo_hi, void *stream) {
     int rc = check_desc(d);
     if (rc) return rc;
     if (!u || !F || !gdiag || !minmax_host || !first_bad_host || !aux_dev) return set_error(ES_ERR_ARG, "null pointer");
-    return run_rosenbrock_prologue(d, u, F, gdiag, minmax_host, first_bad_host, aux_dev, (cudaStream_t)stream);
+    return run_rosenbrock_prologue(d, u, F, gdiag, minmax_host, first_bad_host, aux_dev, halo_lo, halo_hi,
+                                   (cudaStream_t)stream);
 }
+
+extern "C" int es_leja_dist_begin(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
+                                  const double *xi, int32_t ndd, double alpha, double shift, double tol,
+                                  const double *gdiag, const double *halo_lo, const double *halo_hi, void *workspace,
+                                  size_t workspace_bytes, void *stream) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (d->mode == ES_MODE_FACES || d->mode == ES_MODE_PERIODIC)
+        return set_error(ES_ERR_ARG, "slab series need a linear, non-periodic boundary rule");
+    if (!v || !p_out || !dd || !xi || !workspace) return set_error(ES_ERR_ARG, "null pointer");
+    if (v == p_out) return set_error(ES_ERR_ARG, "p_out must not alias v");
+    return dist_begin(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, halo_lo, halo_hi, workspace,
+                      workspace_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int es_leja_dist_source(const void *workspace, int32_t k, const double **src_out) {
+    if (!workspace || !src_out) return set_error(ES_ERR_ARG, "null pointer");
+    return dist_source(workspace, k, src_out);
+}
+
+extern "C" int es_leja_dist_nslices(const void *workspace, int32_t *nslices_out) {
+    if (!workspace || !nslices_out) return set_error(ES_ERR_ARG, "null pointer");
+    int n = 0;
+    const int rc = dist_nslices(workspace, &n);
+    *nslices_out = n;
+    return rc;
+}
+
+extern "C" int es_leja_dist_node(const void *workspace, double *slices_out, void *stream) {
+    if (!workspace || !slices_out) return set_error(ES_ERR_ARG, "null pointer");
+    return dist_node(workspace, slices_out, (cudaStream_t)stream);
+}
+
+extern "C" int es_leja_dist_decide(const void *workspace, const double *slices_all, int32_t nslices, void *stream) {
+    if (!workspace || !slices_all || nslices < 1) return set_error(ES_ERR_ARG, "bad slices");
+    return dist_decide(workspace, slices_all, nslices, (cudaStream_t)stream);
+}
+
+extern "C" int es_leja_dist_end(const void *workspace, void *stream) {
+    if (!workspace) return set_error(ES_ERR_ARG, "null pointer");
+    return dist_end(workspace, (cudaStream_t)stream);
+}
+
+extern "C" size_t es_leja_state_offset(void) { return series_state_offset(); }

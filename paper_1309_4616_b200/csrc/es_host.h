@@ -15,6 +15,7 @@ int current_device();
 
 struct SeriesState;
 SeriesState *series_state_ptr(void *ws);
+size_t series_state_offset();
 void launch_state_trivial(void *ws, cudaStream_t stream);
 int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaStream_t stream);
 
@@ -35,7 +36,16 @@ int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out,
                          const double *gdiag, cudaStream_t stream);
 size_t stencil_series_ws_bytes(const es_stencil_desc *d);
 int run_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F, double *gdiag, double *minmax_host,
-                            int64_t *first_bad_host, void *aux_dev, cudaStream_t stream);
+                            int64_t *first_bad_host, void *aux_dev, const double *halo_lo, const double *halo_hi,
+                            cudaStream_t stream);
+int dist_begin(const es_stencil_desc *d, const double *v, double *p_out, const double *dd, const double *xi, int ndd,
+               double alpha, double shift, double tol, const double *gdiag, const double *halo_lo,
+               const double *halo_hi, void *ws, size_t ws_bytes, cudaStream_t stream);
+int dist_source(const void *ws, int k, const double **src);
+int dist_nslices(const void *ws, int *nslices);
+int dist_node(const void *ws, double *slices_out, cudaStream_t stream);
+int dist_decide(const void *ws, const double *slices_all, int nslices, cudaStream_t stream);
+int dist_end(const void *ws, cudaStream_t stream);
 int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
                        const double *xi, int ndd, double alpha, double shift, double tol,
                        const double *gdiag, void *ws, size_t ws_bytes, es_series_result *res,

@@ -140,6 +140,9 @@ ES_DEV void slice_reduce_decide(const SeriesParams &P, int k) {
         }
         P.slice[2 * c] = a;
         P.slice[2 * c + 1] = b;
+    }
+    if (P.dist) return;  // multi-GPU: the caller gathers the slices of all slabs
+    if (t == 0) {
         __threadfence();
         s_last = atomicAdd(P.global_cnt, 1u) == gridDim.x - 1u;
     }
@@ -159,6 +162,21 @@ ES_DEV void slice_reduce_decide(const SeriesParams &P, int k) {
             *P.global_cnt = 0u;
         }
     }
+}
+
+// Decision of a multi-GPU node on the gathered slices of all slabs (global
+// z-chunk order), identical on every rank.
+ES_DEV void decide_gathered(const SeriesParams &P, int k, const double *slices, int nslices) {
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x >= 32) return;
+    double sw = 0.0, sp = 0.0;
+    for (int s = lane; s < nslices; s += 32) {
+        sw = add(sw, slices[2 * s]);
+        sp = add(sp, slices[2 * s + 1]);
+    }
+    sw = warp_sum(sw);
+    sp = warp_sum(sp);
+    if (lane == 0) decide(P, k, sw, sp);
 }
 
 // Node k's pass description from the device state (k = last completed + 1).

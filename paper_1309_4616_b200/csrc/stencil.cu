@@ -106,7 +106,7 @@ struct ApplyArgsT {
 template <bool DIM3, int COEFF>
 __global__ void __launch_bounds__(TMA_THREADS, 3) k_apply_tma(const __grid_constant__ ApplyArgsT a) {
     extern __shared__ __align__(128) char tsmem[];
-    const PassMaps mp{&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], nullptr, nullptr};
+    const PassMaps mp{&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], nullptr, nullptr, &a.maps.m[MAP_HLO], &a.maps.m[MAP_HHI]};
     tma_pass<DIM3, COEFF, false, false>(a.g, a.ps, mp, a.chunk_len, false, tsmem, nullptr, 0, nullptr);
 }
 
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 3) k_apply_tma(const __grid_const
 template <bool DIM3, int COEFF>
 __global__ void __launch_bounds__(TMA_THREADS, 3) k_rospro_tma(const __grid_constant__ ApplyArgsT a) {
     extern __shared__ __align__(128) char tsmem[];
-    const PassMaps mp{&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], nullptr, nullptr};
+    const PassMaps mp{&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], nullptr, nullptr, &a.maps.m[MAP_HLO], &a.maps.m[MAP_HHI]};
     tma_pass<DIM3, COEFF, false, false, EPI_ROSPRO>(a.g, a.ps, mp, a.chunk_len, false, tsmem, nullptr, 0, nullptr);
 }
 
@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(TMA_THREADS, 3) k_node_tma(const SeriesParams 
     const Pass ps = node_pass(P, k);
     const TmaMaps &M = *static_cast<const TmaMaps *>(P.maps);
     const int wi = k == 1 ? 0 : 1 + ((k - 1) & 1);
-    const PassMaps mp{&M.m[2 * wi], &M.m[2 * wi + 1], &M.m[MAP_P_0 + ((k - 1) & 1)], &M.m[MAP_G]};
+    const PassMaps mp{&M.m[2 * wi], &M.m[2 * wi + 1], &M.m[MAP_P_0 + ((k - 1) & 1)], &M.m[MAP_G], &M.m[MAP_HLO],
+                      &M.m[MAP_HHI]};
     tma_pass<DIM3, COEFF, GD, true>(P.g, ps, mp, P.chunk_len, true, tsmem, Pp, k, P.work);
 }
 
@@ -196,8 +197,10 @@ void launch_state_trivial(void *ws, cudaStream_t stream) {
     k_state_trivial<<<1, 1, 0, stream>>>(series_state_ptr(ws));
 }
 
+size_t series_state_offset() { return (sizeof(SeriesParams) + 255) & ~(size_t)255; }
+
 SeriesState *series_state_ptr(void *ws) {
-    return reinterpret_cast<SeriesState *>(static_cast<char *>(ws) + ((sizeof(SeriesParams) + 255) & ~(size_t)255));
+    return reinterpret_cast<SeriesState *>(static_cast<char *>(ws) + series_state_offset());
 }
 
 __global__ void k_scale_dev(const double *x, const double *s, double *out, int64_t n) {
@@ -356,7 +359,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2 };
+enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3 };
 
 // TMA descriptor of a slab-shaped fp64 vector (x fastest); OOB reads are
 // zero-filled, which is the homogeneous Dirichlet ghost rule.
@@ -368,7 +371,14 @@ static int encode_map(CUtensorMap *m, const double *base, const es_stencil_desc 
     cuuint64_t dims[3], strides[2];
     cuuint32_t box[3], estr[3] = {1, 1, 1};
     cuuint32_t rank;
-    if (dim2) {
+    if (kind == MK_HALO) {  // one (ny, nx) plane, same box as the 3D W tiles
+        rank = 2;
+        dims[0] = (cuuint64_t)d->nx;
+        dims[1] = (cuuint64_t)d->ny;
+        strides[0] = (cuuint64_t)d->nx * 8;
+        box[0] = 68;
+        box[1] = 10;
+    } else if (dim2) {
         rank = 2;
         dims[0] = (cuuint64_t)d->nx;
         dims[1] = (cuuint64_t)d->ny;
@@ -447,7 +457,8 @@ int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out,
                          double beta, const double *halo_lo, const double *halo_hi,
                          const double *gdiag, cudaStream_t stream) {
     if (d->nx * d->ny * d->lz == 0) return ES_OK;
-    const bool plain = !halo_lo && !halo_hi && !gdiag;
+    const bool dim2 = d->nz_total == 1 && d->lz == 1;
+    const bool plain = !gdiag && (dim2 ? (!halo_lo && !halo_hi) : true);
     const StencilPlan pl = plan_stencil(d, {u, out, halo_lo, halo_hi, gdiag}, plain);
     Pass ps;
     ps.src = u;
@@ -460,11 +471,13 @@ int launch_stencil_apply(const es_stencil_desc *d, const double *u, double *out,
     ps.d0 = 0.0;
     if (pl.tma) {
         ApplyArgsT a;
-        a.g = make_geom(d, nullptr, nullptr);
+        a.g = make_geom(d, halo_lo, halo_hi);
         a.ps = ps;
         a.chunk_len = pl.chunk;
         std::memset(&a.maps, 0, sizeof(a.maps));
         int rc = encode_w(&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], u, d, pl.dim2);
+        if (!rc) rc = encode_map(&a.maps.m[MAP_HLO], halo_lo, d, pl.dim2, MK_HALO);
+        if (!rc) rc = encode_map(&a.maps.m[MAP_HHI], halo_hi, d, pl.dim2, MK_HALO);
         if (rc) return rc;
         const ApplyTmaFn fn = pl.dim2 ? pick_apply_tma<false>(d->coeff_kind) : pick_apply_tma<true>(d->coeff_kind);
         StencilPlan lp = pl;
@@ -503,13 +516,15 @@ static double unord(unsigned long long o) {
 }
 
 int run_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F, double *gdiag, double *minmax_host,
-                            int64_t *first_bad_host, void *aux_dev, cudaStream_t stream) {
+                            int64_t *first_bad_host, void *aux_dev, const double *halo_lo, const double *halo_hi,
+                            cudaStream_t stream) {
     const int64_t n = d->nx * d->ny * d->lz;
-    const StencilPlan pl = plan_stencil(d, {u, F, gdiag}, true);
+    const StencilPlan pl = plan_stencil(d, {u, F, gdiag, halo_lo, halo_hi}, true);
+    if ((halo_lo || halo_hi) && pl.dim2) return set_error(ES_ERR_ARG, "halos need a 3D slab");
     if (!pl.tma) return set_error(ES_ERR_ARG, "rosenbrock prologue needs the TMA path (even nx, aligned, no faces)");
     unsigned long long *aux = static_cast<unsigned long long *>(aux_dev);
     ApplyArgsT a;
-    a.g = make_geom(d, nullptr, nullptr);
+    a.g = make_geom(d, halo_lo, halo_hi);
     a.ps.src = u;
     a.ps.dst = F;
     a.ps.p_src = nullptr;
@@ -522,6 +537,8 @@ int run_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F
     a.chunk_len = pl.chunk;
     std::memset(&a.maps, 0, sizeof(a.maps));
     int rc = encode_w(&a.maps.m[MAP_WA_V], &a.maps.m[MAP_WB_V], u, d, pl.dim2);
+    if (!rc) rc = encode_map(&a.maps.m[MAP_HLO], halo_lo, d, pl.dim2, MK_HALO);
+    if (!rc) rc = encode_map(&a.maps.m[MAP_HHI], halo_hi, d, pl.dim2, MK_HALO);
     if (rc) return rc;
     const ApplyTmaFn fn = pl.dim2 ? pick_rospro<false>(d->coeff_kind) : pick_rospro<true>(d->coeff_kind);
     StencilPlan lp = pl;
@@ -641,37 +658,40 @@ static bool build_while_graph(NodeFn nf, const StencilPlan &pl, const SeriesPara
     return true;
 }
 
-int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
-                       const double *xi, int ndd, double alpha, double shift, double tol,
-                       const double *gdiag, void *ws, size_t ws_bytes, es_series_result *res,
-                       cudaStream_t stream) {
-    const int64_t n = d->nx * d->ny * d->lz;
-    if (ndd < 1) return set_error(ES_ERR_ARG, "ndd must be >= 1");
-    char *w = static_cast<char *>(ws);
-    const StencilPlan pl = plan_stencil(d, {v, p_out, gdiag, (const void *)(w + 0)}, true);
-    const WsLayout L = layout(n, pl.nslices, pl.ntiles, pl.nchunks);
-    if (ws_bytes < L.total) return set_error(ES_ERR_ARG, "workspace too small");
-    if (ndd == 1 || n == 0) {  // degenerate interval: dd_0 v, 0 matvecs (matfunc.py:285-286)
-        if (n > 0) k_scale_dev<<<std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, stream>>>(v, dd, p_out, n);
-        launch_state_trivial(ws, stream);
-        int rc = check_launch("scale");
-        if (rc || !res) return rc;
-        return read_series_state(series_state_ptr(ws), res, stream);
-    }
-    // VEC=2 additionally needs the scratch vectors aligned (layout is 256B aligned)
-    ApplyFn af;
+// Everything a series needs before its first node: plan, kernel, device
+// parameters (published with the state reset), TMA descriptors.
+struct SeriesSetup {
+    StencilPlan pl, lp;
     NodeFn nf;
-    StencilPlan lp = pl;
-    if (pl.tma) {
-        nf = pick_node_tma(pl.dim2, d->coeff_kind, gdiag != nullptr);
-        finish_tma_plan(lp, (const void *)nf, node_smem(pl.dim2, gdiag != nullptr, pl.chunk));
-    } else {
-        pick_all(pl, d->coeff_kind, gdiag != nullptr, af, nf);
-        set_smem_attr((const void *)nf, pl.smem);
-    }
+    SeriesParams hp;
+    SeriesParams *dparams;
+    int64_t n;
+};
 
-    SeriesParams hp = {};
-    hp.g = make_geom(d, nullptr, nullptr);
+static int prepare_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
+                          const double *xi, int ndd, double alpha, double shift, double tol, const double *gdiag,
+                          const double *halo_lo, const double *halo_hi, bool dist, void *ws, size_t ws_bytes,
+                          SeriesSetup &S, cudaStream_t stream) {
+    S.n = d->nx * d->ny * d->lz;
+    char *w = static_cast<char *>(ws);
+    S.pl = plan_stencil(d, {v, p_out, gdiag, halo_lo, halo_hi, (const void *)(w + 0)}, true);
+    const StencilPlan &pl = S.pl;
+    if ((halo_lo || halo_hi || dist) && !(pl.tma && !pl.dim2))
+        return set_error(ES_ERR_ARG, "slab series with halos need the 3D TMA path (even nx, aligned vectors)");
+    const WsLayout L = layout(S.n, pl.nslices, pl.ntiles, pl.nchunks);
+    if (ws_bytes < L.total) return set_error(ES_ERR_ARG, "workspace too small");
+    ApplyFn af;
+    S.lp = pl;
+    if (pl.tma) {
+        S.nf = pick_node_tma(pl.dim2, d->coeff_kind, gdiag != nullptr);
+        finish_tma_plan(S.lp, (const void *)S.nf, node_smem(pl.dim2, gdiag != nullptr, pl.chunk));
+    } else {
+        pick_all(pl, d->coeff_kind, gdiag != nullptr, af, S.nf);
+        set_smem_attr((const void *)S.nf, pl.smem);
+    }
+    SeriesParams &hp = S.hp;
+    hp = SeriesParams{};
+    hp.g = make_geom(d, halo_lo, halo_hi);
     hp.v = v;
     hp.wbuf[1] = reinterpret_cast<double *>(w + L.wa);
     hp.wbuf[0] = reinterpret_cast<double *>(w + L.wb);
@@ -696,7 +716,8 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     hp.chunk_len = pl.chunk;
     hp.cond = 0;
     hp.maps = nullptr;
-    SeriesParams *dparams = reinterpret_cast<SeriesParams *>(w + L.params);
+    hp.dist = dist ? 1 : 0;
+    S.dparams = reinterpret_cast<SeriesParams *>(w + L.params);
     if (pl.tma) {
         TmaMaps maps;
         std::memset(&maps, 0, sizeof(maps));
@@ -706,47 +727,158 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
         if (!rc) rc = encode_map(&maps.m[MAP_P_0], hp.pbuf[0], d, pl.dim2, MK_P);
         if (!rc) rc = encode_map(&maps.m[MAP_P_1], hp.pbuf[1], d, pl.dim2, MK_P);
         if (!rc) rc = encode_map(&maps.m[MAP_G], gdiag, d, pl.dim2, MK_P);
+        if (!rc) rc = encode_map(&maps.m[MAP_HLO], halo_lo, d, pl.dim2, MK_HALO);
+        if (!rc) rc = encode_map(&maps.m[MAP_HHI], halo_hi, d, pl.dim2, MK_HALO);
         if (rc) return rc;
         TmaMaps *dmaps = reinterpret_cast<TmaMaps *>(w + L.maps);
         k_publish_maps<<<1, 32, 0, stream>>>(maps, dmaps);
         hp.maps = dmaps;
     }
+    return ES_OK;
+}
 
+int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
+                       const double *xi, int ndd, double alpha, double shift, double tol,
+                       const double *gdiag, void *ws, size_t ws_bytes, es_series_result *res,
+                       cudaStream_t stream) {
+    const int64_t n = d->nx * d->ny * d->lz;
+    if (ndd < 1) return set_error(ES_ERR_ARG, "ndd must be >= 1");
+    if (ndd == 1 || n == 0) {  // degenerate interval: dd_0 v, 0 matvecs (matfunc.py:285-286)
+        const StencilPlan pl = plan_stencil(d, {v, p_out, gdiag, ws}, true);
+        if (ws_bytes < layout(n, pl.nslices, pl.ntiles, pl.nchunks).total)
+            return set_error(ES_ERR_ARG, "workspace too small");
+        if (n > 0) k_scale_dev<<<std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, stream>>>(v, dd, p_out, n);
+        launch_state_trivial(ws, stream);
+        int rc = check_launch("scale");
+        if (rc || !res) return rc;
+        return read_series_state(series_state_ptr(ws), res, stream);
+    }
+    SeriesSetup S;
+    int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, nullptr, nullptr, false, ws,
+                            ws_bytes, S, stream);
+    if (rc) return rc;
     GraphEntry *ge = nullptr;
     if (!env_int("ES_NO_GRAPH", 0)) {
         std::lock_guard<std::mutex> lk(g_graph_mu);
-        auto key = std::make_tuple((const void *)nf, lp.grid.x, lp.grid.y, lp.grid.z, lp.smem, (const void *)dparams,
-                                   current_device());
+        auto key = std::make_tuple((const void *)S.nf, S.lp.grid.x, S.lp.grid.y, S.lp.grid.z, S.lp.smem,
+                                   (const void *)S.dparams, current_device());
         auto it = g_graphs.find(key);
         if (it == g_graphs.end()) {
             GraphEntry e;
-            const bool ok = pl.tma ? build_while_graph(nf, lp, dparams, e, k_slice_reduce, (unsigned)pl.nslices)
-                                   : build_while_graph(nf, lp, dparams, e);
+            const bool ok = S.pl.tma
+                                ? build_while_graph(S.nf, S.lp, S.dparams, e, k_slice_reduce, (unsigned)S.pl.nslices)
+                                : build_while_graph(S.nf, S.lp, S.dparams, e);
             if (ok) it = g_graphs.emplace(key, e).first;
             else cudaGetLastError();
         }
         if (it != g_graphs.end()) ge = &it->second;
     }
-    if (ge) hp.cond = (unsigned long long)ge->handle;
-
-    k_series_init<<<1, 256, 0, stream>>>(hp, dparams);
-    int rc = check_launch("series init");
+    if (ge) S.hp.cond = (unsigned long long)ge->handle;
+    k_series_init<<<1, 256, 0, stream>>>(S.hp, S.dparams);
+    rc = check_launch("series init");
     if (rc) return rc;
     if (ge) {
         if (cudaGraphLaunch(ge->exec, stream) != cudaSuccess) return check_launch("series graph");
     } else {
         for (int k = 1; k < ndd; ++k) {
-            nf<<<lp.grid, lp.block, lp.smem, stream>>>(dparams);
-            if (pl.tma) k_slice_reduce<<<(unsigned)pl.nslices, 256, 0, stream>>>(dparams);
+            S.nf<<<S.lp.grid, S.lp.block, S.lp.smem, stream>>>(S.dparams);
+            if (S.pl.tma) k_slice_reduce<<<(unsigned)S.pl.nslices, 256, 0, stream>>>(S.dparams);
         }
         rc = check_launch("series nodes");
         if (rc) return rc;
     }
-    k_series_finalize<<<148 * 8, 256, 0, stream>>>(dparams, n);
+    k_series_finalize<<<148 * 8, 256, 0, stream>>>(S.dparams, n);
     rc = check_launch("series finalize");
     if (rc) return rc;
     if (!res) return ES_OK;  // asynchronous: es_leja_fetch reads the state later
-    return read_series_state(hp.state, res, stream);
+    return read_series_state(S.hp.state, res, stream);
+}
+
+// ----- multi-GPU slab series: the caller drives the nodes ---------------------
+//
+// Per node k (host-tracked, 1-based): the caller exchanges the boundary
+// planes of dist_source(k) into the halo buffers given at begin, calls
+// dist_node (pass over the slab + local per-chunk slices, no decision),
+// all-gathers the slices of every rank in rank (= global z) order and calls
+// dist_decide, which evaluates the stopping test identically on every rank.
+// Node kernels after the decision return immediately.
+
+static std::mutex g_dist_mu;
+static std::map<const void *, SeriesSetup> g_dist;
+
+int dist_begin(const es_stencil_desc *d, const double *v, double *p_out, const double *dd, const double *xi, int ndd,
+               double alpha, double shift, double tol, const double *gdiag, const double *halo_lo,
+               const double *halo_hi, void *ws, size_t ws_bytes, cudaStream_t stream) {
+    if (ndd < 2) return set_error(ES_ERR_ARG, "a slab series needs ndd >= 2");
+    SeriesSetup S;
+    int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, halo_lo, halo_hi, true, ws, ws_bytes,
+                            S, stream);
+    if (rc) return rc;
+    k_series_init<<<1, 256, 0, stream>>>(S.hp, S.dparams);
+    rc = check_launch("slab series init");
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_dist_mu);
+    g_dist[ws] = S;
+    return ES_OK;
+}
+
+static int dist_get(const void *ws, SeriesSetup *&S) {
+    std::lock_guard<std::mutex> lk(g_dist_mu);
+    auto it = g_dist.find(ws);
+    if (it == g_dist.end()) return set_error(ES_ERR_ARG, "no slab series begun on this workspace");
+    S = &it->second;
+    return ES_OK;
+}
+
+int dist_source(const void *ws, int k, const double **src) {
+    SeriesSetup *S;
+    int rc = dist_get(ws, S);
+    if (rc) return rc;
+    *src = k <= 1 ? S->hp.v : S->hp.wbuf[(k - 1) & 1];
+    return ES_OK;
+}
+
+int dist_nslices(const void *ws, int *nslices) {
+    SeriesSetup *S;
+    int rc = dist_get(ws, S);
+    if (rc) return rc;
+    *nslices = S->pl.nslices;
+    return ES_OK;
+}
+
+int dist_node(const void *ws, double *slices_out, cudaStream_t stream) {
+    SeriesSetup *S;
+    int rc = dist_get(ws, S);
+    if (rc) return rc;
+    S->nf<<<S->lp.grid, S->lp.block, S->lp.smem, stream>>>(S->dparams);
+    k_slice_reduce<<<(unsigned)S->pl.nslices, 256, 0, stream>>>(S->dparams);
+    cudaMemcpyAsync(slices_out, S->hp.slice, sizeof(double) * 2 * S->pl.nslices, cudaMemcpyDeviceToDevice, stream);
+    return check_launch("slab node");
+}
+
+__global__ void k_decide_gathered(const SeriesParams *__restrict__ Pp, const double *slices, int nslices) {
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    decide_gathered(P, P.state->k + 1, slices, nslices);
+}
+
+int dist_decide(const void *ws, const double *slices_all, int nslices, cudaStream_t stream) {
+    SeriesSetup *S;
+    int rc = dist_get(ws, S);
+    if (rc) return rc;
+    k_decide_gathered<<<1, 32, 0, stream>>>(S->dparams, slices_all, nslices);
+    return check_launch("slab decide");
+}
+
+int dist_end(const void *ws, cudaStream_t stream) {
+    SeriesSetup *S;
+    int rc = dist_get(ws, S);
+    if (rc) return rc;
+    k_series_finalize<<<148 * 8, 256, 0, stream>>>(S->dparams, S->n);
+    rc = check_launch("slab series finalize");
+    std::lock_guard<std::mutex> lk(g_dist_mu);
+    g_dist.erase(ws);
+    return rc;
 }
 
 }  // namespace es

@@ -57,6 +57,7 @@ struct SeriesParams {
     int64_t n;
     const void *maps;  // TmaMaps (workspace) for the TMA node kernel
     unsigned *work;    // dynamic work-item counter of the TMA node kernel
+    int dist;          // 1: slab of a multi-GPU series (slices gathered by the caller, k_decide_gathered decides)
 };
 
 // One pass: what a node (or a plain fused apply) reads and writes.

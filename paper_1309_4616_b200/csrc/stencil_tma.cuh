@@ -40,7 +40,7 @@ constexpr int TMA_THREADS = 32 * (TMA_CONSUMER_WARPS + 1);
 
 // tensor maps of one pass; for 2D, W needs two maps (256-wide and 4-wide
 // boxes: TMA boxes are at most 256 elements per dimension)
-enum { MAP_WA_V = 0, MAP_WB_V, MAP_WA_0, MAP_WB_0, MAP_WA_1, MAP_WB_1, MAP_P_0, MAP_P_1, MAP_G, MAP_COUNT };
+enum { MAP_WA_V = 0, MAP_WB_V, MAP_WA_0, MAP_WB_0, MAP_WA_1, MAP_WB_1, MAP_P_0, MAP_P_1, MAP_G, MAP_HLO, MAP_HHI, MAP_COUNT };
 
 struct alignas(64) TmaMaps {
     CUtensorMap m[MAP_COUNT];
@@ -124,6 +124,7 @@ ES_DEV int march_src(const Geom &g, int j, int L) {
 // Maps used by one pass (pointers into param or global memory).
 struct PassMaps {
     const CUtensorMap *wa, *wb, *p, *g;
+    const CUtensorMap *hlo = nullptr, *hhi = nullptr;  // slab halo planes (3D, multi-GPU)
 };
 
 // Work items: (chunk, tile), chunk-major so all CTAs sweep the planes
@@ -196,7 +197,12 @@ ES_DEV void tma_produce(const Geom &g, const Items &its, const PassMaps &mp, cha
             mbar_expect_tx(&wfull[s], Lt::W_BYTES);
             const int js = march_src<DIM3>(g, j, its.L);
             if constexpr (DIM3) {
-                tma_load(st, mp.wa, &wfull[s], it.x0 - 2, it.y0 - 1, js);
+                if (j < 0 && g.halo_lo)  // neighbour slab's last plane
+                    tma_load(st, mp.hlo, &wfull[s], it.x0 - 2, it.y0 - 1);
+                else if (j >= its.L && g.halo_hi)
+                    tma_load(st, mp.hhi, &wfull[s], it.x0 - 2, it.y0 - 1);
+                else
+                    tma_load(st, mp.wa, &wfull[s], it.x0 - 2, it.y0 - 1, js);
             } else {
                 tma_load(st, mp.wa, &wfull[s], it.x0 - 2, js);
                 tma_load(st + 2048, mp.wa, &wfull[s], it.x0 + 254, js);
@@ -463,6 +469,8 @@ ES_DEV void tma_pass(const Geom &g, const Pass &ps, const PassMaps &mp, int chun
     if (warp == TMA_CONSUMER_WARPS) {
         if ((threadIdx.x & 31) == 0) {
             if (acquire_maps) {
+                if (g.halo_lo) tma_acquire(mp.hlo);
+                if (g.halo_hi) tma_acquire(mp.hhi);
                 tma_acquire(mp.wa);
                 if (!DIM3) tma_acquire(mp.wb);
                 if (LEJA && ps.p_src) tma_acquire(mp.p);

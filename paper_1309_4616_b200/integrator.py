@@ -294,8 +294,9 @@ class RosenbrockStepper:
     def __init__(self, problem: SemilinearProblem, tol: float, max_degree: int = 150):
         from .stencil import StencilOperator
 
-        if not isinstance(problem.operator, StencilOperator):
-            raise TypeError("exponential Rosenbrock needs a StencilOperator")
+        self._dist = hasattr(problem.operator, "comm")  # DistributedStencil (one slab per rank)
+        if not (isinstance(problem.operator, StencilOperator) or self._dist):
+            raise TypeError("exponential Rosenbrock needs a StencilOperator or DistributedStencil")
         if problem.jacobian is None:
             raise ValueError("exponential Rosenbrock needs the nonlinearity's Jacobian diagonal")
         self.problem, self.tol, self.max_degree = problem, tol, max_degree
@@ -325,16 +326,30 @@ class RosenbrockStepper:
             bad = ctypes.c_int64(-1)
             if self._aux is None:
                 self._aux = torch.empty(4, dtype=torch.int64, device=u.device)
+            hl = hh = None
+            if self._dist:
+                op.halo_exchange(u)
+                hl, hh = op.halo_lo, op.halo_hi
             rc = _lib.load().es_rosenbrock_prologue(ctypes.byref(d), ptr(u), ptr(f), ptr(gp), mm, ctypes.byref(bad),
-                                                   ptr(self._aux), stream_handle())
+                                                   ptr(self._aux), ptr(hl), ptr(hh), stream_handle())
             del keep
-            if rc == _lib.ES_ERR_DOMAIN:
-                i = int(bad.value)
-                raise DomainError(f"combustion nonlinearity undefined at index {i} (u={float(u[i])!r} <= 0)", index=i)
-            if rc == _lib.ES_OK:
+            if rc in (_lib.ES_OK, _lib.ES_ERR_DOMAIN):
+                gmin, gmax, i = mm[0], mm[1], int(bad.value)
+                if self._dist:  # global interval and first bad point over all slabs
+                    import torch.distributed as dist
+
+                    c = op.comm
+                    big = float(2 ** 62)
+                    t3 = torch.tensor([gmin, -gmax, float(c.z_lo * c.plane + i) if i >= 0 else big],
+                                      dtype=torch.float64, device=u.device)
+                    c.allreduce(t3, dist.ReduceOp.MIN)
+                    gmin, gmax = float(t3[0]), -float(t3[1])
+                    i = int(t3[2]) if float(t3[2]) < big else -1
+                if i >= 0:
+                    raise DomainError(f"combustion nonlinearity undefined at index {i} (u <= 0)", index=i)
                 self._fused = True
-                return f, gp, mm[0], mm[1]
-            if rc != _lib.ES_ERR_ARG:
+                return f, gp, gmin, gmax
+            if rc != _lib.ES_ERR_ARG or self._dist:
                 _lib.check(rc, "es_rosenbrock_prologue")
             self._fused = False  # not eligible (odd nx, faces, ...): generic path from now on
         g = pr.forcing(u, t)

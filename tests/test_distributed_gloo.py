@@ -1,0 +1,182 @@
+"""Multi-process (gloo, CPU) tests of the slab-decomposition host logic in
+paper_1309_4616_b200/distributed.py: the halo exchange, the rank-ordered
+slice gather, the batched/polled series driver and the transfer ledger.
+
+The node arithmetic is supplied by a CPU test double that restates the C
+ABI's es_leja_dist_* contract with the oracle's stencil (test
+infrastructure only); on a GPU box the same driver runs the CUDA backend.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as orc
+from paper_1309_4616_b200.decomp import TransferLedger
+from paper_1309_4616_b200.distributed import SlabComm, drive_series, global_hash_state
+
+CHUNK = 8
+
+
+class OracleSlabBackend:
+    """CPU restatement of one rank's es_leja_dist_* series (test double)."""
+
+    def __init__(self, spec: orc.StencilSpec, comm: SlabComm):
+        self.spec, self.comm = spec, comm
+        plane = comm.plane
+        self.halo_lo = torch.zeros(plane, dtype=torch.float64) if comm.rank > 0 else None
+        self.halo_hi = torch.zeros(plane, dtype=torch.float64) if comm.rank < comm.world - 1 else None
+
+    def begin(self, v, dd, xi, alpha, shift, tol):
+        self.v = torch.from_numpy(np.ascontiguousarray(v))
+        self.dd, self.xi, self.alpha, self.shift, self.tol = dd, xi, alpha, shift, tol
+        self.w = {0: self.v}
+        self.p = None
+        self.k, self.consecutive, self.done, self.converged = 0, 0, False, False
+        self.term, self.pnorm = float("inf"), 0.0
+        self.nslices = (self.comm.lz + CHUNK - 1) // CHUNK
+
+    def slice_counts(self, comm):
+        t = torch.tensor([self.nslices], dtype=torch.int64)
+        parts = [torch.empty_like(t) for _ in range(comm.world)]
+        dist.all_gather(parts, t)
+        return [int(p.item()) for p in parts]
+
+    def source(self, k):  # like es_leja_dist_source, valid after the decision too
+        return self.w[min(k - 1, self.k)]
+
+    def node(self):
+        out = torch.zeros(2 * self.nslices, dtype=torch.float64)
+        if self.done:
+            return out
+        k = self.k + 1
+        c = self.comm
+        beta = -self.shift - self.xi[k - 1]
+        wk = orc.stencil_fused(self.spec, self.alpha, beta, self.w[k - 1].numpy(), z0=c.z_lo,
+                               halo_lo=None if self.halo_lo is None else self.halo_lo.numpy(),
+                               halo_hi=None if self.halo_hi is None else self.halo_hi.numpy())
+        pold = self.dd[0] * self.v.numpy() if self.p is None else self.p
+        self.pk = pold + self.dd[k] * wk
+        self.wk = wk
+        w3 = wk.reshape(c.lz, -1)
+        p3 = self.pk.reshape(c.lz, -1)
+        for s in range(self.nslices):
+            a, b = s * CHUNK, min(c.lz, (s + 1) * CHUNK)
+            out[2 * s] = float(np.sum(w3[a:b] ** 2))
+            out[2 * s + 1] = float(np.sum(p3[a:b] ** 2))
+        return out
+
+    def decide(self, slices_all):
+        if self.done:
+            return
+        k = self.k + 1
+        sw = float(slices_all[0::2].sum())
+        sp = float(slices_all[1::2].sum())
+        self.w[k] = torch.from_numpy(self.wk)
+        self.p = self.pk
+        self.k = k
+        self.term = abs(self.dd[k]) * np.sqrt(sw)
+        self.pnorm = np.sqrt(sp)
+        stop = False
+        if self.tol > 0:
+            if self.term <= self.tol * self.pnorm:
+                self.consecutive += 1
+                if self.consecutive >= 2:
+                    stop, self.converged = True, True
+            else:
+                self.consecutive = 0
+        if not stop and k >= len(self.dd) - 1:
+            stop, self.converged = True, self.tol == 0
+        self.done = stop
+
+    def poll_state(self):
+        return self.done
+
+    @staticmethod
+    def state_done(token):
+        return token
+
+    def end(self):
+        pass
+
+    def fetch(self):
+        return self.k, self.converged, self.p
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, dims, tol, batch, queue):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nx, ny, nz = dims
+        comm = SlabComm(nx, ny, nz)
+        # halo exchange puts the neighbours' seam planes in place
+        g = np.arange(nx * ny * nz, dtype=np.float64)
+        local = torch.from_numpy(g[comm.z_lo * comm.plane: comm.z_hi * comm.plane].copy())
+        lo = torch.zeros(comm.plane, dtype=torch.float64) if rank > 0 else None
+        hi = torch.zeros(comm.plane, dtype=torch.float64) if rank < world - 1 else None
+        comm.exchange(local, lo, hi)
+        ok_halo = (lo is None or np.array_equal(lo.numpy(), g[(comm.z_lo - 1) * comm.plane: comm.z_lo * comm.plane])) and \
+                  (hi is None or np.array_equal(hi.numpy(), g[comm.z_hi * comm.plane: (comm.z_hi + 1) * comm.plane]))
+        # the series over slabs
+        spec_full = orc.StencilSpec(nx, ny, nz)
+        lo_, hi_ = spec_full.gershgorin()
+        it = orc.interpolant(lo_, hi_, "exp", -2e-3, 30)
+        v = np.random.default_rng(9).standard_normal(nx * ny * nz)
+        be = OracleSlabBackend(spec_full, comm)
+        be.begin(v[comm.z_lo * comm.plane: comm.z_hi * comm.plane], it.dd, it.xi, 1.0 / it.gamma,
+                 it.center / it.gamma, tol)
+        ledger = TransferLedger()
+        k, conv, p = drive_series(be, comm, len(it.dd), batch=batch, ledger=ledger)
+        parts = [None] * world
+        dist.all_gather_object(parts, (comm.z_lo, p))
+        hashes = global_hash_state(nx, ny, nz, comm.z_lo, comm.z_hi, "cpu")
+        hparts = [None] * world
+        dist.all_gather_object(hparts, hashes.numpy())
+        if rank == 0:
+            queue.put((ok_halo, k, conv, [q for _, q in sorted(parts, key=lambda t: t[0])], ledger.last_scalars(),
+                       ledger.apply_count, np.concatenate(hparts)))
+        else:
+            queue.put(("ok", ok_halo))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims,tol,batch", [(2, (12, 10, 16), 0.0, 4), (3, (10, 8, 24), 1e-8, 3)])
+def test_slab_series_matches_single_domain(world, dims, tol, batch):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, tol, batch, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    main = [r for r in results if r[0] != "ok"][0]
+    others = [r for r in results if r[0] == "ok"]
+    ok_halo, k, conv, parts, last, napplies, hashes = main
+    assert ok_halo and all(o[1] for o in others)
+    nx, ny, nz = dims
+    spec = orc.StencilSpec(nx, ny, nz)
+    lo, hi = spec.gershgorin()
+    it = orc.interpolant(lo, hi, "exp", -2e-3, 30)
+    v = np.random.default_rng(9).standard_normal(nx * ny * nz)
+    ref, mv = orc.newton_stencil(spec, it, v, tol)
+    assert k == mv and conv
+    assert np.concatenate(parts).tobytes() == ref.tobytes()  # bitwise, whatever the rank count
+    assert last == 2 * (world - 1) * nx * ny  # reference ledger formula (decomp.py:7-8)
+    assert napplies >= k
+    # the synthetic state does not depend on the partition
+    assert np.array_equal(hashes, global_hash_state(nx, ny, nz, 0, nz, "cpu").numpy())

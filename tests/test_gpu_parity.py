@@ -269,3 +269,102 @@ def test_rosenbrock_domain_error():
     with pytest.raises(es.DomainError) as ei:
         es.exponential_rosenbrock_step(prob, u0, 1e-4, 1e-6)
     assert ei.value.index == 77
+
+
+def _emulated_slab_series(op, it, v, tol, bounds):
+    """Run the C ABI slab series for several slabs of one grid in one process
+    (halo planes copied by hand, slices concatenated in z order)."""
+    import ctypes
+
+    from paper_1309_4616_b200 import _lib
+    from paper_1309_4616_b200.device import ptr, stream_handle
+
+    lib = _lib.load()
+    g = op.grid
+    plane = g.nx * g.ny
+    slabs = []
+    dd, xi = it.device_coeffs()
+    vd = torch.from_numpy(v).cuda()
+    for r, (lo, hi) in enumerate(bounds):
+        d, keep = op.desc(z0=lo, lz=hi - lo)
+        ws = torch.empty(int(lib.es_leja_stencil_workspace_bytes(ctypes.byref(d))), dtype=torch.uint8, device="cuda")
+        hl = torch.zeros(plane, dtype=torch.float64, device="cuda") if lo > 0 else None
+        hh = torch.zeros(plane, dtype=torch.float64, device="cuda") if hi < g.nz else None
+        vs = vd[lo * plane: hi * plane].clone()
+        p = torch.empty_like(vs)
+        _lib.check(lib.es_leja_dist_begin(ctypes.byref(d), ptr(vs), ptr(p), ptr(dd), ptr(xi), dd.numel(),
+                                          1.0 / it.interval.halfspan, it.interval.center / it.interval.halfspan, tol,
+                                          None, ptr(hl), ptr(hh), ptr(ws), ws.numel(), stream_handle()))
+        ns = ctypes.c_int32()
+        _lib.check(lib.es_leja_dist_nslices(ptr(ws), ctypes.byref(ns)))
+        slabs.append(dict(d=d, keep=keep, ws=ws, hl=hl, hh=hh, v=vs, p=p, n=vs.numel(),
+                          sl=torch.empty(2 * ns.value, dtype=torch.float64, device="cuda")))
+
+    def source(s, k):
+        src = ctypes.c_void_p()
+        _lib.check(lib.es_leja_dist_source(ptr(s["ws"]), k, ctypes.byref(src)))
+        if src.value == s["v"].data_ptr():
+            return s["v"]
+        off = src.value - s["ws"].data_ptr()
+        return s["ws"][off: off + 8 * s["n"]].view(torch.float64)
+
+    for k in range(1, len(it.dd)):
+        srcs = [source(s, k) for s in slabs]
+        for r, s in enumerate(slabs):
+            if s["hl"] is not None:
+                s["hl"].copy_(srcs[r - 1][-plane:])
+            if s["hh"] is not None:
+                s["hh"].copy_(srcs[r + 1][:plane])
+        for s in slabs:
+            _lib.check(lib.es_leja_dist_node(ptr(s["ws"]), ptr(s["sl"]), stream_handle()))
+        allsl = torch.cat([s["sl"] for s in slabs])
+        for s in slabs:
+            _lib.check(lib.es_leja_dist_decide(ptr(s["ws"]), ptr(allsl), allsl.numel() // 2, stream_handle()))
+    outs, mvs = [], []
+    for s in slabs:
+        _lib.check(lib.es_leja_dist_end(ptr(s["ws"]), stream_handle()))
+        res = _lib.SeriesResult()
+        lib.es_leja_fetch(ptr(s["ws"]), ctypes.byref(res), stream_handle())
+        outs.append(s["p"].cpu().numpy())
+        mvs.append(res.matvecs)
+    return np.concatenate(outs), mvs
+
+
+@pytest.mark.parametrize("tol", [0.0, 1e-8])
+def test_slab_series_kernels_match_single_domain(tol):
+    # chunk-aligned slabs (multiples of 8 planes): bitwise, matvec counts equal
+    g = es.Grid3D(64, 40, 48)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    it = es.make_interpolant(es.gershgorin_interval(op), "exp", -4e-4, 40, 1e-8)
+    v = np.random.default_rng(21).standard_normal(g.n)
+    ref, mv = es.newton_apply(op, it, v, tol)
+    got, mvs = _emulated_slab_series(op, it, v, tol, [(0, 16), (16, 40), (40, 48)])
+    assert mvs == [mv] * 3
+    assert got.tobytes() == ref.tobytes()
+
+
+def test_distributed_stencil_world1_nccl():
+    import torch.distributed as dist
+
+    from paper_1309_4616_b200.distributed import DistributedStencil
+
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    g = es.Grid3D(64, 32, 24)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    dop = DistributedStencil(op)
+    it = es.make_interpolant(es.gershgorin_interval(op), "phi1", -3e-4, 60, 1e-8)
+    v = torch.from_numpy(np.random.default_rng(2).standard_normal(g.n)).cuda()
+    ref, mv = es.newton_apply(op, it, v, 1e-8)
+    got, mv2 = es.newton_apply(dop, it, v, 1e-8)
+    assert mv2 == mv and torch.equal(got, ref)
+    y = dop.fused_apply_flat(0.5, 2.0, v)
+    assert torch.equal(y, op.fused_apply_flat(0.5, 2.0, v))
+    u0 = 1.0 + 0.1 * torch.rand(g.n, dtype=torch.float64, device="cuda")
+    p1 = es.SemilinearProblem(operator=op, nonlinearity=es.combustion_g, u0=u0)
+    p2 = es.SemilinearProblem(operator=dop, nonlinearity=es.combustion_g, u0=u0)
+    a, sa = es.RosenbrockStepper(p1, 1e-6).step(u0, 0.0, 2e-4)
+    b, sb = es.RosenbrockStepper(p2, 1e-6).step(u0, 0.0, 2e-4)
+    assert sa.matvecs == sb.matvecs and torch.equal(a, b)
