@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the fused Leja-stencil integrator step on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C2|C1|C4] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C2|C1|C4|C5] [--impl b200|reference]
 
 Default workload (N=1): BASELINE.json config 3 -- 512^3 7-point stencil,
 homogeneous Dirichlet, combustion reaction term, exponential Rosenbrock-Euler
@@ -9,7 +9,8 @@ with Leja interpolation, fp64.  One "step" = one integrator step (device
 resident state, all series, nonlinearity, Jacobian and step combination).
 
 metric: Gpts.matvec/s = grid points x Newton-Leja nodes (matvecs) / second,
-whole job.  Also reported: the fused node kernel's achieved HBM GB/s against
+whole job (rows x nodes for the CSR config C5, where a step is one
+phi1(-hA) v Newton-Leja action on a fixed v).  Also reported: the fused node kernel's achieved HBM GB/s against
 MEASURED_PEAKS.json (roofline), the end-to-end number through the public API
 with host buffers (e2e), the reference CPU path on the box's cores
 (cpu_baseline), SM clocks during the timed region.
@@ -52,7 +53,35 @@ CONFIGS = {
     "C4": dict(workload="1024^3 7-point, homogeneous Dirichlet, combustion, exponential Rosenbrock-Euler + Leja",
                dims=(1024, 1024, 1024), bc="homogeneous", coeff=None, method="rosenbrock", h=6.3e-6, tol=1e-4,
                bytes_per_node=40),
+    "C5": dict(workload="CSR n=2^22 synthetic symmetric (6 U(-1,0) couplings/row mirrored, diagonal 12; 5.45e7 nnz), "
+                        "phi1(-hA) v Newton-Leja action",
+               kind="csr", n=2**22, per_row=6, dims=(2**22, 1, 1), bc=None, coeff=None, method="phi1", h=1.0,
+               tol=1e-8, bytes_per_node=None),
 }
+
+
+def is_csr(cfg) -> bool:
+    return cfg.get("kind") == "csr"
+
+
+_CSR_CACHE: dict = {}
+
+
+def csr_matrix(cfg):
+    """The C5 operator (seeded, built once per process)."""
+    from paper_1309_4616_b200.sparse import synthetic_symmetric
+
+    key = (cfg["n"], cfg["per_row"])
+    if key not in _CSR_CACHE:
+        _CSR_CACHE.clear()
+        _CSR_CACHE[key] = synthetic_symmetric(cfg["n"], cfg["per_row"], seed=1234)
+    return _CSR_CACHE[key]
+
+
+def csr_node_bytes(n_rows: int, nnz: int) -> int:
+    """Algorithmic bytes of one CSR Leja node: 8 vals + 4 col per
+    nonzero, 8 (n+1) row_ptr, 8 n x, 8 n w', 16 n p."""
+    return 12 * nnz + 40 * n_rows + 8
 
 
 def parse():
@@ -154,6 +183,8 @@ def reference_node_sample(cfg: dict, nodes: int):
     StencilOperator with the same grid (Dirichlet for Neumann, the sampled D
     array for the radial coefficient, A instead of A - diag g'), the closest
     cost-equivalent of the same hot loop."""
+    if is_csr(cfg):
+        return reference_csr_sample(cfg, nodes)
     nx, ny, nz = cfg["dims"]
     n = nx * ny * nz
     key = (tuple(cfg["dims"]), cfg["coeff"], nodes)
@@ -196,7 +227,49 @@ def reference_node_sample(cfg: dict, nodes: int):
     return dt, n * mv, kind, threads, desc
 
 
+def reference_csr_sample(cfg: dict, nodes: int):
+    """`nodes` fixed-degree Newton-Leja nodes of the reference's newton_apply
+    on its own CsrMatrix of the C5 matrix (compiled core, one core)."""
+    a = csr_matrix(cfg)
+    n = a.nrows
+    cache = _REF_CACHE.setdefault(("csr", n, nodes), {})
+    if "x" not in cache:
+        cache["x"] = np.random.default_rng(1234).standard_normal(n)
+    x = cache["x"]
+    if reference_available():
+        sys.path.insert(0, os.path.join(REPO, "oracle", "_ref"))
+        os.environ.setdefault("EXPSTENCIL_KERNELS", "compiled")
+        import expstencil as ref
+        from expstencil import _kernels
+
+        if "op" not in cache:
+            cache["op"] = ref.CsrMatrix(n, n, a.row_ptr, a.col_idx, a.vals)
+            cache["it"] = ref.make_interpolant(ref.gershgorin_interval(cache["op"]), "phi1", -cfg["h"], nodes,
+                                               cfg["tol"])
+        t0 = time.perf_counter()
+        _, mv = ref.newton_apply(cache["op"], cache["it"], x, 0.0)
+        dt = time.perf_counter() - t0
+        kind, threads = "reference", 1
+        desc = (f"reference newton_apply (expstencil {_kernels.default_backend()} core, oracle/_ref) on its "
+                f"CsrMatrix n={n}, nnz={a.nnz}, fixed degree {mv} (tol=0), phi1")
+    else:
+        from oracle import oracle as orc
+
+        oc = orc.Csr(n, a.row_ptr, a.col_idx, a.vals)
+        lo, hi = oc.gershgorin()
+        it = orc.interpolant(lo, hi, "phi1", -cfg["h"], nodes)
+        t0 = time.perf_counter()
+        _, mv = orc.newton_csr(oc, it, x, 0.0)
+        dt = time.perf_counter() - t0
+        kind, threads = "port", 1
+        desc = f"plain-C oracle port newton series on CSR n={n}, nnz={a.nnz}, fixed degree {mv}"
+    return dt, n * mv, kind, threads, desc
+
+
 def reference_nodes_for(cfg: dict) -> int:
+    if is_csr(cfg):
+        return 8  # ~0.65 s per node on one core at 5.5e7 nonzeros
+
     n = int(np.prod(cfg["dims"]))
     # ~2 s per node at 512^3 on one core: keep each sample at ~10-30 s of CPU
     return max(2, min(40, int(3e8 // max(n, 1))))
@@ -261,8 +334,50 @@ def make_problem(cfg, es, world, use_dist):
     return es.SemilinearProblem(operator=op, nonlinearity=nl, u0=u0), u0
 
 
+def make_csr_problem(cfg, es, use_dist):
+    """(operator, v): the C5 matrix (this rank's row block under torch.distributed)
+    and the fixed series input v ~ N(0, 1) from default_rng(1234) over all rows."""
+    import torch
+
+    from paper_1309_4616_b200.distributed import DistributedCsr
+
+    a = csr_matrix(cfg)
+    v = np.random.default_rng(1234).standard_normal(a.nrows)
+    if use_dist:
+        op = DistributedCsr(a)
+        v = v[op.comm.r_lo: op.comm.r_hi]
+    else:
+        op = a
+    return op, torch.from_numpy(np.ascontiguousarray(v)).cuda()
+
+
+class CsrStepper:
+    """One phi1(-hA) v Newton-Leja action through the public API
+    (es.newton_apply on a CsrMatrix / DistributedCsr); the input is fixed,
+    the output is the action."""
+
+    chain = False
+
+    def __init__(self, cfg, es, op, use_dist=False):
+        self.cfg, self.es, self.op, self.dist = cfg, es, op, use_dist
+        self.h = cfg["h"]
+        self.it = es.make_interpolant(es.gershgorin_interval(op), "phi1", -self.h, 150, cfg["tol"])
+
+    def __call__(self, v, t):
+        from paper_1309_4616_b200.integrator import StepStats
+
+        p, mv = self.es.newton_apply(self.op, self.it, v)
+        return p, StepStats(matvecs=mv)
+
+    def launches(self, stats) -> int:
+        # init + (node + slice reduce) per matvec + finalize; the row-block driver adds a decide per node
+        return 3 * stats.matvecs + 2 if self.dist else 2 * stats.matvecs + 2
+
+
 class Stepper:
     """One integrator step of the configured method through the public API."""
+
+    chain = True
 
     def __init__(self, cfg, es, problem, use_dist=False):
         self.cfg, self.es, self.problem, self.dist = cfg, es, problem, use_dist
@@ -313,6 +428,22 @@ def profiled_traffic(cfg_name: str):
         return None
 
 
+def config_block(args, cfg, n, world, nnz=None):
+    c = {"workload": cfg["workload"], "config": args.config, "method": cfg["method"], "h": cfg["h"],
+         "tol": cfg["tol"]}
+    if nnz is not None:
+        c.update({"rows": n, "nnz": nnz,
+                  "parallelism": f"row blocks x{world} (NCCL all-gather of w)" if world > 1 else "single",
+                  "l2": f"matrix ({12 * nnz / 2**20:.0f} MiB of vals+col) streams from HBM, larger than L2; "
+                        f"the {8 * n / 2**20:.0f} MiB vectors are L2-resident by design (no flush)"})
+        return c
+    c.update({"grid": list(cfg["dims"]), "bc": cfg["bc"], "coeff": cfg["coeff"],
+              "parallelism": f"z-slabs x{world} (NCCL halo exchange)" if world > 1 else "single",
+              "l2": f"inputs larger than L2 ({8 * n / 2**20:.0f} MiB per vector)" if 8 * n >= 2**27
+              else "working set inside L2 (no flush)"})
+    return c
+
+
 def run_b200(args, cfg):
     import torch
     import torch.distributed as dist
@@ -328,10 +459,18 @@ def run_b200(args, cfg):
         os.environ.setdefault("MASTER_PORT", "29541")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
     nx, ny, nz = cfg["dims"]
-    n = nx * ny * nz  # global points
-    problem, u0 = make_problem(cfg, es, world, use_dist)
+    n = nx * ny * nz  # global points (rows for CSR)
+    if is_csr(cfg):
+        op, u0 = make_csr_problem(cfg, es, use_dist)
+        step = CsrStepper(cfg, es, op, use_dist)
+        nnz_local = int(op.vals.shape[0]) if use_dist else op.nnz
+        bytes_node = csr_node_bytes(u0.numel(), nnz_local)
+        nnz_total = csr_matrix(cfg).nnz
+    else:
+        problem, u0 = make_problem(cfg, es, world, use_dist)
+        step = Stepper(cfg, es, problem, use_dist)
+        bytes_node = cfg["bytes_per_node"] * u0.numel()
     n_local = u0.numel()
-    step = Stepper(cfg, es, problem, use_dist)
 
     def barrier():
         if use_dist:
@@ -341,7 +480,8 @@ def run_b200(args, cfg):
     u = u0.clone()
     t = 0.0
     for _ in range(args.warmup):
-        u, _ = step(u, t)
+        out, _ = step(u, t)
+        u = out if step.chain else u
         t += cfg["h"]
     barrier()
     # ---- device-resident timed region ----
@@ -352,7 +492,8 @@ def run_b200(args, cfg):
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
         for _ in range(args.steps):
-            u, st = step(u, t)
+            out, st = step(u, t)
+            u = out if step.chain else u
             t += cfg["h"]
             matvecs += st.matvecs
             launches += step.launches(st)
@@ -373,12 +514,13 @@ def run_b200(args, cfg):
 
     # roofline of the dominant kernel: the fused node (series time / nodes)
     node_s = series_s / max(series_mv, 1)
-    bytes_node = cfg["bytes_per_node"] * n_local
     achieved = bytes_node / node_s / 1e9
     peak, peak_src = measured_peak()
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": profiled_traffic(args.config), "kernel": "k_node3d/k_node2d (fused Leja node)",
-                "bytes_per_point": cfg["bytes_per_node"], "node_us": node_s * 1e6, "peak_source": peak_src,
+                "traffic": profiled_traffic(args.config),
+                "kernel": "k_csr_node (fused CSR Leja node)" if is_csr(cfg) else "k_node_tma (fused Leja node)",
+                "bytes_per_node": bytes_node,
+                "bytes_per_point": bytes_node / n_local, "node_us": node_s * 1e6, "peak_source": peak_src,
                 "series_share_of_step": series_s / elapsed if elapsed > 0 else None}
 
     # ---- end to end through the public API with host buffers ----
@@ -386,6 +528,7 @@ def run_b200(args, cfg):
     if not args.no_e2e:
         pin_in = torch.from_numpy(u.cpu().numpy()).pin_memory()
         pin_out = torch.empty_like(pin_in).pin_memory()
+        fixed_in = pin_in
         e2e_steps = max(3, args.steps // 2)
         mv_e2e = 0
         barrier()
@@ -398,7 +541,7 @@ def run_b200(args, cfg):
             t += cfg["h"]
             pin_out.copy_(ud, non_blocking=True)
             torch.cuda.current_stream().synchronize()
-            pin_in, pin_out = pin_out, pin_in
+            pin_in, pin_out = (pin_out, pin_in) if step.chain else (fixed_in, pin_out)
             mv_e2e += st.matvecs
         e1.record()
         barrier()
@@ -410,6 +553,8 @@ def run_b200(args, cfg):
             e_el = float(b.item())
         e2e = {"value": e_units / e_el / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                "d2h_bytes_per_step": 8 * n, "steps": e2e_steps, "ms_per_step": 1e3 * e_el / e2e_steps}
+        if is_csr(cfg):
+            e2e["note"] = "the matrix is uploaded once (operator set-up); each step copies v in and p out"
         if world > 1:
             e2e["note"] = "each rank copies its own slab; bytes are whole-job"
 
@@ -425,13 +570,11 @@ def run_b200(args, cfg):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
-            "data": ("synthetic: u0 = 1 + 0.1 U[0,1), numpy default_rng(1234) over the global grid" if n <= 2**28
+            "data": ("synthetic: seeded symmetric CSR (default_rng(1234)), v ~ N(0,1) default_rng(1234)"
+                     if is_csr(cfg) else
+                     "synthetic: u0 = 1 + 0.1 U[0,1), numpy default_rng(1234) over the global grid" if n <= 2**28
                      else "synthetic: u0 = 1 + 0.1 hash(global index)"),
-            "config": {"workload": cfg["workload"], "config": args.config, "grid": list(cfg["dims"]),
-                       "bc": cfg["bc"], "coeff": cfg["coeff"], "method": cfg["method"], "h": cfg["h"],
-                       "tol": cfg["tol"], "parallelism": f"z-slabs x{world} (NCCL halo exchange)" if world > 1 else "single",
-                       "l2": f"inputs larger than L2 ({8 * n / 2**20:.0f} MiB per vector)" if 8 * n > 2**27
-                       else "working set inside L2 (no flush)"},
+            "config": config_block(args, cfg, n, world, nnz_total if is_csr(cfg) else None),
             "matvecs_per_step": matvecs / args.steps, "steps_per_s": args.steps / t_max,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             "gpu_launches": launches,

@@ -147,6 +147,32 @@ int es_leja_dist_nslices(const void *workspace, int32_t *nslices_out);
 int es_leja_dist_node(const void *workspace, double *slices_out, void *stream);
 int es_leja_dist_decide(const void *workspace, const double *slices_all, int32_t nslices, void *stream);
 int es_leja_dist_end(const void *workspace, void *stream);
+
+/* Multi-GPU row-block CSR series (decomp.py:285-345, PartitionedCsr._run
+ * :304-333, on one rank per GPU).  Each rank owns rows [r_lo, r_hi) as a
+ * local CSR block (row_ptr rebased to 0, n_local + 1 entries) whose column
+ * indices address x_gathered, the caller-owned buffer of n_gathered doubles
+ * into which every node's source vectors of all ranks are all-gathered
+ * (rank order).
+ * The workspace is es_leja_csr_workspace_bytes(n_local).  Per node k the
+ * caller
+ *   1. all-gathers *es_leja_csr_dist_source(ws, k) (n_local doubles) of every
+ *      rank into x_gathered,
+ *   2. es_leja_csr_dist_node: the local rows' fused pass plus per-chunk
+ *      (16384-row) partial sums (nslices x 2 doubles) into slices_out,
+ *   3. all-gathers the slices of all ranks in rank order and calls
+ *      es_leja_dist_decide (shared with the slab series),
+ * and finally es_leja_csr_dist_end + es_leja_fetch. */
+int es_leja_csr_dist_begin(int64_t n_local, const int64_t *row_ptr, const int32_t *col_idx,
+                           const double *vals, const double *x_gathered, int64_t n_gathered,
+                           const double *v,
+                           double *p_out, const double *dd, const double *xi, int32_t ndd,
+                           double alpha, double shift, double tol, void *workspace,
+                           size_t workspace_bytes, void *stream);
+int es_leja_csr_dist_source(const void *workspace, int32_t k, const double **src_out);
+int es_leja_csr_dist_nslices(const void *workspace, int32_t *nslices_out);
+int es_leja_csr_dist_node(const void *workspace, double *slices_out, void *stream);
+int es_leja_csr_dist_end(const void *workspace, void *stream);
 /* Byte offset of the series state {int k, consecutive, done, converged;
  * double last_term, last_pnorm} inside a series workspace (for asynchronous
  * polling of `done` with a plain device-to-host copy). */

@@ -28,7 +28,8 @@ EXPORTS = (
     "es_half_sum", "es_combustion_jacobian", "es_max_abs", "es_leja_stencil_async", "es_leja_fetch",
     "es_leja_csr_async", "es_rosenbrock_prologue", "es_leja_dist_begin", "es_leja_dist_source",
     "es_leja_dist_nslices", "es_leja_dist_node", "es_leja_dist_decide", "es_leja_dist_end",
-    "es_leja_state_offset",
+    "es_leja_state_offset", "es_leja_csr_dist_begin", "es_leja_csr_dist_source", "es_leja_csr_dist_nslices",
+    "es_leja_csr_dist_node", "es_leja_csr_dist_end",
 )
 
 
@@ -81,6 +82,12 @@ def _declare(lib):
         "es_leja_dist_decide": ([vp, vp, i32, vp], ctypes.c_int),
         "es_leja_dist_end": ([vp, vp], ctypes.c_int),
         "es_leja_state_offset": ([], sz),
+        "es_leja_csr_dist_begin": ([i64, vp, vp, vp, vp, i64, vp, vp, vp, vp, i32, d, d, d, vp, sz, vp],
+                                   ctypes.c_int),
+        "es_leja_csr_dist_source": ([vp, i32, P(vp)], ctypes.c_int),
+        "es_leja_csr_dist_nslices": ([vp, P(i32)], ctypes.c_int),
+        "es_leja_csr_dist_node": ([vp, vp, vp], ctypes.c_int),
+        "es_leja_csr_dist_end": ([vp, vp], ctypes.c_int),
         "es_axpy": ([vp, vp, d, vp, i64, vp], ctypes.c_int),
         "es_scale": ([vp, d, vp, i64, vp], ctypes.c_int),
         "es_half_sum": ([vp, vp, vp, i64, vp], ctypes.c_int),

@@ -212,4 +212,41 @@ extern "C" int es_leja_dist_end(const void *workspace, void *stream) {
     return dist_end(workspace, (cudaStream_t)stream);
 }
 
+extern "C" int es_leja_csr_dist_begin(int64_t n_local, const int64_t *row_ptr, const int32_t *col_idx,
+                                      const double *vals, const double *x_gathered, int64_t n_gathered,
+                                      const double *v, double *p_out,
+                                      const double *dd, const double *xi, int32_t ndd, double alpha, double shift,
+                                      double tol, void *workspace, size_t workspace_bytes, void *stream) {
+    if (n_local < 0) return set_error(ES_ERR_ARG, "negative n_local");
+    if (!v || !p_out || !dd || !xi || !workspace || !x_gathered || (n_local > 0 && (!row_ptr || !col_idx || !vals)))
+        return set_error(ES_ERR_ARG, "null pointer");
+    if (v == p_out) return set_error(ES_ERR_ARG, "p_out must not alias v");
+    if (n_gathered < n_local) return set_error(ES_ERR_ARG, "the gathered vector is shorter than the local block");
+    return csr_dist_begin(n_local, row_ptr, col_idx, vals, x_gathered, n_gathered, v, p_out, dd, xi, ndd, alpha, shift, tol,
+                          workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int es_leja_csr_dist_source(const void *workspace, int32_t k, const double **src_out) {
+    if (!workspace || !src_out) return set_error(ES_ERR_ARG, "null pointer");
+    return csr_dist_source(workspace, k, src_out);
+}
+
+extern "C" int es_leja_csr_dist_nslices(const void *workspace, int32_t *nslices_out) {
+    if (!workspace || !nslices_out) return set_error(ES_ERR_ARG, "null pointer");
+    int n = 0;
+    const int rc = csr_dist_nslices(workspace, &n);
+    *nslices_out = n;
+    return rc;
+}
+
+extern "C" int es_leja_csr_dist_node(const void *workspace, double *slices_out, void *stream) {
+    if (!workspace || !slices_out) return set_error(ES_ERR_ARG, "null pointer");
+    return csr_dist_node(workspace, slices_out, (cudaStream_t)stream);
+}
+
+extern "C" int es_leja_csr_dist_end(const void *workspace, void *stream) {
+    if (!workspace) return set_error(ES_ERR_ARG, "null pointer");
+    return csr_dist_end(workspace, (cudaStream_t)stream);
+}
+
 extern "C" size_t es_leja_state_offset(void) { return series_state_offset(); }

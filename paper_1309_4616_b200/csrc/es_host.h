@@ -12,6 +12,19 @@ namespace es {
 int set_error(int code, const char *fmt, ...);
 int check_launch(const char *what);
 int current_device();
+int env_int(const char *name, int dflt);
+
+// One kernel node of a series loop body; every kernel takes the device
+// SeriesParams pointer as its only argument.
+struct GraphKernel {
+    const void *fn;
+    dim3 grid, block;
+    size_t smem;
+};
+// Cached CUDA graph running `ks` in order inside a conditional WHILE node
+// (graph.cu); nullptr when graphs are disabled (ES_NO_GRAPH=1) or
+// unavailable, in which case the caller launches the nodes itself.
+cudaGraphExec_t series_graph(const GraphKernel *ks, int nk, const void *dparams, unsigned long long *handle);
 
 struct SeriesState;
 SeriesState *series_state_ptr(void *ws);
@@ -59,5 +72,13 @@ int run_csr_series(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
                    const double *v, double *p_out, const double *dd, const double *xi, int ndd,
                    double alpha, double shift, double tol, void *ws, size_t ws_bytes,
                    es_series_result *res, cudaStream_t stream);
+
+int csr_dist_begin(int64_t n_local, const int64_t *row_ptr, const int32_t *col, const double *vals, const double *xg,
+                   int64_t n_xg, const double *v, double *p_out, const double *dd, const double *xi, int ndd, double alpha,
+                   double shift, double tol, void *ws, size_t ws_bytes, cudaStream_t stream);
+int csr_dist_source(const void *ws, int k, const double **src);
+int csr_dist_nslices(const void *ws, int *nslices);
+int csr_dist_node(const void *ws, double *slices_out, cudaStream_t stream);
+int csr_dist_end(const void *ws, cudaStream_t stream);
 
 }  // namespace es

@@ -89,6 +89,10 @@ ES_DEV bool reduce_and_decide(const SeriesParams &P, int k, int chunk, int64_t s
     }
     __threadfence();
     group_sync<NT>();
+    if (P.dist) {  // multi-GPU: the caller gathers the slices of all ranks and decides
+        if (tid == 0) P.chunk_cnt[chunk] = 0u;
+        return false;
+    }
     if (tid == 0) s_last = atomicAdd(P.global_cnt, 1u) == (unsigned)P.nchunks - 1u;
     group_sync<NT>();
     const bool last_chunk = s_last;

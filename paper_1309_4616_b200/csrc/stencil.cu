@@ -212,7 +212,7 @@ __global__ void k_scale_dev(const double *x, const double *s, double *out, int64
 // ---------------------------------------------------------------------------
 // host side
 
-static int env_int(const char *name, int dflt) {
+int env_int(const char *name, int dflt) {
     const char *s = std::getenv(name);
     return s ? std::atoi(s) : dflt;
 }
@@ -596,68 +596,6 @@ size_t stencil_series_ws_bytes(const es_stencil_desc *d) {
                     layout(n, pt.nslices, pt.ntiles, pt.nchunks).total);
 }
 
-// ----- the while-loop graph per (node kernel, launch shape, params slot) -----
-
-struct GraphEntry {
-    cudaGraphExec_t exec = nullptr;
-    cudaGraphConditionalHandle handle = 0;
-};
-
-static std::mutex g_graph_mu;
-static std::map<std::tuple<const void *, unsigned, unsigned, unsigned, size_t, const void *, int>, GraphEntry> g_graphs;
-
-static bool build_while_graph(NodeFn nf, const StencilPlan &pl, const SeriesParams *dparams, GraphEntry &e,
-                              NodeFn rf = nullptr, unsigned rgrid = 0) {
-    cudaGraph_t graph = nullptr;
-    if (cudaGraphCreate(&graph, 0) != cudaSuccess) return false;
-    if (cudaGraphConditionalHandleCreate(&e.handle, graph, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
-        cudaGraphDestroy(graph);
-        return false;
-    }
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = e.handle;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t cnode;
-    if (cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp) != cudaSuccess) {
-        cudaGraphDestroy(graph);
-        return false;
-    }
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    void *args[] = {(void *)&dparams};
-    cudaKernelNodeParams kp = {};
-    kp.func = (void *)nf;
-    kp.gridDim = pl.grid;
-    kp.blockDim = pl.block;
-    kp.sharedMemBytes = (unsigned)pl.smem;
-    kp.kernelParams = args;
-    cudaGraphNode_t knode;
-    if (cudaGraphAddKernelNode(&knode, body, nullptr, 0, &kp) != cudaSuccess) {
-        cudaGraphDestroy(graph);
-        return false;
-    }
-    if (rf) {
-        cudaKernelNodeParams rp = {};
-        rp.func = (void *)rf;
-        rp.gridDim = dim3(rgrid, 1, 1);
-        rp.blockDim = dim3(256, 1, 1);
-        rp.sharedMemBytes = 0;
-        rp.kernelParams = args;
-        cudaGraphNode_t rnode;
-        if (cudaGraphAddKernelNode(&rnode, body, &knode, 1, &rp) != cudaSuccess) {
-            cudaGraphDestroy(graph);
-            return false;
-        }
-    }
-    if (cudaGraphInstantiate(&e.exec, graph, 0) != cudaSuccess) {
-        cudaGraphDestroy(graph);
-        return false;
-    }
-    cudaGraphDestroy(graph);
-    return true;
-}
-
 // Everything a series needs before its first node: plan, kernel, device
 // parameters (published with the state reset), TMA descriptors.
 struct SeriesSetup {
@@ -757,28 +695,16 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, nullptr, nullptr, false, ws,
                             ws_bytes, S, stream);
     if (rc) return rc;
-    GraphEntry *ge = nullptr;
-    if (!env_int("ES_NO_GRAPH", 0)) {
-        std::lock_guard<std::mutex> lk(g_graph_mu);
-        auto key = std::make_tuple((const void *)S.nf, S.lp.grid.x, S.lp.grid.y, S.lp.grid.z, S.lp.smem,
-                                   (const void *)S.dparams, current_device());
-        auto it = g_graphs.find(key);
-        if (it == g_graphs.end()) {
-            GraphEntry e;
-            const bool ok = S.pl.tma
-                                ? build_while_graph(S.nf, S.lp, S.dparams, e, k_slice_reduce, (unsigned)S.pl.nslices)
-                                : build_while_graph(S.nf, S.lp, S.dparams, e);
-            if (ok) it = g_graphs.emplace(key, e).first;
-            else cudaGetLastError();
-        }
-        if (it != g_graphs.end()) ge = &it->second;
-    }
-    if (ge) S.hp.cond = (unsigned long long)ge->handle;
+    GraphKernel gk[2] = {{(const void *)S.nf, S.lp.grid, S.lp.block, S.lp.smem},
+                         {(const void *)k_slice_reduce, dim3((unsigned)S.pl.nslices), dim3(256), 0}};
+    unsigned long long handle = 0;
+    cudaGraphExec_t ge = series_graph(gk, S.pl.tma ? 2 : 1, S.dparams, &handle);
+    if (ge) S.hp.cond = handle;
     k_series_init<<<1, 256, 0, stream>>>(S.hp, S.dparams);
     rc = check_launch("series init");
     if (rc) return rc;
     if (ge) {
-        if (cudaGraphLaunch(ge->exec, stream) != cudaSuccess) return check_launch("series graph");
+        if (cudaGraphLaunch(ge, stream) != cudaSuccess) return check_launch("series graph");
     } else {
         for (int k = 1; k < ndd; ++k) {
             S.nf<<<S.lp.grid, S.lp.block, S.lp.smem, stream>>>(S.dparams);
@@ -862,11 +788,11 @@ __global__ void k_decide_gathered(const SeriesParams *__restrict__ Pp, const dou
     decide_gathered(P, P.state->k + 1, slices, nslices);
 }
 
+// Shared by the slab and the row-block (CSR) series: both workspace layouts
+// keep the device SeriesParams at offset 0.
 int dist_decide(const void *ws, const double *slices_all, int nslices, cudaStream_t stream) {
-    SeriesSetup *S;
-    int rc = dist_get(ws, S);
-    if (rc) return rc;
-    k_decide_gathered<<<1, 32, 0, stream>>>(S->dparams, slices_all, nslices);
+    if (!ws || !slices_all || nslices < 1) return set_error(ES_ERR_ARG, "bad gathered slices");
+    k_decide_gathered<<<1, 32, 0, stream>>>(reinterpret_cast<const SeriesParams *>(ws), slices_all, nslices);
     return check_launch("slab decide");
 }
 

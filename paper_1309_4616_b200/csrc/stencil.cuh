@@ -54,6 +54,8 @@ struct SeriesParams {
     const int64_t *row_ptr;
     const int32_t *col;
     const double *vals;
+    unsigned long long tex[4];  // CSR texture gathers: wbuf[0], wbuf[1], v, xg
+    const double *xg;  // multi-GPU CSR: the all-gathered w_{k-1} the row gathers read (nullptr: the local source)
     int64_t n;
     const void *maps;  // TmaMaps (workspace) for the TMA node kernel
     unsigned *work;    // dynamic work-item counter of the TMA node kernel

@@ -16,6 +16,12 @@ two-phase supersteps).  Here every rank owns one slab in its own HBM:
   do not depend on the rank count (the reference's partition invariance,
   verify.py:90-125).
 
+The CSR operator shards as row blocks (``DistributedCsr``): per node the
+ranks' w_{k-1} slices are all-gathered over NCCL into one gathered vector
+(the reference's private full copy of x per worker, decomp.py:304-333;
+(m-1) n scalars per node), the local rows' fused pass gathers from it, and
+the same rank-ordered slice gather drives the identical stopping test.
+
 The host loop enqueues nodes in batches and polls the device state with an
 asynchronous copy, so no rank waits on a per-node host sync; all ranks see
 the same state at the same batch boundary, which keeps their collectives in
@@ -90,6 +96,53 @@ class SlabComm:
         return 2 * (self.world - 1) * self.plane
 
 
+class RowComm:
+    """Vector all-gather and slice gathering for one rank's row block.
+
+    Row blocks follow make_partition (first `rem` ranks one row larger,
+    decomp.py:58-83).  The gathered vector has one slot of `width` =
+    max(block) doubles per rank, so the exchange is one
+    ncclAllGather (all_gather_into_tensor); column indices are remapped
+    into that padded layout once, when the local block is built (no padding
+    when m divides n, e.g. n = 2^22 at m = 1/2/4/8)."""
+
+    def __init__(self, n: int, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.n_total = int(n)
+        self.partition = make_partition(self.n_total, self.world, mode="csr_rows")
+        rng = self.partition.ranges()
+        self.r_lo, self.r_hi = rng[self.rank]
+        self.counts = [hi - lo for lo, hi in rng]
+        self.starts = np.array([lo for lo, _ in rng], dtype=np.int64)
+        self.width = max(self.counts)
+        self.padded = self.width * self.world
+        self.n_local = self.r_hi - self.r_lo
+
+    def padded_index(self, cols: np.ndarray) -> np.ndarray:
+        """Global column index -> position in the gathered vector."""
+        cols = np.asarray(cols, dtype=np.int64)
+        owner = np.searchsorted(self.starts, cols, side="right") - 1
+        return owner * self.width + (cols - self.starts[owner])
+
+    def exchange(self, src: torch.Tensor, xg: torch.Tensor) -> None:
+        """All ranks' slices of a row-block vector into xg (rank order)."""
+        if self.n_local == self.width:
+            dist.all_gather_into_tensor(xg, src[: self.width], group=self.group)
+        else:
+            buf = torch.zeros(self.width, dtype=src.dtype, device=src.device)
+            buf[: self.n_local] = src
+            dist.all_gather_into_tensor(xg, buf, group=self.group)
+
+    def gather(self, local: torch.Tensor, counts: list[int]) -> torch.Tensor:
+        return SlabComm.gather(self, local, counts)
+
+    def ledger_scalars(self) -> int:
+        # every worker receives the other blocks (decomp.py:323)
+        return (self.world - 1) * self.n_total
+
+
 @dataclass
 class SeriesOutcome:
     matvecs: int
@@ -98,9 +151,10 @@ class SeriesOutcome:
     last_pnorm: float
 
 
-def drive_series(backend, comm: SlabComm, ndd: int, batch: int = 4, ledger: Optional[TransferLedger] = None):
-    """Host loop of a slab series: exchange -> node -> gather -> decide per
-    node, batches of `batch` nodes between asynchronous state polls."""
+def drive_series(backend, comm, ndd: int, batch: int = 4, ledger: Optional[TransferLedger] = None):
+    """Host loop of a multi-GPU series (slab or row block): exchange -> node
+    -> gather -> decide per node, batches of `batch` nodes between
+    asynchronous state polls."""
     counts = backend.slice_counts(comm)
     k, pending = 0, []
     while k < ndd - 1:
@@ -108,7 +162,7 @@ def drive_series(backend, comm: SlabComm, ndd: int, batch: int = 4, ledger: Opti
             if k >= ndd - 1:
                 break
             k += 1
-            comm.exchange(backend.source(k), backend.halo_lo, backend.halo_hi)
+            backend.exchange(k)
             if ledger is not None:
                 ledger.record(comm.ledger_scalars(), 8)
             local = backend.node()
@@ -120,30 +174,29 @@ def drive_series(backend, comm: SlabComm, ndd: int, batch: int = 4, ledger: Opti
     return backend.fetch()
 
 
-class CudaSlabBackend:
-    """The C ABI slab series (es_leja_dist_*) on this rank's GPU."""
+class _CudaSeriesBackend:
+    """Shared part of the C ABI multi-GPU series backends: the slice gather
+    counts, the shared decision (es_leja_dist_decide), asynchronous polling
+    of the device state, fetch."""
 
-    def __init__(self, op: StencilOperator, comm: SlabComm, ws: torch.Tensor, halo_lo, halo_hi):
-        self.op, self.comm, self.ws = op, comm, ws
-        self.halo_lo, self.halo_hi = halo_lo, halo_hi
+    SOURCE = NSLICES = NODE = END = ""
+
+    def __init__(self, comm, ws: torch.Tensor):
+        self.comm, self.ws = comm, ws
         self.lib = _lib.load()
         self._state_off = int(self.lib.es_leja_state_offset())
         self._pinned = [torch.empty(_STATE.size, dtype=torch.uint8).pin_memory() for _ in range(3)]
         self._pi = 0
 
-    def begin(self, d, v, p_out, dd, xi, alpha, shift, tol, gdiag):
+    def _after_begin(self, v):
         self.v = v
         self.n = v.numel()
-        rc = self.lib.es_leja_dist_begin(ctypes.byref(d), ptr(v), ptr(p_out), ptr(dd), ptr(xi), dd.numel(),
-                                         float(alpha), float(shift), float(tol), ptr(gdiag), ptr(self.halo_lo),
-                                         ptr(self.halo_hi), ptr(self.ws), self.ws.numel(), stream_handle())
-        _lib.check(rc, "es_leja_dist_begin")
         ns = ctypes.c_int32()
-        _lib.check(self.lib.es_leja_dist_nslices(ptr(self.ws), ctypes.byref(ns)))
+        _lib.check(getattr(self.lib, self.NSLICES)(ptr(self.ws), ctypes.byref(ns)))
         self.nslices = ns.value
         self.slices = torch.empty(2 * self.nslices, dtype=torch.float64, device=v.device)
 
-    def slice_counts(self, comm: SlabComm):
+    def slice_counts(self, comm):
         t = torch.tensor([self.nslices], dtype=torch.int64, device=self.slices.device)
         parts = [torch.empty_like(t) for _ in range(comm.world)]
         dist.all_gather(parts, t, group=comm.group)
@@ -151,14 +204,14 @@ class CudaSlabBackend:
 
     def source(self, k: int) -> torch.Tensor:
         src = ctypes.c_void_p()
-        _lib.check(self.lib.es_leja_dist_source(ptr(self.ws), k, ctypes.byref(src)))
+        _lib.check(getattr(self.lib, self.SOURCE)(ptr(self.ws), k, ctypes.byref(src)))
         if src.value == self.v.data_ptr():
             return self.v
         off = src.value - self.ws.data_ptr()
         return self.ws[off: off + 8 * self.n].view(torch.float64)
 
     def node(self) -> torch.Tensor:
-        _lib.check(self.lib.es_leja_dist_node(ptr(self.ws), ptr(self.slices), stream_handle()), "es_leja_dist_node")
+        _lib.check(getattr(self.lib, self.NODE)(ptr(self.ws), ptr(self.slices), stream_handle()), self.NODE)
         return self.slices
 
     def decide(self, slices_all: torch.Tensor) -> None:
@@ -180,7 +233,7 @@ class CudaSlabBackend:
         return _STATE.unpack(bytes(buf.numpy()))[2] != 0
 
     def end(self):
-        _lib.check(self.lib.es_leja_dist_end(ptr(self.ws), stream_handle()), "es_leja_dist_end")
+        _lib.check(getattr(self.lib, self.END)(ptr(self.ws), stream_handle()), self.END)
 
     def fetch(self):
         res = _lib.SeriesResult()
@@ -188,6 +241,50 @@ class CudaSlabBackend:
         if rc != _lib.ES_ERR_NOT_CONVERGED:
             _lib.check(rc, "es_leja_fetch")
         return res
+
+
+class CudaSlabBackend(_CudaSeriesBackend):
+    """The C ABI slab series (es_leja_dist_*) on this rank's GPU."""
+
+    SOURCE, NSLICES, NODE, END = "es_leja_dist_source", "es_leja_dist_nslices", "es_leja_dist_node", "es_leja_dist_end"
+
+    def __init__(self, op: StencilOperator, comm: SlabComm, ws: torch.Tensor, halo_lo, halo_hi):
+        super().__init__(comm, ws)
+        self.op = op
+        self.halo_lo, self.halo_hi = halo_lo, halo_hi
+
+    def begin(self, d, v, p_out, dd, xi, alpha, shift, tol, gdiag):
+        rc = self.lib.es_leja_dist_begin(ctypes.byref(d), ptr(v), ptr(p_out), ptr(dd), ptr(xi), dd.numel(),
+                                         float(alpha), float(shift), float(tol), ptr(gdiag), ptr(self.halo_lo),
+                                         ptr(self.halo_hi), ptr(self.ws), self.ws.numel(), stream_handle())
+        _lib.check(rc, "es_leja_dist_begin")
+        self._after_begin(v)
+
+    def exchange(self, k: int) -> None:
+        self.comm.exchange(self.source(k), self.halo_lo, self.halo_hi)
+
+
+class CudaRowBackend(_CudaSeriesBackend):
+    """The C ABI row-block CSR series (es_leja_csr_dist_*) on this rank's GPU."""
+
+    SOURCE, NSLICES, NODE, END = ("es_leja_csr_dist_source", "es_leja_csr_dist_nslices", "es_leja_csr_dist_node",
+                                  "es_leja_csr_dist_end")
+
+    def __init__(self, op: "DistributedCsr", ws: torch.Tensor):
+        super().__init__(op.comm, ws)
+        self.op = op
+
+    def begin(self, v, p_out, dd, xi, alpha, shift, tol):
+        rp, col, vals = self.op.device_arrays()
+        rc = self.lib.es_leja_csr_dist_begin(self.op.n, ptr(rp), ptr(col), ptr(vals), ptr(self.op.xg),
+                                             self.op.xg.numel(), ptr(v),
+                                             ptr(p_out), ptr(dd), ptr(xi), dd.numel(), float(alpha), float(shift),
+                                             float(tol), ptr(self.ws), self.ws.numel(), stream_handle())
+        _lib.check(rc, "es_leja_csr_dist_begin")
+        self._after_begin(v)
+
+    def exchange(self, k: int) -> None:
+        self.comm.exchange(self.source(k), self.op.xg)
 
 
 class DistributedStencil:
@@ -262,6 +359,84 @@ class DistributedStencil:
         prologue passes that read x's neighbours)."""
         self.comm.exchange(x, self.halo_lo, self.halo_hi)
         self.ledger.record(self.comm.ledger_scalars(), 8)
+
+
+class DistributedCsr:
+    """One rank's row block of a square CSR operator over torch.distributed
+    (the multi-process form of decomp.PartitionedCsr); same operator
+    protocol, vectors are the local rows (``n`` = local row count)."""
+
+    def __init__(self, a, group=None, ledger: Optional[TransferLedger] = None, batch: int = 4):
+        if a.nrows != a.ncols:
+            raise ValueError("partitioned apply requires a square matrix")
+        if a.vals.dtype != np.float64:
+            raise NotImplementedError("device CSR supports real fp64 values")
+        self.base_operator = a
+        self.comm = RowComm(a.nrows, group)
+        c = self.comm
+        if c.padded > 2**31 - 1:
+            raise NotImplementedError("device CSR needs 32-bit column indices")
+        k0, k1 = int(a.row_ptr[c.r_lo]), int(a.row_ptr[c.r_hi])
+        self.row_ptr = np.ascontiguousarray(a.row_ptr[c.r_lo: c.r_hi + 1] - k0)
+        self.col_idx = np.ascontiguousarray(c.padded_index(a.col_idx[k0:k1]).astype(np.int32))
+        self.vals = np.ascontiguousarray(a.vals[k0:k1])
+        self.ledger = ledger if ledger is not None else TransferLedger()
+        self.batch = batch
+        self._dev = None
+        self._ws = None
+        self._xg = None
+
+    @property
+    def n(self) -> int:
+        return self.comm.n_local
+
+    @property
+    def xg(self) -> torch.Tensor:
+        if self._xg is None:
+            self._xg = torch.zeros(self.comm.padded, dtype=torch.float64, device="cuda")
+        return self._xg
+
+    def device_arrays(self):
+        if self._dev is None:
+            self._dev = (torch.from_numpy(self.row_ptr).cuda(), torch.from_numpy(self.col_idx).cuda(),
+                         torch.from_numpy(self.vals).cuda())
+        return self._dev
+
+    def local_slice(self, x_global):
+        return x_global[self.comm.r_lo: self.comm.r_hi]
+
+    def fused_apply_flat(self, alpha, beta, x: torch.Tensor) -> torch.Tensor:
+        """alpha A x + beta x on the local rows: gather, then the local block
+        (alpha * acc), then + beta x with the reference's rounding order."""
+        if tuple(x.shape) != (self.n,):
+            raise GridMismatchError(f"local vector length {tuple(x.shape)} != {self.n}")
+        self.comm.exchange(x, self.xg)
+        self.ledger.record(self.comm.ledger_scalars(), 8)
+        rp, col, vals = self.device_arrays()
+        y = torch.empty_like(x)
+        lib = _lib.load()
+        _lib.check(lib.es_csr_fused_rows(0, self.n, ptr(rp), ptr(col), ptr(vals), ptr(self.xg), ptr(y),
+                                         float(alpha), 0.0, 0, stream_handle()), "es_csr_fused_rows")
+        _lib.check(lib.es_axpy(ptr(y), ptr(x), float(beta), ptr(y), self.n, stream_handle()), "es_axpy")
+        return y
+
+    def _workspace(self):
+        nbytes = int(_lib.load().es_leja_csr_workspace_bytes(self.n))
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        return self._ws
+
+    def _leja(self, v, p_out, dd, xi, alpha, shift, tol, gdiag=None):
+        if gdiag is not None:
+            raise NotImplementedError("a Jacobian diagonal is defined for stencil operators only")
+        be = CudaRowBackend(self, self._workspace())
+        tm = timing.active()
+        ev0 = timing.event() if tm else None
+        be.begin(v, p_out, dd, xi, alpha, shift, tol)
+        res = drive_series(be, self.comm, dd.numel(), self.batch, self.ledger)
+        if tm:
+            tm.add(ev0, timing.event(), res.matvecs)
+        return res
 
 
 def global_hash_state(nx: int, ny: int, nz: int, z_lo: int, z_hi: int, device) -> torch.Tensor:

@@ -37,3 +37,14 @@ def oracle():
 
 def coeff_d(x, y, z):
     return 1.0 / np.sqrt(1.0 + x * x + y * y)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Tear down the world-size-1 NCCL group some GPU tests create."""
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:  # pragma: no cover - best effort at exit
+        pass

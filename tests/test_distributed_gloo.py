@@ -18,7 +18,8 @@ import torch.multiprocessing as mp
 
 from oracle import oracle as orc
 from paper_1309_4616_b200.decomp import TransferLedger
-from paper_1309_4616_b200.distributed import SlabComm, drive_series, global_hash_state
+from paper_1309_4616_b200.distributed import DistributedCsr, RowComm, SlabComm, drive_series, global_hash_state
+from paper_1309_4616_b200.sparse import synthetic_symmetric
 
 CHUNK = 8
 
@@ -50,6 +51,9 @@ class OracleSlabBackend:
     def source(self, k):  # like es_leja_dist_source, valid after the decision too
         return self.w[min(k - 1, self.k)]
 
+    def exchange(self, k):
+        self.comm.exchange(self.source(k), self.halo_lo, self.halo_hi)
+
     def node(self):
         out = torch.zeros(2 * self.nslices, dtype=torch.float64)
         if self.done:
@@ -72,27 +76,7 @@ class OracleSlabBackend:
         return out
 
     def decide(self, slices_all):
-        if self.done:
-            return
-        k = self.k + 1
-        sw = float(slices_all[0::2].sum())
-        sp = float(slices_all[1::2].sum())
-        self.w[k] = torch.from_numpy(self.wk)
-        self.p = self.pk
-        self.k = k
-        self.term = abs(self.dd[k]) * np.sqrt(sw)
-        self.pnorm = np.sqrt(sp)
-        stop = False
-        if self.tol > 0:
-            if self.term <= self.tol * self.pnorm:
-                self.consecutive += 1
-                if self.consecutive >= 2:
-                    stop, self.converged = True, True
-            else:
-                self.consecutive = 0
-        if not stop and k >= len(self.dd) - 1:
-            stop, self.converged = True, self.tol == 0
-        self.done = stop
+        _decide(self, slices_all)
 
     def poll_state(self):
         return self.done
@@ -106,6 +90,138 @@ class OracleSlabBackend:
 
     def fetch(self):
         return self.k, self.converged, self.p
+
+
+def _decide(self, slices_all):
+    if self.done:
+        return
+    k = self.k + 1
+    sw = float(slices_all[0::2].sum())
+    sp = float(slices_all[1::2].sum())
+    self.w[k] = torch.from_numpy(self.wk)
+    self.p = self.pk
+    self.k = k
+    self.term = abs(self.dd[k]) * np.sqrt(sw)
+    self.pnorm = np.sqrt(sp)
+    stop = False
+    if self.tol > 0:
+        if self.term <= self.tol * self.pnorm:
+            self.consecutive += 1
+            if self.consecutive >= 2:
+                stop, self.converged = True, True
+        else:
+            self.consecutive = 0
+    if not stop and k >= len(self.dd) - 1:
+        stop, self.converged = True, self.tol == 0
+    self.done = stop
+
+
+class OracleRowBackend:
+    """CPU restatement of one rank's es_leja_csr_dist_* series (test double):
+    the local block of a DistributedCsr, gathers from the all-gathered
+    vector, per-chunk slices."""
+
+    def __init__(self, op: DistributedCsr):
+        self.op, self.comm = op, op.comm
+        self.xg = torch.zeros(op.comm.padded, dtype=torch.float64)
+        self.local = orc.Csr(op.n, op.row_ptr, op.col_idx, op.vals)
+
+    def begin(self, v, dd, xi, alpha, shift, tol):
+        self.v = torch.from_numpy(np.ascontiguousarray(v))
+        self.dd, self.xi, self.alpha, self.shift, self.tol = dd, xi, alpha, shift, tol
+        self.w = {0: self.v}
+        self.p = None
+        self.k, self.consecutive, self.done, self.converged = 0, 0, False, False
+        self.nslices = (self.comm.n_local + CHUNK - 1) // CHUNK
+
+    slice_counts = OracleSlabBackend.slice_counts
+    source = OracleSlabBackend.source
+    decide = _decide
+    poll_state = OracleSlabBackend.poll_state
+    state_done = staticmethod(OracleSlabBackend.state_done)
+    end = OracleSlabBackend.end
+    fetch = OracleSlabBackend.fetch
+
+    def exchange(self, k):
+        self.comm.exchange(self.source(k), self.xg)
+
+    def node(self):
+        out = torch.zeros(2 * self.nslices, dtype=torch.float64)
+        if self.done:
+            return out
+        k = self.k + 1
+        beta = -self.shift - self.xi[k - 1]
+        acc = orc.csr_fused(self.local, self.alpha, 0.0, self.xg.numpy(), use_beta=False)
+        wk = acc + beta * self.w[k - 1].numpy()  # alpha * acc + beta * x[r] (_core.pyx:257)
+        pold = self.dd[0] * self.v.numpy() if self.p is None else self.p
+        self.pk = pold + self.dd[k] * wk
+        self.wk = wk
+        for s in range(self.nslices):
+            a, b = s * CHUNK, min(self.comm.n_local, (s + 1) * CHUNK)
+            out[2 * s] = float(np.sum(wk[a:b] ** 2))
+            out[2 * s + 1] = float(np.sum(self.pk[a:b] ** 2))
+        return out
+
+
+def _row_worker(rank, world, port, n, tol, batch, queue):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = synthetic_symmetric(n, 3, seed=5)
+        op = DistributedCsr(a)
+        c = op.comm
+        # the all-gather puts every block at its padded slot
+        g = torch.arange(n, dtype=torch.float64) + 1.0
+        xg = torch.zeros(c.padded, dtype=torch.float64)
+        c.exchange(g[c.r_lo: c.r_hi].clone(), xg)
+        pos = c.padded_index(np.arange(n))
+        ok_gather = np.array_equal(xg.numpy()[pos], g.numpy())
+        # the local block addresses the gathered vector like the global matrix addresses x
+        k0, k1 = a.row_ptr[c.r_lo], a.row_ptr[c.r_hi]
+        ok_block = np.array_equal(xg.numpy()[op.col_idx], g.numpy()[a.col_idx[k0:k1]])
+        lo, hi = orc.Csr(n, a.row_ptr, a.col_idx.astype(np.int32), a.vals).gershgorin()
+        it = orc.interpolant(lo, hi, "phi1", -0.5, 40)
+        v = np.random.default_rng(4).standard_normal(n)
+        be = OracleRowBackend(op)
+        be.begin(v[c.r_lo: c.r_hi], it.dd, it.xi, 1.0 / it.gamma, it.center / it.gamma, tol)
+        ledger = TransferLedger()
+        k, conv, p = drive_series(be, c, len(it.dd), batch=batch, ledger=ledger)
+        parts = [None] * world
+        dist.all_gather_object(parts, (c.r_lo, p))
+        if rank == 0:
+            queue.put((ok_gather and ok_block, k, conv, [q for _, q in sorted(parts, key=lambda t: t[0])],
+                       ledger.last_scalars()))
+        else:
+            queue.put(("ok", ok_gather and ok_block))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,tol,batch", [(2, 64, 0.0, 4), (3, 50, 1e-10, 3)])
+def test_row_block_series_matches_single_matrix(world, n, tol, batch):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_row_worker, args=(r, world, port, n, tol, batch, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    main = [r for r in results if r[0] != "ok"][0]
+    others = [r for r in results if r[0] == "ok"]
+    ok, k, conv, parts, last = main
+    assert ok and all(o[1] for o in others)
+    a = synthetic_symmetric(n, 3, seed=5)
+    ac = orc.Csr(n, a.row_ptr, a.col_idx.astype(np.int32), a.vals)
+    lo, hi = ac.gershgorin()
+    it = orc.interpolant(lo, hi, "phi1", -0.5, 40)
+    v = np.random.default_rng(4).standard_normal(n)
+    ref, mv = orc.newton_csr(ac, it, v, tol)
+    assert k == mv and conv
+    assert np.concatenate(parts).tobytes() == ref.tobytes()  # bitwise, whatever the rank count
+    assert last == (world - 1) * n  # reference ledger formula (decomp.py:323)
 
 
 def _free_port():

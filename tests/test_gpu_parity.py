@@ -368,3 +368,163 @@ def test_distributed_stencil_world1_nccl():
     a, sa = es.RosenbrockStepper(p1, 1e-6).step(u0, 0.0, 2e-4)
     b, sb = es.RosenbrockStepper(p2, 1e-6).step(u0, 0.0, 2e-4)
     assert sa.matvecs == sb.matvecs and torch.equal(a, b)
+
+
+def _orc_csr(a):
+    return orc.Csr(a.nrows, a.row_ptr, a.col_idx.astype(np.int32), a.vals)
+
+
+def _irregular_csr(n=3000, long_row=9000, seed=3):
+    """Empty rows, a row longer than one staging round (4096 products), a
+    ragged tail tile (n % 256 != 0)."""
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for r in range(n):
+        if r % 7 == 3:
+            continue  # empty row
+        k = long_row if r == 1234 else int(rng.integers(1, 40))
+        c = np.unique(rng.integers(0, n, size=min(k, n)))
+        rows.append(np.full(len(c), r))
+        cols.append(c)
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    vals = rng.standard_normal(len(rows))
+    return es.CsrMatrix.from_coo(n, n, rows, cols, vals)
+
+
+@pytest.mark.parametrize("n,long_row", [(3000, 2999), (20000, 20000)])
+def test_csr_apply_irregular_rows_bitwise(n, long_row):
+    a = _irregular_csr(n, long_row)
+    x = np.random.default_rng(1).standard_normal(n)
+    got = a.fused_apply_flat(0.3, -2.5, x)
+    assert got.tobytes() == orc.csr_fused(_orc_csr(a), 0.3, -2.5, x).tobytes()
+    got = es.spmv(a, x)
+    assert got.tobytes() == orc.csr_fused(_orc_csr(a), 1.0, 0.0, x, use_beta=False).tobytes()
+
+
+@pytest.mark.parametrize("graph", [True, False])
+@pytest.mark.parametrize("tol", [0.0, 1e-8])
+def test_csr_series_vs_oracle(graph, tol, monkeypatch):
+    if not graph:
+        monkeypatch.setenv("ES_NO_GRAPH", "1")
+    from paper_1309_4616_b200.sparse import synthetic_symmetric
+
+    a = synthetic_symmetric(300_001, 6, seed=11)
+    oc = _orc_csr(a)
+    lo, hi = oc.gershgorin()
+    iv = es.gershgorin_interval(a)
+    assert (iv.a, iv.b) == (lo, hi)
+    it = es.make_interpolant(iv, "phi1", -1.0, 60, 1e-8)
+    it_o = orc.Interp(lo, hi, "phi1", -1.0, it.xi, it.dd)
+    v = np.random.default_rng(5).standard_normal(a.nrows)
+    ref, mv_ref = orc.newton_csr(oc, it_o, v, tol)
+    got, mv = es.newton_apply(a, it, v, tol)
+    assert mv == mv_ref
+    assert got.tobytes() == ref.tobytes()
+
+
+def test_csr_series_irregular_rows_bitwise():
+    a = _irregular_csr(20000, 20000, seed=8)
+    oc = _orc_csr(a)
+    lo, hi = oc.gershgorin()
+    it = es.make_interpolant(es.gershgorin_interval(a), "exp", -1e-3, 60, 1e-8)
+    it_o = orc.Interp(lo, hi, "exp", -1e-3, it.xi, it.dd)
+    v = np.random.default_rng(6).standard_normal(a.nrows)
+    ref, mv_ref = orc.newton_csr(oc, it_o, v, 1e-10)
+    got, mv = es.newton_apply(a, it, v, 1e-10)
+    assert mv == mv_ref and got.tobytes() == ref.tobytes()
+
+
+def _emulated_row_series(a, it, v, tol, bounds):
+    """The C ABI row-block series (es_leja_csr_dist_*) for several row blocks
+    of one matrix in one process: the gathered vector is assembled by hand
+    (global column indices address it directly), slices concatenated in
+    block order."""
+    import ctypes
+
+    from paper_1309_4616_b200 import _lib
+    from paper_1309_4616_b200.device import ptr, stream_handle
+
+    lib = _lib.load()
+    dd, xi = it.device_coeffs()
+    xg = torch.zeros(a.nrows, dtype=torch.float64, device="cuda")
+    blocks = []
+    for lo, hi in bounds:
+        k0, k1 = int(a.row_ptr[lo]), int(a.row_ptr[hi])
+        rp = torch.from_numpy(a.row_ptr[lo: hi + 1] - k0).cuda()
+        col = torch.from_numpy(a.col_idx[k0:k1].astype(np.int32)).cuda()
+        vals = torch.from_numpy(a.vals[k0:k1].copy()).cuda()
+        n = hi - lo
+        vs = torch.from_numpy(v[lo:hi].copy()).cuda()
+        p = torch.empty_like(vs)
+        ws = torch.empty(int(lib.es_leja_csr_workspace_bytes(n)), dtype=torch.uint8, device="cuda")
+        _lib.check(lib.es_leja_csr_dist_begin(n, ptr(rp), ptr(col), ptr(vals), ptr(xg), xg.numel(), ptr(vs), ptr(p),
+                                              ptr(dd),
+                                              ptr(xi), dd.numel(), 1.0 / it.interval.halfspan,
+                                              it.interval.center / it.interval.halfspan, tol, ptr(ws), ws.numel(),
+                                              stream_handle()))
+        ns = ctypes.c_int32()
+        _lib.check(lib.es_leja_csr_dist_nslices(ptr(ws), ctypes.byref(ns)))
+        blocks.append(dict(keep=(rp, col, vals), ws=ws, v=vs, p=p, n=n, lo=lo, hi=hi,
+                           sl=torch.empty(2 * ns.value, dtype=torch.float64, device="cuda")))
+
+    def source(b, k):
+        src = ctypes.c_void_p()
+        _lib.check(lib.es_leja_csr_dist_source(ptr(b["ws"]), k, ctypes.byref(src)))
+        if src.value == b["v"].data_ptr():
+            return b["v"]
+        off = src.value - b["ws"].data_ptr()
+        return b["ws"][off: off + 8 * b["n"]].view(torch.float64)
+
+    for k in range(1, len(it.dd)):
+        for b in blocks:
+            xg[b["lo"]: b["hi"]].copy_(source(b, k))
+        for b in blocks:
+            _lib.check(lib.es_leja_csr_dist_node(ptr(b["ws"]), ptr(b["sl"]), stream_handle()))
+        allsl = torch.cat([b["sl"] for b in blocks])
+        for b in blocks:
+            _lib.check(lib.es_leja_dist_decide(ptr(b["ws"]), ptr(allsl), allsl.numel() // 2, stream_handle()))
+    outs, mvs = [], []
+    for b in blocks:
+        _lib.check(lib.es_leja_csr_dist_end(ptr(b["ws"]), stream_handle()))
+        res = _lib.SeriesResult()
+        lib.es_leja_fetch(ptr(b["ws"]), ctypes.byref(res), stream_handle())
+        outs.append(b["p"].cpu().numpy())
+        mvs.append(res.matvecs)
+    return np.concatenate(outs), mvs
+
+
+@pytest.mark.parametrize("tol", [0.0, 1e-8])
+def test_row_block_series_kernels_match_single_matrix(tol):
+    # blocks aligned to the 16384-row reduction chunks: bitwise, equal matvec counts
+    from paper_1309_4616_b200.sparse import synthetic_symmetric
+
+    n = 3 * 16384 + 777
+    a = synthetic_symmetric(n, 5, seed=2)
+    it = es.make_interpolant(es.gershgorin_interval(a), "phi1", -0.7, 50, 1e-8)
+    v = np.random.default_rng(3).standard_normal(n)
+    ref, mv = es.newton_apply(a, it, v, tol)
+    got, mvs = _emulated_row_series(a, it, v, tol, [(0, 16384), (16384, 49152), (49152, n)])
+    assert mvs == [mv] * 3
+    assert got.tobytes() == ref.tobytes()
+
+
+def test_distributed_csr_world1_nccl():
+    import torch.distributed as dist
+
+    from paper_1309_4616_b200.distributed import DistributedCsr
+    from paper_1309_4616_b200.sparse import synthetic_symmetric
+
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    a = synthetic_symmetric(70_000, 6, seed=4)
+    dop = DistributedCsr(a)
+    it = es.make_interpolant(es.gershgorin_interval(a), "phi1", -1.0, 80, 1e-8)
+    v = torch.from_numpy(np.random.default_rng(2).standard_normal(a.nrows)).cuda()
+    ref, mv = es.newton_apply(a, it, v, 1e-8)
+    got, mv2 = es.newton_apply(dop, it, v, 1e-8)
+    assert mv2 == mv and torch.equal(got, ref)
+    y = dop.fused_apply_flat(0.5, 2.0, v)
+    assert torch.equal(y, a.fused_apply_flat(0.5, 2.0, v))
+    assert dop.ledger.last_scalars() == 0  # one rank: nothing crosses a link

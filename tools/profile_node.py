@@ -18,6 +18,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--nodes", type=int, default=6)
 a = ap.parse_args()
+if a.config == "C5":
+    from paper_1309_4616_b200.sparse import synthetic_symmetric
+
+    m = synthetic_symmetric(2**22, 6, seed=1234)
+    it = es.make_interpolant(es.gershgorin_interval(m), "phi1", -1.0, a.nodes, 1e-8)
+    v = torch.rand(m.nrows, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        p, mv = es.newton_apply(m, it, v, 0.0)
+    torch.cuda.synchronize()
+    print("nodes", mv)
+    sys.exit(0)
 dims = {"C3": (512, 512, 512), "C2": (4096, 4096, 1), "C4": (1024, 1024, 1024)}[a.config]
 g = es.Grid3D(*dims)
 bc = es.BoundaryCondition.neumann() if a.config == "C2" else es.BoundaryCondition.homogeneous()
