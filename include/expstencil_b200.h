@@ -125,6 +125,33 @@ int es_leja_csr_async(int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
                       const double *xi, int32_t ndd, double alpha, double shift, double tol,
                       void *workspace, size_t workspace_bytes, void *stream);
 
+/* Complex CSR (the reference's propagate path, cli.py:304-357; its compiled
+ * core _core.pyx:263-278).  Complex arrays are interleaved (re, im) doubles
+ * (C99 double complex / numpy complex128 layout); vals are real
+ * (vals_complex = 0) or interleaved complex.  alpha / beta are complex
+ * scalars given as (re, im) parts. */
+int es_csr_fused_rows_z(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr,
+                        const int32_t *col_idx, const double *vals, int32_t vals_complex,
+                        const double *x, double *y, double alpha_re, double alpha_im,
+                        double beta_re, double beta_im, int32_t use_beta, void *stream);
+
+/* Complex Newton-Leja series: p = sum_k dd_k w_k with complex dd (ndd
+ * interleaved values), w_k = (alpha A + beta_k) w_{k-1}, complex alpha (the
+ * reference's op_alpha: 1/gamma, or -1j/gamma on an imaginary-axis interval),
+ * real beta_k = -shift - xi[k-1]; ddabs[k] = |dd_k| as the host computed it
+ * (numpy abs) drives the stopping test.  Same semantics as es_leja_csr. */
+size_t es_leja_csr_z_workspace_bytes(int64_t n);
+int es_leja_csr_z(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *vals,
+                  int32_t vals_complex, const double *v, double *p_out, const double *dd,
+                  const double *ddabs, const double *xi, int32_t ndd, double alpha_re,
+                  double alpha_im, double shift, double tol, void *workspace,
+                  size_t workspace_bytes, es_series_result *result_host, void *stream);
+int es_leja_csr_z_async(int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                        const double *vals, int32_t vals_complex, const double *v, double *p_out,
+                        const double *dd, const double *ddabs, const double *xi, int32_t ndd,
+                        double alpha_re, double alpha_im, double shift, double tol,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
 /* Multi-GPU slab series (decomp.py:146-266 / :368-382 on one rank per GPU).
  * The series state lives on every rank; per node k = 1, 2, ... the caller
  *   1. sends the first/last plane of *es_leja_dist_source(ws, k) to the

@@ -237,6 +237,99 @@ int orc_newton_csr(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
     return tol == 0 ? 0 : 2;
 }
 
+/* ---- complex CSR (the propagate path, cli.py:304-357) -------------------
+ * Vectors are interleaved (re, im) pairs.  Two complex products appear:
+ *   cmul_c: the reference's compiled core, C99 `double complex` a*b under
+ *           -ffp-contract=off (_core.pyx:263-278, GCC lowering):
+ *           (a.r b.r - a.i b.i, a.r b.i + a.i b.r), a real vals[k] promoted
+ *           to (v, 0) first (Cython __pyx_t_double_complex_from_parts);
+ *   cmul_np: numpy's complex128 multiply as measured on this build
+ *           (p += dd[k] * w, matfunc.py:300):
+ *           (fma(a.r, b.r, -(a.i b.i)), fma(a.r, b.i, a.i b.r)). */
+static inline void cmul_c(double ar, double ai, double br, double bi, double *cr, double *ci) {
+    double ac = ar * br, bd = ai * bi, ad = ar * bi, bc = ai * br;
+    *cr = ac - bd;
+    *ci = ad + bc;
+}
+static inline void cmul_np(double ar, double ai, double br, double bi, double *cr, double *ci) {
+    *cr = fma(ar, br, -(ai * bi));
+    *ci = fma(ar, bi, ai * br);
+}
+
+/* y[r] = alpha (sum_k vals[k] x[col[k]]) (+ beta x[r]); vals real
+ * (vals_complex = 0) or interleaved complex; alpha, beta complex. */
+void orc_csr_fused_rows_z(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr, const int32_t *col,
+                          const double *vals, int vals_complex, const double *x, double *y, double alpha_r,
+                          double alpha_i, double beta_r, double beta_i, int use_beta) {
+#pragma omp parallel for schedule(static)
+    for (int64_t r = row_lo; r < row_hi; ++r) {
+        double acc_r = 0.0, acc_i = 0.0;
+        for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+            const double vr = vals_complex ? vals[2 * k] : vals[k], vi = vals_complex ? vals[2 * k + 1] : 0.0;
+            double pr, pi;
+            cmul_c(vr, vi, x[2 * (int64_t)col[k]], x[2 * (int64_t)col[k] + 1], &pr, &pi);
+            acc_r = acc_r + pr;
+            acc_i = acc_i + pi;
+        }
+        double yr, yi;
+        cmul_c(alpha_r, alpha_i, acc_r, acc_i, &yr, &yi);
+        if (use_beta) {
+            double br, bi;
+            cmul_c(beta_r, beta_i, x[2 * r], x[2 * r + 1], &br, &bi);
+            yr = yr + br;
+            yi = yi + bi;
+        }
+        y[2 * r] = yr;
+        y[2 * r + 1] = yi;
+    }
+}
+
+/* Complex Newton-Leja series (matfunc.py:271-318 with complex dd / v):
+ * w_k = (alpha A + beta_k) w_{k-1} through the complex core, p += dd_k w_k
+ * with numpy's product, term = |dd_k| ||w_k|| (ddabs = numpy abs(dd)).
+ * ws: 4n doubles. */
+int orc_newton_csr_z(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *vals, int vals_complex,
+                     const double *v, double *p, const double *dd, const double *ddabs, const double *xi,
+                     int32_t ndd, double alpha_r, double alpha_i, double shift, double tol, double *ws,
+                     int32_t *matvecs, double *last_term, double *last_pnorm) {
+    double *wa = ws, *wb = ws + 2 * n;
+    *matvecs = 0;
+    *last_term = INFINITY;
+    *last_pnorm = 0.0;
+    for (int64_t i = 0; i < n; ++i) cmul_np(dd[0], dd[1], v[2 * i], v[2 * i + 1], &p[2 * i], &p[2 * i + 1]);
+    if (ndd == 1) return 0;
+    const double *wsrc = v;
+    int consecutive = 0;
+    for (int32_t k = 1; k < ndd; ++k) {
+        double beta = -shift - xi[k - 1];
+        double *wdst = (k & 1) ? wa : wb;
+        orc_csr_fused_rows_z(0, n, row_ptr, col, vals, vals_complex, wsrc, wdst, alpha_r, alpha_i, beta, 0.0, 1);
+        double sw = 0.0, sp = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            double tr, ti;
+            cmul_np(dd[2 * k], dd[2 * k + 1], wdst[2 * i], wdst[2 * i + 1], &tr, &ti);
+            p[2 * i] = p[2 * i] + tr;
+            p[2 * i + 1] = p[2 * i + 1] + ti;
+            sw += wdst[2 * i] * wdst[2 * i] + wdst[2 * i + 1] * wdst[2 * i + 1];
+            sp += p[2 * i] * p[2 * i] + p[2 * i + 1] * p[2 * i + 1];
+        }
+        *matvecs = k;
+        double term = ddabs[k] * sqrt(sw);
+        double pn = sqrt(sp);
+        *last_term = term;
+        *last_pnorm = pn;
+        if (tol > 0) {
+            if (term <= tol * pn) {
+                if (++consecutive >= 2) return 0;
+            } else {
+                consecutive = 0;
+            }
+        }
+        wsrc = wdst;
+    }
+    return tol == 0 ? 0 : 2;
+}
+
 /* out = (1/4 (2 - u)) exp(20 (1 - 1/u)) (_core.pyx:325-338); returns the first
  * index with u <= 0 (integrator.py:43-49) or -1. */
 int64_t orc_combustion(const double *u, double *out, int64_t n) {

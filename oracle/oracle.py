@@ -64,6 +64,10 @@ def lib():
         _lib.orc_csr_fused_rows.argtypes = [i64, i64, vp, vp, vp, vp, vp, d, d, ctypes.c_int]
         _lib.orc_newton_csr.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp, i32, d, d, d, vp, vp, vp, vp]
         _lib.orc_newton_csr.restype = ctypes.c_int
+        _lib.orc_csr_fused_rows_z.argtypes = [i64, i64, vp, vp, vp, ctypes.c_int, vp, vp, d, d, d, d, ctypes.c_int]
+        _lib.orc_newton_csr_z.argtypes = [i64, vp, vp, vp, ctypes.c_int, vp, vp, vp, vp, vp, i32, d, d, d, d, vp,
+                                          vp, vp, vp]
+        _lib.orc_newton_csr_z.restype = ctypes.c_int
         _lib.orc_combustion.argtypes = [vp, vp, i64]
         _lib.orc_combustion.restype = i64
         _lib.orc_combustion_jac.argtypes = [vp, vp, i64]
@@ -376,6 +380,48 @@ def newton_csr(a: Csr, it: Interp, v: np.ndarray, tol: float):
         p.ctypes.data, np.ascontiguousarray(it.dd).ctypes.data, it.xi.ctypes.data, len(it.dd),
         1.0 / gamma, it.center / gamma, float(tol), ws.ctypes.data,
         ctypes.byref(mv), ctypes.byref(term), ctypes.byref(pn))
+    if rc == 2:
+        ref = pn.value
+        raise OracleConvergenceError(term.value / ref if ref > 0 else float("inf"), mv.value)
+    return p, mv.value
+
+
+def _z(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+
+
+def csr_fused_z(a: Csr, alpha, beta, x, use_beta=True):
+    """The reference's complex CSR rows (_core.pyx:263-278 / _csr_same[cplx]):
+    real or complex vals, complex x, complex alpha / beta."""
+    x = _z(x)
+    vals = a.vals if np.iscomplexobj(a.vals) else np.ascontiguousarray(a.vals, dtype=np.float64)
+    y = np.empty(a.n, dtype=np.complex128)
+    al, be = complex(alpha), complex(beta)
+    lib().orc_csr_fused_rows_z(0, a.n, a.row_ptr.ctypes.data, a.col.ctypes.data, vals.ctypes.data,
+                               int(np.iscomplexobj(vals)), x.ctypes.data, y.ctypes.data, al.real, al.imag,
+                               be.real, be.imag, int(use_beta))
+    return y
+
+
+def newton_csr_z(a: Csr, dd, xi, center: float, gamma: float, alpha, v, tol: float):
+    """matfunc.newton_apply with complex divided differences / vectors on a
+    CSR operator (the propagate path); alpha is the reference's op_alpha
+    (1/gamma, or -1j/gamma on an imaginary-axis interval)."""
+    v = _z(v)
+    dd = _z(dd)
+    if len(dd) == 1:
+        return dd[0] * v, 0
+    vals = a.vals if np.iscomplexobj(a.vals) else np.ascontiguousarray(a.vals, dtype=np.float64)
+    p = np.empty_like(v)
+    ws = np.empty(4 * a.n)
+    ddabs = np.ascontiguousarray(np.abs(dd))
+    xi = np.ascontiguousarray(xi, dtype=np.float64)
+    mv, term, pn = ctypes.c_int32(), ctypes.c_double(), ctypes.c_double()
+    al = complex(alpha)
+    rc = lib().orc_newton_csr_z(
+        a.n, a.row_ptr.ctypes.data, a.col.ctypes.data, vals.ctypes.data, int(np.iscomplexobj(vals)),
+        v.ctypes.data, p.ctypes.data, dd.ctypes.data, ddabs.ctypes.data, xi.ctypes.data, len(dd), al.real, al.imag,
+        center / gamma, float(tol), ws.ctypes.data, ctypes.byref(mv), ctypes.byref(term), ctypes.byref(pn))
     if rc == 2:
         ref = pn.value
         raise OracleConvergenceError(term.value / ref if ref > 0 else float("inf"), mv.value)

@@ -29,7 +29,8 @@ EXPORTS = (
     "es_leja_csr_async", "es_rosenbrock_prologue", "es_leja_dist_begin", "es_leja_dist_source",
     "es_leja_dist_nslices", "es_leja_dist_node", "es_leja_dist_decide", "es_leja_dist_end",
     "es_leja_state_offset", "es_leja_csr_dist_begin", "es_leja_csr_dist_source", "es_leja_csr_dist_nslices",
-    "es_leja_csr_dist_node", "es_leja_csr_dist_end",
+    "es_leja_csr_dist_node", "es_leja_csr_dist_end", "es_csr_fused_rows_z", "es_leja_csr_z_workspace_bytes",
+    "es_leja_csr_z", "es_leja_csr_z_async",
 )
 
 
@@ -85,6 +86,12 @@ def _declare(lib):
         "es_leja_csr_dist_begin": ([i64, vp, vp, vp, vp, i64, vp, vp, vp, vp, i32, d, d, d, vp, sz, vp],
                                    ctypes.c_int),
         "es_leja_csr_dist_source": ([vp, i32, P(vp)], ctypes.c_int),
+        "es_csr_fused_rows_z": ([i64, i64, vp, vp, vp, i32, vp, vp, d, d, d, d, i32, vp], ctypes.c_int),
+        "es_leja_csr_z_workspace_bytes": ([i64], sz),
+        "es_leja_csr_z": ([i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, d, d, d, d, vp, sz, P(SeriesResult), vp],
+                          ctypes.c_int),
+        "es_leja_csr_z_async": ([i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, d, d, d, d, vp, sz, vp],
+                                ctypes.c_int),
         "es_leja_csr_dist_nslices": ([vp, P(i32)], ctypes.c_int),
         "es_leja_csr_dist_node": ([vp, vp, vp], ctypes.c_int),
         "es_leja_csr_dist_end": ([vp, vp], ctypes.c_int),

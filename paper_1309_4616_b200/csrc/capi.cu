@@ -249,4 +249,38 @@ extern "C" int es_leja_csr_dist_end(const void *workspace, void *stream) {
     return csr_dist_end(workspace, (cudaStream_t)stream);
 }
 
+extern "C" int es_csr_fused_rows_z(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr, const int32_t *col_idx,
+                                   const double *vals, int32_t vals_complex, const double *x, double *y,
+                                   double alpha_re, double alpha_im, double beta_re, double beta_im,
+                                   int32_t use_beta, void *stream) {
+    if (row_lo < 0 || row_hi < row_lo) return set_error(ES_ERR_ARG, "bad row range");
+    if (row_hi > row_lo && (!row_ptr || !col_idx || !vals || !x || !y)) return set_error(ES_ERR_ARG, "null pointer");
+    return launch_csr_rows_z(row_lo, row_hi, row_ptr, col_idx, vals, vals_complex, x, y, alpha_re, alpha_im, beta_re,
+                             beta_im, use_beta, (cudaStream_t)stream);
+}
+
+extern "C" size_t es_leja_csr_z_workspace_bytes(int64_t n) { return n < 0 ? 0 : csr_z_series_ws_bytes(n); }
+
+extern "C" int es_leja_csr_z(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *vals,
+                             int32_t vals_complex, const double *v, double *p_out, const double *dd,
+                             const double *ddabs, const double *xi, int32_t ndd, double alpha_re, double alpha_im,
+                             double shift, double tol, void *workspace, size_t workspace_bytes,
+                             es_series_result *result_host, void *stream) {
+    if (n < 0) return set_error(ES_ERR_ARG, "negative n");
+    if (!v || !p_out || !dd || !ddabs || !xi || !workspace || (n > 0 && (!row_ptr || !col_idx || !vals)))
+        return set_error(ES_ERR_ARG, "null pointer");
+    if (v == p_out) return set_error(ES_ERR_ARG, "p_out must not alias v");
+    return run_csr_series_z(n, row_ptr, col_idx, vals, vals_complex, v, p_out, dd, ddabs, xi, ndd, alpha_re,
+                            alpha_im, shift, tol, workspace, workspace_bytes, result_host, (cudaStream_t)stream);
+}
+
+extern "C" int es_leja_csr_z_async(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, const double *vals,
+                                   int32_t vals_complex, const double *v, double *p_out, const double *dd,
+                                   const double *ddabs, const double *xi, int32_t ndd, double alpha_re,
+                                   double alpha_im, double shift, double tol, void *workspace,
+                                   size_t workspace_bytes, void *stream) {
+    return es_leja_csr_z(n, row_ptr, col_idx, vals, vals_complex, v, p_out, dd, ddabs, xi, ndd, alpha_re, alpha_im,
+                         shift, tol, workspace, workspace_bytes, nullptr, stream);
+}
+
 extern "C" size_t es_leja_state_offset(void) { return series_state_offset(); }

@@ -266,17 +266,17 @@ static int csr_variant() { return env_int("ES_CSR_VARIANT", 8); }
 static std::mutex g_tex_mu;
 static std::map<std::pair<const void *, int64_t>, unsigned long long> g_tex;
 
-static unsigned long long tex_for(const double *p, int64_t n) {
+static unsigned long long tex_for(const double *p, int64_t n, bool z = false) {
     if (!p || n <= 0) return 0;
     std::lock_guard<std::mutex> lk(g_tex_mu);
-    auto key = std::make_pair((const void *)p, n);
+    auto key = std::make_pair((const void *)p, z ? -n : n);
     auto it = g_tex.find(key);
     if (it != g_tex.end()) return it->second;
     cudaResourceDesc rd = {};
     rd.resType = cudaResourceTypeLinear;
     rd.res.linear.devPtr = const_cast<double *>(p);
-    rd.res.linear.desc = cudaCreateChannelDesc<int2>();
-    rd.res.linear.sizeInBytes = (size_t)n * sizeof(double);
+    rd.res.linear.desc = z ? cudaCreateChannelDesc<int4>() : cudaCreateChannelDesc<int2>();
+    rd.res.linear.sizeInBytes = (size_t)n * sizeof(double) * (z ? 2 : 1);
     cudaTextureDesc td = {};
     td.readMode = cudaReadModeElementType;
     cudaTextureObject_t t = 0;
@@ -297,7 +297,7 @@ struct CsrLayout {
     int nchunks;
 };
 
-static CsrLayout csr_layout(int64_t n) {
+static CsrLayout csr_layout(int64_t n, int width = 1) {
     CsrLayout L;
     const int64_t rows_per_chunk = (int64_t)W4_T * W4_CHB;  // 16384
     L.nchunks = (int)std::max<int64_t>(1, (n + rows_per_chunk - 1) / rows_per_chunk);
@@ -307,14 +307,15 @@ static CsrLayout csr_layout(int64_t n) {
     L.cnt = o; o = up(o + sizeof(unsigned) * (L.nchunks + 1));
     L.part = o; o = up(o + sizeof(double) * 2 * (size_t)L.nchunks * W4_CHB);
     L.slice = o; o = up(o + sizeof(double) * 2 * (size_t)L.nchunks);
-    L.wa = o; o = up(o + sizeof(double) * n);
-    L.wb = o; o = up(o + sizeof(double) * n);
-    L.pb = o; o = up(o + sizeof(double) * n);
+    L.wa = o; o = up(o + sizeof(double) * width * n);
+    L.wb = o; o = up(o + sizeof(double) * width * n);
+    L.pb = o; o = up(o + sizeof(double) * width * n);
     L.total = o;
     return L;
 }
 
 size_t csr_series_ws_bytes(int64_t n) { return csr_layout(n).total; }
+size_t csr_z_series_ws_bytes(int64_t n) { return csr_layout(n, 2).total; }
 
 struct CsrSetup {
     SeriesParams hp;
@@ -418,6 +419,260 @@ int run_csr_series(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
     if (rc) return rc;
     if (!res) return ES_OK;
     return read_series_state(S.hp.state, res, stream);
+}
+
+// ----- complex CSR: the propagate path (cli.py:304-357) ------------------------
+//
+// Vectors are interleaved (re, im) doubles; vals real or interleaved complex.
+// Two complex products, each restating the reference bit for bit:
+//   cmul_c  -- the compiled core's C99 `double complex` product under
+//              -ffp-contract=off (_core.pyx:263-278; real vals promoted to
+//              (v, 0)):  (a.r b.r - a.i b.i, a.r b.i + a.i b.r);
+//   cmul_np -- numpy's complex128 product in p += dd_k w_k (matfunc.py:300),
+//              which on this build is (fma(a.r, b.r, -(a.i b.i)),
+//              fma(a.r, b.i, a.i b.r)) (pinned by the oracle tests).
+
+ES_DEV double2 cmul_c(double ar, double ai, double br, double bi) {
+    return make_double2(sub(mul(ar, br), mul(ai, bi)), add(mul(ar, bi), mul(ai, br)));
+}
+ES_DEV double2 cmul_np(double ar, double ai, double br, double bi) {
+    return make_double2(__fma_rn(ar, br, -mul(ai, bi)), __fma_rn(ar, bi, mul(ai, br)));
+}
+
+template <int G>
+ES_DEV double2 gather_z(const double2 *__restrict__ x, unsigned long long tex, int c) {
+    if constexpr (G == 1) {
+        const int4 t = tex1Dfetch<int4>((cudaTextureObject_t)tex, c);
+        return make_double2(__hiloint2double(t.y, t.x), __hiloint2double(t.w, t.z));
+    } else {
+        return __ldg(x + c);
+    }
+}
+
+// acc of row r over this warp's 32-row tile [r0, rend); products staged per warp.
+template <int G, int U, bool VC>
+ES_DEV double2 csr_warp_sum_z(int64_t r0, int64_t rend, int64_t r, bool act, const int64_t *__restrict__ rp,
+                              const int32_t *__restrict__ col, const double *__restrict__ vals,
+                              const double2 *__restrict__ xs, unsigned long long tex, double2 *sp) {
+    constexpr int ROUND = 32 * U;
+    const int lane = threadIdx.x & 31;
+    double2 acc = make_double2(0.0, 0.0);
+    if (r0 >= rend) return acc;
+    const int64_t kb = __ldg(rp + r0), ke = __ldg(rp + rend);
+    const int64_t ks = act ? __ldg(rp + r) : 0, kend = act ? __ldg(rp + r + 1) : 0;
+    for (int64_t base = kb; base < ke; base += ROUND) {
+        const int lim = (int)min((int64_t)ROUND, ke - base);
+        int c[U];
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = lane + 32 * u;
+            c[u] = j < lim ? __ldcs(col + base + j) : 0;
+            if constexpr (VC) {
+                v[u] = j < lim ? __ldcs(reinterpret_cast<const double2 *>(vals) + base + j) : make_double2(0.0, 0.0);
+            } else {
+                v[u] = make_double2(j < lim ? __ldcs(vals + base + j) : 0.0, 0.0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = lane + 32 * u;
+            if (j < lim) {
+                const double2 x = gather_z<G>(xs, tex, c[u]);
+                sp[j] = cmul_c(v[u].x, v[u].y, x.x, x.y);
+            }
+        }
+        __syncwarp();
+        const int lo = (int)(max(ks, base) - base), hi = (int)(min(kend, base + lim) - base);
+        for (int q = lo; q < hi; ++q) {
+            const double2 t = sp[q];
+            acc.x = add(acc.x, t.x);
+            acc.y = add(acc.y, t.y);
+        }
+        __syncwarp();
+    }
+    return acc;
+}
+
+constexpr int ZU = 4;  // gathers in flight per lane (complex)
+
+template <int G, bool VC>
+__global__ void __launch_bounds__(W4_T, 8) k_csr_node_z(const SeriesParams *__restrict__ Pp) {
+    __shared__ double2 s_prod[W4_WARPS][32 * ZU];
+    __shared__ double s_red[W4_WARPS][2];
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    const int k = P.state->k + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n = P.n;
+    const int64_t r0 = ((int64_t)blockIdx.x * W4_WARPS + warp) * 32;
+    const int64_t r = r0 + lane;
+    const bool act = r < n;
+    const double2 *src = reinterpret_cast<const double2 *>(k == 1 ? P.v : P.wbuf[(k - 1) & 1]);
+    const unsigned long long tex = P.tex[k == 1 ? 2 : (k - 1) & 1];
+    const double2 acc = csr_warp_sum_z<G, ZU, VC>(r0, min(r0 + 32, n), r, act, P.row_ptr, P.col, P.vals, src, tex,
+                                                  s_prod[warp]);
+    double sw = 0.0, sq = 0.0;
+    if (act) {
+        const double2 c = __ldg(src + r);
+        const double beta = sub(-P.shift, P.xi[k - 1]);  // matfunc.py:298
+        const double2 t1 = cmul_c(P.alpha, P.alpha_im, acc.x, acc.y);
+        const double2 t2 = cmul_c(beta, 0.0, c.x, c.y);
+        const double2 wn = make_double2(add(t1.x, t2.x), add(t1.y, t2.y));
+        const double2 *dd = reinterpret_cast<const double2 *>(P.dd);
+        const double2 d0 = dd[0], dk = dd[k];
+        const double2 pold = k == 1 ? cmul_np(d0.x, d0.y, c.x, c.y)
+                                    : __ldcs(reinterpret_cast<const double2 *>(P.pbuf[(k - 1) & 1]) + r);
+        const double2 t3 = cmul_np(dk.x, dk.y, wn.x, wn.y);
+        const double2 pn = make_double2(add(pold.x, t3.x), add(pold.y, t3.y));
+        reinterpret_cast<double2 *>(P.wbuf[k & 1])[r] = wn;
+        __stcs(reinterpret_cast<double2 *>(P.pbuf[k & 1]) + r, pn);
+        sw = add(mul(wn.x, wn.x), mul(wn.y, wn.y));
+        sq = add(mul(pn.x, pn.x), mul(pn.y, pn.y));
+    }
+    sw = warp_sum(sw);
+    sq = warp_sum(sq);
+    if (lane == 0) {
+        s_red[warp][0] = sw;
+        s_red[warp][1] = sq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double aw = s_red[0][0], ap = s_red[0][1];
+        for (int w = 1; w < W4_WARPS; ++w) {
+            aw = add(aw, s_red[w][0]);
+            ap = add(ap, s_red[w][1]);
+        }
+        P.part[(int64_t)blockIdx.x * 2] = aw;
+        P.part[(int64_t)blockIdx.x * 2 + 1] = ap;
+    }
+}
+
+struct CsrRowsZArgs {
+    int64_t row_lo, row_hi;
+    const int64_t *rp;
+    const int32_t *col;
+    const double *vals;
+    const double2 *x;
+    double2 *y;
+    double ar, ai, br, bi;
+    int use_beta;
+};
+
+template <bool VC>
+__global__ void __launch_bounds__(W4_T) k_csr_rows_z(const CsrRowsZArgs a) {
+    __shared__ double2 s_prod[W4_WARPS][32 * ZU];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = a.row_lo + ((int64_t)blockIdx.x * W4_WARPS + warp) * 32;
+    const int64_t rend = min(r0 + 32, a.row_hi);
+    const int64_t r = r0 + lane;
+    const bool act = r < rend;
+    const double2 acc = csr_warp_sum_z<0, ZU, VC>(r0, rend, r, act, a.rp, a.col, a.vals, a.x, 0, s_prod[warp]);
+    if (!act) return;
+    double2 y = cmul_c(a.ar, a.ai, acc.x, acc.y);  // _core.pyx:257-260
+    if (a.use_beta) {
+        const double2 xr = __ldg(a.x + r);
+        const double2 t = cmul_c(a.br, a.bi, xr.x, xr.y);
+        y = make_double2(add(y.x, t.x), add(y.y, t.y));
+    }
+    a.y[r] = y;
+}
+
+__global__ void k_scale_z(const double2 *x, const double2 *s, double2 *out, int64_t n) {
+    const double2 a = *s;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = cmul_np(a.x, a.y, x[i].x, x[i].y);
+}
+
+int launch_csr_rows_z(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr, const int32_t *col, const double *vals,
+                      int vals_complex, const double *x, double *y, double ar, double ai, double br, double bi,
+                      int use_beta, cudaStream_t stream) {
+    if (row_hi <= row_lo) return ES_OK;
+    CsrRowsZArgs a{row_lo, row_hi, row_ptr, col, vals, reinterpret_cast<const double2 *>(x),
+                   reinterpret_cast<double2 *>(y), ar, ai, br, bi, use_beta};
+    const unsigned grid = (unsigned)((row_hi - row_lo + W4_T - 1) / W4_T);
+    if (vals_complex) k_csr_rows_z<true><<<grid, W4_T, 0, stream>>>(a);
+    else k_csr_rows_z<false><<<grid, W4_T, 0, stream>>>(a);
+    return check_launch("csr rows (complex)");
+}
+
+int run_csr_series_z(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *vals, int vals_complex,
+                     const double *v, double *p_out, const double *dd, const double *ddabs, const double *xi, int ndd,
+                     double alpha_re, double alpha_im, double shift, double tol, void *ws, size_t ws_bytes,
+                     es_series_result *res, cudaStream_t stream) {
+    if (ndd < 1) return set_error(ES_ERR_ARG, "ndd must be >= 1");
+    const CsrLayout L = csr_layout(n, 2);
+    if (ws_bytes < L.total) return set_error(ES_ERR_ARG, "workspace too small");
+    if (ndd == 1 || n == 0) {  // degenerate interval: dd_0 v, 0 matvecs (matfunc.py:285-286)
+        if (n > 0)
+            k_scale_z<<<std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, stream>>>(
+                reinterpret_cast<const double2 *>(v), reinterpret_cast<const double2 *>(dd),
+                reinterpret_cast<double2 *>(p_out), n);
+        launch_state_trivial(ws, stream);
+        int rc = check_launch("scale (complex)");
+        if (rc || !res) return rc;
+        return read_series_state(series_state_ptr(ws), res, stream);
+    }
+    char *w = static_cast<char *>(ws);
+    SeriesParams hp = {};
+    hp.v = v;
+    hp.wbuf[1] = reinterpret_cast<double *>(w + L.wa);
+    hp.wbuf[0] = reinterpret_cast<double *>(w + L.wb);
+    hp.pbuf[1] = p_out;
+    hp.pbuf[0] = reinterpret_cast<double *>(w + L.pb);
+    hp.dd = dd;
+    hp.ddabs = ddabs;
+    hp.xi = xi;
+    hp.ndd = ndd;
+    hp.alpha = alpha_re;
+    hp.alpha_im = alpha_im;
+    hp.shift = shift;
+    hp.tol = tol;
+    hp.state = reinterpret_cast<SeriesState *>(w + L.state);
+    hp.part = reinterpret_cast<double *>(w + L.part);
+    hp.slice = reinterpret_cast<double *>(w + L.slice);
+    hp.chunk_cnt = reinterpret_cast<unsigned *>(w + L.cnt);
+    hp.global_cnt = hp.chunk_cnt + L.nchunks;
+    hp.nslices = L.nchunks;
+    hp.ntiles = W4_CHB;
+    hp.nchunks = L.nchunks;
+    hp.chunk_len = 1;
+    hp.row_ptr = row_ptr;
+    hp.col = col;
+    hp.vals = vals;
+    hp.vals_complex = vals_complex;
+    hp.n = n;
+    SeriesParams *dparams = reinterpret_cast<SeriesParams *>(w + L.params);
+    const unsigned grid = (unsigned)L.nchunks * W4_CHB;
+    hp.tex[0] = tex_for(hp.wbuf[0], n, true);
+    hp.tex[1] = tex_for(hp.wbuf[1], n, true);
+    hp.tex[2] = tex_for(v, n, true);
+    const bool tex = hp.tex[0] && hp.tex[1] && hp.tex[2];
+    CsrNodeFn nf = vals_complex ? (tex ? k_csr_node_z<1, true> : k_csr_node_z<0, true>)
+                                : (tex ? k_csr_node_z<1, false> : k_csr_node_z<0, false>);
+    GraphKernel gk[2] = {{(const void *)nf, dim3(grid), dim3(W4_T), 0},
+                         {(const void *)k_csr_slice_reduce, dim3((unsigned)L.nchunks), dim3(256), 0}};
+    unsigned long long handle = 0;
+    cudaGraphExec_t ge = series_graph(gk, 2, dparams, &handle);
+    if (ge) hp.cond = handle;
+    k_csr_init<<<1, 256, 0, stream>>>(hp, dparams);
+    int rc = check_launch("csr init (complex)");
+    if (rc) return rc;
+    if (ge) {
+        if (cudaGraphLaunch(ge, stream) != cudaSuccess) return check_launch("complex csr series graph");
+    } else {
+        for (int k = 1; k < ndd; ++k) {
+            nf<<<grid, W4_T, 0, stream>>>(dparams);
+            k_csr_slice_reduce<<<(unsigned)L.nchunks, 256, 0, stream>>>(dparams);
+        }
+        rc = check_launch("complex csr nodes");
+        if (rc) return rc;
+    }
+    k_csr_finalize<<<148 * 8, 256, 0, stream>>>(dparams, 2 * n);
+    rc = check_launch("csr finalize (complex)");
+    if (rc) return rc;
+    if (!res) return ES_OK;
+    return read_series_state(hp.state, res, stream);
 }
 
 // ----- multi-GPU row-block series (decomp.py:285-345 on one rank per GPU) ----

@@ -38,8 +38,10 @@ ES_DEV double lap7(double c, double xm, double xp, double ym, double yp, double 
 // D(x, y) = 1/sqrt((1 + x*x) + y*y) with x = (ix+1)/(nx+1) (grid.py:80-83,
 // bench.py:40-41): correctly rounded div/sqrt reproduce numpy's sampling.
 ES_DEV double axis_coord(int64_t i, int64_t n) { return div((double)(i + 1), (double)(n + 1)); }
+// __drcp_rn is the correctly rounded 1/s, i.e. bit-identical to
+// __ddiv_rn(1.0, s), with a shorter refinement sequence.
 ES_DEV double radial_from_sq(double one_plus_x2, double y) {
-    return div(1.0, sqrt_rn(add(one_plus_x2, mul(y, y))));
+    return __drcp_rn(sqrt_rn(add(one_plus_x2, mul(y, y))));
 }
 
 // ordered-integer image of a double (monotone in the value) for atomic

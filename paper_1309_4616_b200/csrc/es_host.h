@@ -73,6 +73,14 @@ int run_csr_series(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
                    double alpha, double shift, double tol, void *ws, size_t ws_bytes,
                    es_series_result *res, cudaStream_t stream);
 
+size_t csr_z_series_ws_bytes(int64_t n);
+int launch_csr_rows_z(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr, const int32_t *col, const double *vals,
+                      int vals_complex, const double *x, double *y, double ar, double ai, double br, double bi,
+                      int use_beta, cudaStream_t stream);
+int run_csr_series_z(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *vals, int vals_complex,
+                     const double *v, double *p_out, const double *dd, const double *ddabs, const double *xi, int ndd,
+                     double alpha_re, double alpha_im, double shift, double tol, void *ws, size_t ws_bytes,
+                     es_series_result *res, cudaStream_t stream);
 int csr_dist_begin(int64_t n_local, const int64_t *row_ptr, const int32_t *col, const double *vals, const double *xg,
                    int64_t n_xg, const double *v, double *p_out, const double *dd, const double *xi, int ndd, double alpha,
                    double shift, double tol, void *ws, size_t ws_bytes, cudaStream_t stream);

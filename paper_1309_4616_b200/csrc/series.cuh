@@ -25,8 +25,9 @@ ES_DEV void group_sync() {
 // The stopping test of matfunc.py:302-311 on the reduced sums (one thread).
 ES_DEV void decide(const SeriesParams &P, int k, double sumw, double sump) {
     SeriesState &st = *P.state;
-    const double dk = P.dd[k];
-    const double term = mul(fabs(dk), sqrt_rn(sumw));
+    // |dd_k|: real series read dd directly; complex series pass numpy's abs(dd)
+    const double adk = P.ddabs ? P.ddabs[k] : fabs(P.dd[k]);
+    const double term = mul(adk, sqrt_rn(sumw));
     const double pn = sqrt_rn(sump);
     st.k = k;
     st.last_term = term;

@@ -128,7 +128,7 @@ __global__ void k_aux_init(unsigned long long *aux, unsigned long long n) {
 
 // One Newton-Leja node, persistent CTAs over (chunk, tile) items.
 template <bool DIM3, int COEFF, bool GD>
-__global__ void __launch_bounds__(TMA_THREADS, 3) k_node_tma(const SeriesParams *__restrict__ Pp) {
+__global__ void __launch_bounds__(TMA_THREADS, (COEFF == ES_COEFF_RADIAL && !DIM3) ? 2 : 3) k_node_tma(const SeriesParams *__restrict__ Pp) {
     extern __shared__ __align__(128) char tsmem[];
     const SeriesParams &P = *Pp;
     if (P.state->done) return;
@@ -271,10 +271,9 @@ StencilPlan plan_stencil(const es_stencil_desc *d, std::initializer_list<const v
         pl.block = dim3(TMA_THREADS, 1, 1);
         if (pl.dim2) {
             // one wave: tiles_x * nchunks <= SMs * 3 resident CTAs
-            const int64_t tiles_x = (d->nx + 511) / 512;
-            const int64_t slots = (int64_t)sm_count() * 3;
-            const int64_t per = std::max<int64_t>(1, slots / tiles_x);
-            pl.chunk = env_int("ES_TCHUNK2D", (int)std::max<int64_t>(4, (d->ny + per - 1) / per));
+            // short row chunks, claimed dynamically by the persistent CTAs
+            // (4096^2: chunk 8 -> 106 us/node, one-wave chunk 75 -> 122 us)
+            pl.chunk = env_int("ES_TCHUNK2D", 8);
             pl.grid = dim3((unsigned)((d->nx + 511) / 512), (unsigned)((d->ny + pl.chunk - 1) / pl.chunk), 1);
             pl.smem = 0;  // set by the launcher (depends on the kernel variant)
             pl.nchunks = pl.grid.y;

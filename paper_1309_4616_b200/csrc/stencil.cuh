@@ -55,6 +55,9 @@ struct SeriesParams {
     const int32_t *col;
     const double *vals;
     unsigned long long tex[4];  // CSR texture gathers: wbuf[0], wbuf[1], v, xg
+    const double *ddabs;        // complex series: |dd_k| (else nullptr)
+    double alpha_im;            // complex series: imaginary part of alpha
+    int vals_complex;           // complex CSR: interleaved complex vals
     const double *xg;  // multi-GPU CSR: the all-gathered w_{k-1} the row gathers read (nullptr: the local source)
     int64_t n;
     const void *maps;  // TmaMaps (workspace) for the TMA node kernel

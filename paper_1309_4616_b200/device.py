@@ -33,6 +33,20 @@ def to_device(x, dtype=torch.float64) -> torch.Tensor:
     return torch.from_numpy(arr).to(device())
 
 
+def to_device_z(x) -> torch.Tensor:
+    """Contiguous complex128 CUDA tensor of x (real input gets a zero
+    imaginary part, like numpy's astype(complex128))."""
+    if isinstance(x, torch.Tensor):
+        if x.device.type != "cuda":
+            x = x.to(device())
+        return x.to(torch.complex128).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex128)).to(device())
+
+
+def is_complex_data(x) -> bool:
+    return x.is_complex() if isinstance(x, torch.Tensor) else np.iscomplexobj(x)
+
+
 def like_input(t: torch.Tensor, host: bool):
     """Return t as a numpy array when the caller passed host data."""
     return t.cpu().numpy() if host else t
@@ -42,8 +56,8 @@ def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
-def empty(n: int) -> torch.Tensor:
-    return torch.empty(n, dtype=torch.float64, device=device())
+def empty(n: int, dtype=torch.float64) -> torch.Tensor:
+    return torch.empty(n, dtype=dtype, device=device())
 
 
 class Workspace:

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib, timing
-from .device import Workspace, empty, is_host, like_input, ptr, stream_handle, to_device
+from .device import Workspace, empty, is_complex_data, is_host, like_input, ptr, stream_handle, to_device, to_device_z
 
 
 class CsrMatrix:
@@ -120,11 +120,17 @@ class CsrMatrix:
 
     # -- device copies -------------------------------------------------------
 
+    @property
+    def is_complex(self) -> bool:
+        return bool(np.iscomplexobj(self.vals))
+
     def device_arrays(self):
+        """(row_ptr i64, col i32, vals f64 | c128) on the current device,
+        uploaded once."""
         dev = torch.cuda.current_device()
         if dev not in self._dev:
-            if self.vals.dtype != np.float64:
-                raise NotImplementedError("device CSR supports real fp64 values")
+            if self.vals.dtype not in (np.float64, np.complex128):
+                raise NotImplementedError("device CSR supports fp64 or complex128 values")
             if self.col_idx.dtype != np.int32:
                 raise NotImplementedError("device CSR needs 32-bit column indices")
             self._dev[dev] = (torch.from_numpy(self.row_ptr).to("cuda"),
@@ -135,9 +141,32 @@ class CsrMatrix:
     def fused_apply_flat(self, alpha, beta, x):
         return fused_spmv(self, alpha, beta, x)
 
+    def _leja_z(self, v, p_out, dd, ddabs, xi, alpha: complex, shift, tol):
+        """Complex series (complex dd / vectors, the propagate path) through
+        es_leja_csr_z; v, p_out complex128, dd complex128, ddabs float64."""
+        lib = _lib.load()
+        rp, col, vals = self.device_arrays()
+        ws = self._ws.get(lib.es_leja_csr_z_workspace_bytes(self.n))
+        tm = timing.active()
+        ev0 = timing.event() if tm else None
+        rc = lib.es_leja_csr_z_async(self.n, ptr(rp), ptr(col), ptr(vals), int(self.is_complex), ptr(v), ptr(p_out),
+                                     ptr(dd), ptr(ddabs), ptr(xi), dd.numel(), alpha.real, alpha.imag, float(shift),
+                                     float(tol), ptr(ws), ws.numel(), stream_handle())
+        _lib.check(rc, "es_leja_csr_z_async")
+        ev1 = timing.event() if tm else None
+        res = _lib.SeriesResult()
+        rc = lib.es_leja_fetch(ptr(ws), ctypes.byref(res), stream_handle())
+        if rc != _lib.ES_ERR_NOT_CONVERGED:
+            _lib.check(rc, "es_leja_fetch")
+        if tm:
+            tm.add(ev0, ev1, res.matvecs)
+        return res
+
     def _leja(self, v, p_out, dd, xi, alpha, shift, tol, gdiag=None):
         if gdiag is not None:
             raise NotImplementedError("a Jacobian diagonal is defined for stencil operators only")
+        if self.is_complex:
+            raise NotImplementedError("complex matrices run the complex series (_leja_z)")
         lib = _lib.load()
         rp, col, vals = self.device_arrays()
         nbytes = lib.es_leja_csr_workspace_bytes(self.n)
@@ -168,11 +197,18 @@ def csr_storage_bytes(nrows: int, nnz: int, value_bytes: int = 8, index_width: i
 def _product(a: CsrMatrix, alpha, beta, x, use_beta: bool, row_lo: int = 0, row_hi: Optional[int] = None,
              out=None):
     host = is_host(x)
-    if (np.iscomplexobj(x) if host else x.is_complex()):
-        re = _product(a, 1.0, 0.0, x.real.copy() if host else x.real.contiguous(), False)
-        im = _product(a, 1.0, 0.0, x.imag.copy() if host else x.imag.contiguous(), False)
-        y = alpha * (re + 1j * im)
-        return y + beta * x if use_beta else y
+    if is_complex_data(x) or a.is_complex or isinstance(alpha, complex) or isinstance(beta, complex):
+        # the reference's complex core (_core.pyx:263-278): complex alpha/beta, real or complex vals
+        xd = to_device_z(x)
+        rp, col, vals = a.device_arrays()
+        y = empty(a.nrows, torch.complex128) if out is None else out
+        hi = a.nrows if row_hi is None else row_hi
+        al, be = complex(alpha), complex(beta)
+        rc = _lib.load().es_csr_fused_rows_z(row_lo, hi, ptr(rp), ptr(col), ptr(vals), int(a.is_complex), ptr(xd),
+                                             ptr(y), al.real, al.imag, be.real, be.imag, int(use_beta),
+                                             stream_handle())
+        _lib.check(rc, "es_csr_fused_rows_z")
+        return like_input(y, host)
     xd = to_device(x)
     rp, col, vals = a.device_arrays()
     y = empty(a.nrows) if out is None else out

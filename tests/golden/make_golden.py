@@ -248,6 +248,103 @@ def csr_cases():
          mv0=np.array(mv0))
 
 
+MM_GOOD = {
+    "sym": "%%MatrixMarket matrix coordinate real symmetric\n% comment\n4 4 5\n1 1 2.5\n2 1 -1\n3 2 -0.5\n"
+           "4 4 3\n4 3 1e-3\n",
+    "herm": "%%MatrixMarket matrix coordinate complex hermitian\n3 3 4\n1 1 1 0\n2 1 0.5 -0.25\n3 3 2 0\n"
+            "3 2 0 1\n",
+    "skew": "%%MatrixMarket matrix coordinate real skew-symmetric\n3 3 2\n2 1 1.5\n3 1 -2\n",
+    "pattern": "%%MatrixMarket matrix coordinate pattern general\n\n3 4 3\n1 2\n3 4 7.5\n2 1\n",
+    "general": "%%MatrixMarket matrix coordinate integer general\n2 3 3\n2 3 4\n1 1 -2\n1 3 5\n",
+}
+MM_BAD = {
+    "header": "%%MatrixMarket matrix array real general\n2 2 1\n1 1 1\n",
+    "field": "%%MatrixMarket matrix coordinate quaternion general\n2 2 1\n1 1 1\n",
+    "size": "%%MatrixMarket matrix coordinate real general\n% c\n2 2\n1 1 1\n",
+    "bounds": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n3 1 2\n",
+    "value": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 x\n",
+    "upper": "%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 1\n1 2 3\n",
+    "hdiag": "%%MatrixMarket matrix coordinate complex hermitian\n2 2 1\n1 1 1 2\n",
+    "dup": "%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1\n2 2 1\n1 1 4\n",
+    "count": "%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1\n2 2 1\n",
+    "extra": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 1\n2 2 1\n",
+    "square": "%%MatrixMarket matrix coordinate real symmetric\n2 3 1\n1 1 1\n",
+}
+
+
+def csr_complex_cases():
+    """The propagate path (cli.py:304-357): complex CSR rows for real and
+    Hermitian matrices (_core.pyx:263-278), complex Newton series on real-
+    and imaginary-axis intervals, exp(-i t H) psi0 through apply_matfunc with
+    halving, and Matrix Market parsing (sparse.py:292-428)."""
+    import tempfile
+
+    from expstencil.errors import MatrixMarketError
+    from expstencil.matfunc import SpectralInterval
+    from expstencil.sparse import read_matrix_market, spmv
+
+    rng = np.random.default_rng(108)
+    out = {}
+    n = 700
+    mats = {}
+    d = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.02)
+    d = d + d.T + np.diag(rng.random(n) * 4.0)
+    mats["real"] = CsrMatrix.from_dense(d)
+    hmat = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * (rng.random((n, n)) < 0.02)
+    hmat = hmat + hmat.conj().T + np.diag(rng.random(n))
+    mats["herm"] = CsrMatrix.from_dense(hmat)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    out["x"] = x
+    for name, m in mats.items():
+        out[f"{name}_row_ptr"], out[f"{name}_col"], out[f"{name}_vals"] = m.row_ptr, m.col_idx, m.vals
+        out[f"{name}_y"] = m.fused_apply_flat(0.7 - 0.2j, -1.3, x)
+        out[f"{name}_spmv"] = spmv(m, x)
+        k = 0
+        for axis, target, scale in (("real", "exp", -0.8j), ("real", "phi1", -0.5j), ("imag", "exp", -0.8)):
+            iv = gershgorin_interval(m, axis)
+            it = make_interpolant(iv, target, scale, 100, 1e-10)
+            for tol in (0.0, 1e-10):
+                p, mv = newton_apply(m, it, x, tol)
+                key = f"{name}_s{k}"
+                out[key + "_meta"] = np.array([iv.a, iv.b, tol, mv])
+                out[key + "_axis"] = np.array(axis)
+                out[key + "_target"] = np.array(target)
+                out[key + "_scale"] = np.array(scale, dtype=np.complex128)
+                out[key + "_dd"], out[key + "_xi"], out[key + "_p"] = it.dd, it.xi, p
+                k += 1
+        out[f"{name}_nseries"] = np.array(k)
+        # exp(-i t H) psi0 with a degree cap that forces the halving rescue
+        psi0 = np.full(n, 1.0 / np.sqrt(n), dtype=np.complex128)
+        iv = gershgorin_interval(m)
+        psi, st = apply_matfunc(m, psi0, "exp", scale=-1j * 3.0, interval=iv, tol=1e-8, max_degree=40)
+        out[f"{name}_psi"] = psi
+        out[f"{name}_prop_stats"] = np.array([st.matvecs, st.degree, st.halvings])
+    # Matrix Market
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, text in MM_GOOD.items():
+            path = os.path.join(tmp, name + ".mtx")
+            with open(path, "w") as fh:
+                fh.write(text)
+            a = read_matrix_market(path)
+            out[f"mm_{name}_text"] = np.array(text)
+            out[f"mm_{name}"] = np.array([a.nrows, a.ncols])
+            out[f"mm_{name}_row_ptr"], out[f"mm_{name}_col"], out[f"mm_{name}_vals"] = a.row_ptr, a.col_idx, a.vals
+        for name, text in MM_BAD.items():
+            path = os.path.join(tmp, name + ".mtx")
+            with open(path, "w") as fh:
+                fh.write(text)
+            try:
+                read_matrix_market(path)
+                raise AssertionError(f"{name} parsed")
+            except MatrixMarketError as err:
+                out[f"mmbad_{name}_text"] = np.array(text)
+                out[f"mmbad_{name}_line"] = np.array(err.line)
+                out[f"mmbad_{name}_msg"] = np.array(str(err))
+    out["mm_good"] = np.array(sorted(MM_GOOD))
+    out["mm_bad"] = np.array(sorted(MM_BAD))
+    save("csr_complex", **out)
+
+
 def combustion_cases():
     rng = np.random.default_rng(107)
     u = rng.uniform(0.05, 2.5, 5000)
@@ -263,3 +360,4 @@ if __name__ == "__main__":
     rescue_cases()
     csr_cases()
     combustion_cases()
+    csr_complex_cases()

@@ -528,3 +528,67 @@ def test_distributed_csr_world1_nccl():
     y = dop.fused_apply_flat(0.5, 2.0, v)
     assert torch.equal(y, a.fused_apply_flat(0.5, 2.0, v))
     assert dop.ledger.last_scalars() == 0  # one rank: nothing crosses a link
+
+
+# ---- the propagate path: complex CSR (golden: csr_complex) -----------------
+
+
+def _zmat(d, name):
+    n = len(d[f"{name}_row_ptr"]) - 1
+    return es.CsrMatrix(n, n, d[f"{name}_row_ptr"], d[f"{name}_col"], d[f"{name}_vals"])
+
+
+@pytest.mark.parametrize("name", ["real", "herm"])
+def test_complex_csr_apply_bitwise(golden, name):
+    d = golden("csr_complex")
+    a = _zmat(d, name)
+    assert a.fused_apply_flat(0.7 - 0.2j, -1.3, d["x"]).tobytes() == d[f"{name}_y"].tobytes()
+    assert es.spmv(a, d["x"]).tobytes() == d[f"{name}_spmv"].tobytes()
+
+
+@pytest.mark.parametrize("graph", [True, False])
+@pytest.mark.parametrize("name", ["real", "herm"])
+def test_complex_csr_series_bitwise(golden, name, graph, monkeypatch):
+    if not graph:
+        monkeypatch.setenv("ES_NO_GRAPH", "1")
+    d = golden("csr_complex")
+    a = _zmat(d, name)
+    for k in range(int(d[f"{name}_nseries"])):
+        key = f"{name}_s{k}"
+        lo, hi, tol, mv_ref = d[key + "_meta"]
+        iv = es.SpectralInterval(float(lo), float(hi), str(d[key + "_axis"]))
+        xi, dd = d[key + "_xi"], d[key + "_dd"]
+        it = es.LejaInterpolant(iv, str(d[key + "_target"]), complex(d[key + "_scale"]), len(dd) - 1, 1e-10,
+                                iv.center + iv.halfspan * xi, xi, dd)
+        p, mv = es.newton_apply(a, it, d["x"], float(tol))
+        assert mv == int(mv_ref), key
+        assert p.tobytes() == d[key + "_p"].tobytes(), key
+
+
+@pytest.mark.parametrize("name", ["real", "herm"])
+def test_propagate_with_halving_bitwise(golden, name):
+    d = golden("csr_complex")
+    a = _zmat(d, name)
+    n = a.nrows
+    psi0 = np.full(n, 1.0 / np.sqrt(n), dtype=np.complex128)
+    psi, st = es.apply_matfunc(a, psi0, "exp", -3.0j, es.gershgorin_interval(a), tol=1e-8, max_degree=40)
+    assert [st.matvecs, st.degree, st.halvings] == [int(v) for v in d[f"{name}_prop_stats"]]
+    assert psi.tobytes() == d[f"{name}_psi"].tobytes()
+    res = es.propagate(a, 3.0, tol=1e-8, max_degree=40)
+    assert res.psi.tobytes() == psi.tobytes()
+    assert res.norm_drift < 1e-6  # unitary evolution
+    part = es.propagate(a, 3.0, tol=1e-8, max_degree=40, workers=3)
+    assert part.psi.tobytes() == psi.tobytes()  # partitioned: identical, ledger counts (m-1) n per apply
+
+
+def test_complex_series_large_vs_oracle():
+    from paper_1309_4616_b200.sparse import synthetic_symmetric
+
+    a = synthetic_symmetric(200_003, 6, seed=12)
+    oc = orc.Csr(a.nrows, a.row_ptr, a.col_idx.astype(np.int32), a.vals)
+    iv = es.gershgorin_interval(a)
+    it = es.make_interpolant(iv, "exp", -0.2j, 80, 1e-10)
+    v = np.random.default_rng(1).standard_normal(a.nrows) + 1j * np.random.default_rng(2).standard_normal(a.nrows)
+    ref, mv_ref = orc.newton_csr_z(oc, it.dd, it.xi, iv.center, iv.halfspan, 1.0 / iv.halfspan, v, 1e-10)
+    got, mv = es.newton_apply(a, it, v, 1e-10)
+    assert mv == mv_ref and got.tobytes() == ref.tobytes()
