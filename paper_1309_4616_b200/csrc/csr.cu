@@ -266,8 +266,21 @@ static int csr_variant() { return env_int("ES_CSR_VARIANT", 8); }
 static std::mutex g_tex_mu;
 static std::map<std::pair<const void *, int64_t>, unsigned long long> g_tex;
 
+static size_t texture_alignment() {
+    static size_t a = 0;
+    if (!a) {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        a = cudaDeviceGetAttribute(&v, cudaDevAttrTextureAlignment, dev) == cudaSuccess && v > 0 ? (size_t)v : 512;
+    }
+    return a;
+}
+
+// nullptr-equivalent 0 when the buffer cannot back a linear texture
+// (misaligned, e.g. a torch slice, or longer than the texture limit): the
+// caller then runs the LDG-gather variant.
 static unsigned long long tex_for(const double *p, int64_t n, bool z = false) {
-    if (!p || n <= 0) return 0;
+    if (!p || n <= 0 || ((uintptr_t)p % texture_alignment()) != 0 || n >= (int64_t)1 << 30) return 0;
     std::lock_guard<std::mutex> lk(g_tex_mu);
     auto key = std::make_pair((const void *)p, z ? -n : n);
     auto it = g_tex.find(key);
@@ -288,7 +301,8 @@ static unsigned long long tex_for(const double *p, int64_t n, bool z = false) {
     return (unsigned long long)t;
 }
 
-static size_t up(size_t x) { return (x + 255) & ~(size_t)255; }
+// 512-byte segments: the w / p buffers must satisfy the texture alignment
+static size_t up(size_t x) { return (x + 511) & ~(size_t)511; }
 
 // Workspace: params at offset 0 (like the stencil layout: the device
 // SeriesParams pointer of a series is its workspace pointer).
