@@ -402,8 +402,13 @@ class Stepper:
         """Kernels this step launched (counted from the code path).
         A TMA series = publish maps + init + (node + slice reduce) per node + finalize."""
         m = stats.matvecs
-        # slab series: node + slice reduce + decide per node (NCCL kernels not counted)
-        series = 3 * m + 3 if self.dist else 2 * m + 3
+        op = self.problem.operator
+        if self.dist and getattr(op, "exchange", "nccl") == "p2p":
+            series = 2 * m + 4  # + the round-0 halo kernel; no NCCL per node
+        elif self.dist:
+            series = 3 * m + 3  # node + slice reduce + decide per node (NCCL kernels not counted)
+        else:
+            series = 2 * m + 3
         if self.cfg["method"] == "rosenbrock":
             if self.ros._fused:
                 return series + 2 + 1  # aux init + fused prologue; final axpy
@@ -442,7 +447,8 @@ def config_block(args, cfg, n, world, nnz=None):
                         f"the {8 * n / 2**20:.0f} MiB vectors are L2-resident by design (no flush)"})
         return c
     c.update({"grid": list(cfg["dims"]), "bc": cfg["bc"], "coeff": cfg["coeff"],
-              "parallelism": f"z-slabs x{world} (NCCL halo exchange)" if world > 1 else "single",
+              "parallelism": (f"z-slabs x{world} (halo planes and norm slices over NVLink peer memory, "
+                              f"fused into the node kernels)" if world > 1 else "single"),
               "l2": f"inputs larger than L2 ({8 * n / 2**20:.0f} MiB per vector)" if 8 * n >= 2**27
               else "working set inside L2 (no flush)"})
     return c

@@ -175,6 +175,50 @@ int es_leja_dist_node(const void *workspace, double *slices_out, void *stream);
 int es_leja_dist_decide(const void *workspace, const double *slices_all, int32_t nslices, void *stream);
 int es_leja_dist_end(const void *workspace, void *stream);
 
+/* Peer-memory (NVLink P2P) slab series: the fused compute + exchange form of
+ * the slab series above.  One call enqueues the whole series as one CUDA
+ * graph on this rank's stream; no host involvement per node:
+ *   - after node k the slice kernel stores the first / last plane of w_k
+ *     straight into the lower / upper neighbour's halo buffer of parity
+ *     (k + 1) & 1 (peer stores over NVLink), writes this slab's per-chunk
+ *     sums into every rank's slice table at slice_offset and adds 1 to
+ *     every rank's arrival counter
+ *     (system-scope), then waits until its own counter reaches
+ *     base + nranks * (k + 1) and runs the stopping test on the full table;
+ *   - round 0 (before node 1) exchanges v's boundary planes the same way.
+ * Every pointer below is a device address valid in THIS process: peers'
+ * buffers are mapped with es_ipc_open (or are local buffers of other
+ * in-process ranks).  Slice tables hold 2 x total_slices x 2 doubles, halo
+ * buffers one (ny, nx) plane each; counters are u64, zero-initialised once
+ * and never reset (pass base = nranks x rounds completed so far, where a
+ * series of K nodes completes K + 1 rounds).  A peer that does not arrive
+ * within timeout_ns ends the series with ES_ERR_CUDA at es_leja_fetch.
+ * Completion / result: es_leja_fetch. */
+typedef struct es_p2p_desc {
+    int32_t nranks, rank;
+    int64_t slice_offset, total_slices;
+    double *halo_lo[2], *halo_hi[2];  /* this rank's receive buffers by parity (NULL: no neighbour) */
+    double *peer_lo[2], *peer_hi[2];  /* lower neighbour's halo_hi[2] / upper neighbour's halo_lo[2] */
+    double *const *rank_slices;       /* device array [nranks] of slice-table pointers */
+    unsigned long long *const *rank_arrive; /* device array [nranks] of counter pointers */
+    unsigned long long *arrive_local; /* this rank's counter */
+    unsigned long long base;
+    int64_t timeout_ns;               /* <= 0: 10 s */
+} es_p2p_desc;
+
+int es_leja_stencil_nslices(const es_stencil_desc *d, int32_t *nslices_out);
+int es_leja_p2p(const es_stencil_desc *d, const es_p2p_desc *p2p, const double *v, double *p_out,
+                const double *dd, const double *xi, int32_t ndd, double alpha, double shift,
+                double tol, const double *gdiag, void *workspace, size_t workspace_bytes,
+                void *stream);
+
+/* CUDA IPC for the peer mappings: a 64-byte handle of a device allocation
+ * (cudaIpcGetMemHandle; offset_out = dev_ptr - allocation base) and its
+ * mapping in another process (peer access over NVLink). */
+int es_ipc_handle(const void *dev_ptr, void *handle_out, int64_t *offset_out);
+int es_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out);
+int es_ipc_close(void *dev_ptr);
+
 /* Multi-GPU row-block CSR series (decomp.py:285-345, PartitionedCsr._run
  * :304-333, on one rank per GPU).  Each rank owns rows [r_lo, r_hi) as a
  * local CSR block (row_ptr rebased to 0, n_local + 1 entries) whose column

@@ -30,7 +30,8 @@ EXPORTS = (
     "es_leja_dist_nslices", "es_leja_dist_node", "es_leja_dist_decide", "es_leja_dist_end",
     "es_leja_state_offset", "es_leja_csr_dist_begin", "es_leja_csr_dist_source", "es_leja_csr_dist_nslices",
     "es_leja_csr_dist_node", "es_leja_csr_dist_end", "es_csr_fused_rows_z", "es_leja_csr_z_workspace_bytes",
-    "es_leja_csr_z", "es_leja_csr_z_async",
+    "es_leja_csr_z", "es_leja_csr_z_async", "es_leja_stencil_nslices", "es_leja_p2p", "es_ipc_handle",
+    "es_ipc_open", "es_ipc_close",
 )
 
 
@@ -41,6 +42,17 @@ class StencilDesc(ctypes.Structure):
         ("wx", ctypes.c_double), ("wy", ctypes.c_double), ("wz", ctypes.c_double),
         ("mode", ctypes.c_int32), ("coeff_kind", ctypes.c_int32),
         ("coeff", ctypes.c_void_p), ("faces", ctypes.c_void_p * 6),
+    ]
+
+
+class P2PDesc(ctypes.Structure):
+    _fields_ = [
+        ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
+        ("slice_offset", ctypes.c_int64), ("total_slices", ctypes.c_int64),
+        ("halo_lo", ctypes.c_void_p * 2), ("halo_hi", ctypes.c_void_p * 2),
+        ("peer_lo", ctypes.c_void_p * 2), ("peer_hi", ctypes.c_void_p * 2),
+        ("rank_slices", ctypes.c_void_p), ("rank_arrive", ctypes.c_void_p), ("arrive_local", ctypes.c_void_p),
+        ("base", ctypes.c_uint64), ("timeout_ns", ctypes.c_int64),
     ]
 
 
@@ -88,6 +100,11 @@ def _declare(lib):
         "es_leja_csr_dist_source": ([vp, i32, P(vp)], ctypes.c_int),
         "es_csr_fused_rows_z": ([i64, i64, vp, vp, vp, i32, vp, vp, d, d, d, d, i32, vp], ctypes.c_int),
         "es_leja_csr_z_workspace_bytes": ([i64], sz),
+        "es_leja_stencil_nslices": ([P(StencilDesc), P(i32)], ctypes.c_int),
+        "es_leja_p2p": ([P(StencilDesc), P(P2PDesc), vp, vp, vp, vp, i32, d, d, d, vp, vp, sz, vp], ctypes.c_int),
+        "es_ipc_handle": ([vp, vp, P(i64)], ctypes.c_int),
+        "es_ipc_open": ([vp, i64, P(vp)], ctypes.c_int),
+        "es_ipc_close": ([vp], ctypes.c_int),
         "es_leja_csr_z": ([i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, d, d, d, d, vp, sz, P(SeriesResult), vp],
                           ctypes.c_int),
         "es_leja_csr_z_async": ([i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, d, d, d, d, vp, sz, vp],

@@ -3,6 +3,11 @@
 #include <cstdio>
 #include <cstring>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "es_common.cuh"
 #include "es_host.h"
 
@@ -50,6 +55,8 @@ int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaS
     res->last_term = st.last_term;
     res->last_pnorm = st.last_pnorm;
     if (!st.done) return set_error(ES_ERR_CUDA, "series did not finish (k=%d)", st.k);
+    if (st.converged < 0)
+        return set_error(ES_ERR_CUDA, "peer-memory series: a peer did not arrive within the timeout (node %d)", st.k);
     if (!st.converged)
         return set_error(ES_ERR_NOT_CONVERGED, "Newton series did not converge within degree %d", st.k);
     return ES_OK;
@@ -281,6 +288,81 @@ extern "C" int es_leja_csr_z_async(int64_t n, const int64_t *row_ptr, const int3
                                    size_t workspace_bytes, void *stream) {
     return es_leja_csr_z(n, row_ptr, col_idx, vals, vals_complex, v, p_out, dd, ddabs, xi, ndd, alpha_re, alpha_im,
                          shift, tol, workspace, workspace_bytes, nullptr, stream);
+}
+
+extern "C" int es_leja_stencil_nslices(const es_stencil_desc *d, int32_t *nslices_out) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (!nslices_out) return set_error(ES_ERR_ARG, "null pointer");
+    *nslices_out = stencil_nslices(d);
+    return ES_OK;
+}
+
+extern "C" int es_leja_p2p(const es_stencil_desc *d, const es_p2p_desc *p2p, const double *v, double *p_out,
+                           const double *dd, const double *xi, int32_t ndd, double alpha, double shift, double tol,
+                           const double *gdiag, void *workspace, size_t workspace_bytes, void *stream) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (d->mode == ES_MODE_FACES || d->mode == ES_MODE_PERIODIC)
+        return set_error(ES_ERR_ARG, "slab series need a linear, non-periodic boundary rule");
+    if (!p2p || !v || !p_out || !dd || !xi || !workspace) return set_error(ES_ERR_ARG, "null pointer");
+    if (v == p_out) return set_error(ES_ERR_ARG, "p_out must not alias v");
+    return run_p2p_series(d, p2p, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, workspace, workspace_bytes,
+                          (cudaStream_t)stream);
+}
+
+// allocation base of a device pointer (torch's caching allocator hands out
+// sub-allocations; IPC handles name whole allocations)
+static int alloc_base(const void *p, void **base_out) {
+    static PFN_cuMemGetAddressRange_v3020 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *q = nullptr;
+        cudaDriverEntryPointQueryResult r;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &q, cudaEnableDefault, &r) == cudaSuccess &&
+            r == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(q);
+    });
+    if (!fn) return set_error(ES_ERR_CUDA, "cuMemGetAddressRange is unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, (CUdeviceptr)(uintptr_t)p) != CUDA_SUCCESS)
+        return set_error(ES_ERR_ARG, "not a device allocation");
+    *base_out = (void *)(uintptr_t)base;
+    return ES_OK;
+}
+
+extern "C" int es_ipc_handle(const void *dev_ptr, void *handle_out, int64_t *offset_out) {
+    if (!dev_ptr || !handle_out || !offset_out) return set_error(ES_ERR_ARG, "null pointer");
+    void *base = nullptr;
+    int rc = alloc_base(dev_ptr, &base);
+    if (rc) return rc;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, base) != cudaSuccess) return check_launch("cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (int64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+    return ES_OK;
+}
+
+extern "C" int es_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return set_error(ES_ERR_ARG, "null pointer");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void *p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return check_launch("cudaIpcOpenMemHandle");
+    *dev_ptr_out = static_cast<char *>(p) + offset;
+    return ES_OK;
+}
+
+extern "C" int es_ipc_close(void *dev_ptr) {
+    if (!dev_ptr) return set_error(ES_ERR_ARG, "null pointer");
+    void *base = nullptr;
+    int rc = alloc_base(dev_ptr, &base);
+    if (rc) return rc;
+    if (cudaIpcCloseMemHandle(base) != cudaSuccess) return check_launch("cudaIpcCloseMemHandle");
+    return ES_OK;
 }
 
 extern "C" size_t es_leja_state_offset(void) { return series_state_offset(); }

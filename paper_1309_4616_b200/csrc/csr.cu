@@ -316,8 +316,9 @@ static CsrLayout csr_layout(int64_t n, int width = 1) {
     const int64_t rows_per_chunk = (int64_t)W4_T * W4_CHB;  // 16384
     L.nchunks = (int)std::max<int64_t>(1, (n + rows_per_chunk - 1) / rows_per_chunk);
     size_t o = 0;
-    L.params = o; o = up(o + sizeof(SeriesParams));
-    L.state = o; o = up(o + sizeof(SeriesState));
+    L.params = o;
+    L.state = o = series_state_offset();  // es_leja_fetch reads the state here
+    o = up(o + sizeof(SeriesState));
     L.cnt = o; o = up(o + sizeof(unsigned) * (L.nchunks + 1));
     L.part = o; o = up(o + sizeof(double) * 2 * (size_t)L.nchunks * W4_CHB);
     L.slice = o; o = up(o + sizeof(double) * 2 * (size_t)L.nchunks);

@@ -120,6 +120,35 @@ ES_DEV bool reduce_and_decide(const SeriesParams &P, int k, int chunk, int64_t s
 // Separate reduction step of the TMA node (one CTA per slice = z-chunk):
 // slice c's entries (tile, warp partials) are summed thread-strided, warp
 // trees, warps in order; the last CTA sums the slices in order and decides.
+// Slice c's sums (thread 0 of the CTA gets them): entries thread-strided,
+// warp trees, warps in order.
+ES_DEV void cta_slice_sum(const SeriesParams &P, int c, double &a_out, double &b_out) {
+    __shared__ double s_w[32], s_p[32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+    const double *row = P.part + (int64_t)c * P.ntiles * 2;
+    double aw = 0.0, ap = 0.0;
+    for (int e = t; e < P.ntiles; e += blockDim.x) {
+        aw = add(aw, __ldcg(row + 2 * e));
+        ap = add(ap, __ldcg(row + 2 * e + 1));
+    }
+    aw = warp_sum(aw);
+    ap = warp_sum(ap);
+    if (lane == 0) {
+        s_w[warp] = aw;
+        s_p[warp] = ap;
+    }
+    __syncthreads();
+    if (t == 0) {
+        double a = s_w[0], b = s_p[0];
+        for (int w = 1; w < nw; ++w) {
+            a = add(a, s_w[w]);
+            b = add(b, s_p[w]);
+        }
+        a_out = a;
+        b_out = b;
+    }
+}
+
 ES_DEV void slice_reduce_decide(const SeriesParams &P, int k) {
     __shared__ double s_w[32], s_p[32];
     __shared__ int s_last;
@@ -196,6 +225,85 @@ ES_DEV Pass node_pass(const SeriesParams &P, int k) {
     ps.dk = P.dd[k];
     ps.d0 = P.dd[0];
     return ps;
+}
+
+// ----- peer-memory (NVLink P2P) multi-GPU rounds --------------------------------
+//
+// Every rank adds 1 to every rank's arrival counter once per round (round 0:
+// the initial halo exchange, round k: node k), after its round's peer writes
+// are fenced; a rank proceeds past round j once its own counter reaches
+// base + nranks (j + 1).  A timeout (a peer died or was never launched) ends
+// the series with converged = -1 instead of hanging the GPU.
+
+ES_DEV unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// One thread: signal every rank, then wait for all ranks' arrivals of this round.
+ES_DEV bool p2p_round(const SeriesParams &P, int round) {
+    __threadfence_system();
+    for (int q = 0; q < P.nranks; ++q) atomicAdd_system(P.rank_arrive[q], 1ull);
+    const unsigned long long target = P.base + (unsigned long long)P.nranks * (unsigned long long)(round + 1);
+    const unsigned long long t0 = global_ns();
+    for (;;) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(P.arrive_local) : "memory");
+        if (v >= target) return true;
+        if ((long long)(global_ns() - t0) > P.timeout_ns) return false;
+        __nanosleep(256);
+    }
+}
+
+// in_graph: called from a kernel of the series' while-loop body (the round-0
+// kernel runs before the graph; the loop then exits at its first slice kernel)
+ES_DEV void p2p_fail(const SeriesParams &P, int k, bool in_graph) {
+    SeriesState &st = *P.state;
+    st.k = k;
+    st.done = 1;
+    st.converged = -1;  // es_leja_fetch: peer exchange timed out
+    if (in_graph && P.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)P.cond, 0);
+}
+
+// Slice reduction of a peer-memory node: this rank's slices go into every
+// rank's table (rank order = global z order), then the round barrier, then
+// the identical stopping test on every rank over the full table.
+ES_DEV void slice_p2p_decide(const SeriesParams &P, int k) {
+    __shared__ int s_last, s_ok;
+    const int c = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    double a = 0.0, b = 0.0;
+    cta_slice_sum(P, c, a, b);
+    const int par = k & 1;
+    if (t == 0) {
+        for (int q = 0; q < P.nranks; ++q)
+            *reinterpret_cast<double2 *>(P.rank_slices[q] + ((int64_t)par * P.total_slices + P.slice_off + c) * 2) =
+                make_double2(a, b);
+        __threadfence_system();
+        s_last = atomicAdd(P.global_cnt, 1u) == gridDim.x - 1u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (t == 0) {
+        *P.global_cnt = 0u;
+        s_ok = p2p_round(P, k);
+    }
+    __syncthreads();
+    if (!s_ok) {
+        if (t == 0) p2p_fail(P, k, true);
+        return;
+    }
+    if (warp == 0) {
+        const double *tab = P.rank_slices[P.rank] + (int64_t)par * P.total_slices * 2;
+        double sw = 0.0, sp = 0.0;
+        for (int64_t s = lane; s < P.total_slices; s += 32) {
+            sw = add(sw, __ldcg(tab + 2 * s));
+            sp = add(sp, __ldcg(tab + 2 * s + 1));
+        }
+        sw = warp_sum(sw);
+        sp = warp_sum(sp);
+        if (lane == 0) decide(P, k, sw, sp);
+    }
 }
 
 }  // namespace es

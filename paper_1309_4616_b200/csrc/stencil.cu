@@ -136,8 +136,9 @@ __global__ void __launch_bounds__(TMA_THREADS, (COEFF == ES_COEFF_RADIAL && !DIM
     const Pass ps = node_pass(P, k);
     const TmaMaps &M = *static_cast<const TmaMaps *>(P.maps);
     const int wi = k == 1 ? 0 : 1 + ((k - 1) & 1);
-    const PassMaps mp{&M.m[2 * wi], &M.m[2 * wi + 1], &M.m[MAP_P_0 + ((k - 1) & 1)], &M.m[MAP_G], &M.m[MAP_HLO],
-                      &M.m[MAP_HHI]};
+    const bool odd = P.p2p && (k & 1);  // peer-memory series: node k reads halo parity k & 1
+    const PassMaps mp{&M.m[2 * wi], &M.m[2 * wi + 1], &M.m[MAP_P_0 + ((k - 1) & 1)], &M.m[MAP_G],
+                      &M.m[odd ? MAP_HLO_1 : MAP_HLO], &M.m[odd ? MAP_HHI_1 : MAP_HHI]};
     tma_pass<DIM3, COEFF, GD, true>(P.g, ps, mp, P.chunk_len, true, tsmem, Pp, k, P.work);
 }
 
@@ -147,6 +148,58 @@ __global__ void __launch_bounds__(256) k_slice_reduce(const SeriesParams *__rest
     if (P.state->done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0 && P.work) *P.work = 0u;  // every node CTA has finished claiming
     slice_reduce_decide(P, P.state->k + 1);
+}
+
+// Peer-memory series: slice reduction + round barrier + shared decision.
+// Peer-memory series, after node k: every CTA first pushes its share of the
+// slab's first / last plane of w_k into the neighbours' halo buffers of
+// parity (k + 1) & 1 (NVLink stores, 16 B per thread), then reduces its
+// slice and joins the round.  (Storing the planes from the node kernel's
+// epilogue instead overlaps the transfer with the sweep, but costs the hot
+// kernel registers: 974 vs 897 us per 512^3 node even without peers.)
+__global__ void __launch_bounds__(256) k_slice_p2p(const SeriesParams *__restrict__ Pp) {
+    const SeriesParams &P = *Pp;
+    if (P.state->done) {  // the series ended before this node (round-0 failure): leave the loop
+        if (blockIdx.x == 0 && threadIdx.x == 0 && P.cond)
+            cudaGraphSetConditional((cudaGraphConditionalHandle)P.cond, 0);
+        return;
+    }
+    const int k = P.state->k + 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && P.work) *P.work = 0u;
+    const int par = (k + 1) & 1;
+    const double2 *w = reinterpret_cast<const double2 *>(P.wbuf[k & 1]);
+    double2 *lo = reinterpret_cast<double2 *>(P.peer_lo[par]), *hi = reinterpret_cast<double2 *>(P.peer_hi[par]);
+    const int64_t half = P.g.nx * P.g.ny / 2, lz = P.g.lz;
+    if (lo || hi) {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < half; i += (int64_t)gridDim.x * blockDim.x) {
+            if (lo) lo[i] = __ldcg(w + i);
+            if (hi) hi[i] = __ldcg(w + (lz - 1) * half + i);
+        }
+        __threadfence_system();
+        __syncthreads();
+    }
+    slice_p2p_decide(P, k);
+}
+
+// Peer-memory series, round 0: v's first / last plane into the neighbours'
+// halo buffers of parity 1 (read by node 1), then the round barrier.
+__global__ void __launch_bounds__(256) k_p2p_init(const SeriesParams *__restrict__ Pp, int64_t plane, int64_t lz) {
+    __shared__ int s_last;
+    const SeriesParams &P = *Pp;
+    const int64_t half = plane / 2;  // plane = nx * ny, nx even on the TMA path: double2 copies
+    const double2 *v = reinterpret_cast<const double2 *>(P.v);
+    double2 *lo = reinterpret_cast<double2 *>(P.peer_lo[1]), *hi = reinterpret_cast<double2 *>(P.peer_hi[1]);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < half; i += (int64_t)gridDim.x * blockDim.x) {
+        if (lo) lo[i] = v[i];
+        if (hi) hi[i] = v[(lz - 1) * half + i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(P.global_cnt, 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    *P.global_cnt = 0u;
+    if (!p2p_round(P, 0)) p2p_fail(P, 0, false);
 }
 
 __global__ void k_publish_maps(const TmaMaps maps, TmaMaps *dst) {
@@ -608,7 +661,8 @@ struct SeriesSetup {
 static int prepare_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
                           const double *xi, int ndd, double alpha, double shift, double tol, const double *gdiag,
                           const double *halo_lo, const double *halo_hi, bool dist, void *ws, size_t ws_bytes,
-                          SeriesSetup &S, cudaStream_t stream) {
+                          SeriesSetup &S, cudaStream_t stream, const double *halo_lo_1 = nullptr,
+                          const double *halo_hi_1 = nullptr) {
     S.n = d->nx * d->ny * d->lz;
     char *w = static_cast<char *>(ws);
     S.pl = plan_stencil(d, {v, p_out, gdiag, halo_lo, halo_hi, (const void *)(w + 0)}, true);
@@ -666,6 +720,8 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
         if (!rc) rc = encode_map(&maps.m[MAP_G], gdiag, d, pl.dim2, MK_P);
         if (!rc) rc = encode_map(&maps.m[MAP_HLO], halo_lo, d, pl.dim2, MK_HALO);
         if (!rc) rc = encode_map(&maps.m[MAP_HHI], halo_hi, d, pl.dim2, MK_HALO);
+        if (!rc) rc = encode_map(&maps.m[MAP_HLO_1], halo_lo_1, d, pl.dim2, MK_HALO);
+        if (!rc) rc = encode_map(&maps.m[MAP_HHI_1], halo_hi_1, d, pl.dim2, MK_HALO);
         if (rc) return rc;
         TmaMaps *dmaps = reinterpret_cast<TmaMaps *>(w + L.maps);
         k_publish_maps<<<1, 32, 0, stream>>>(maps, dmaps);
@@ -804,6 +860,73 @@ int dist_end(const void *ws, cudaStream_t stream) {
     std::lock_guard<std::mutex> lk(g_dist_mu);
     g_dist.erase(ws);
     return rc;
+}
+
+// ----- peer-memory (NVLink P2P) slab series ------------------------------------
+//
+// One CUDA graph per series and rank, no host involvement per node: node k
+// writes its boundary planes of w_k into the neighbours' halo buffers
+// (parity (k + 1) & 1) from the consumer epilogue, the slice kernel writes
+// this slab's per-chunk sums into every rank's table and joins the round
+// barrier, and every rank evaluates the identical stopping test on the full
+// table (rank order = global z order: with chunk-aligned slabs the sums are
+// bitwise those of one GPU).
+
+int stencil_nslices(const es_stencil_desc *d) { return plan_stencil(d, {}, true).nslices; }
+
+int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double *v, double *p_out, const double *dd,
+                   const double *xi, int ndd, double alpha, double shift, double tol, const double *gdiag, void *ws,
+                   size_t ws_bytes, cudaStream_t stream) {
+    if (ndd < 2) return set_error(ES_ERR_ARG, "a peer-memory series needs ndd >= 2");
+    if (x->nranks < 1 || x->rank < 0 || x->rank >= x->nranks || !x->rank_slices || !x->rank_arrive ||
+        !x->arrive_local)
+        return set_error(ES_ERR_ARG, "bad peer-memory descriptor");
+    if ((x->halo_lo[0] == nullptr) != (x->halo_lo[1] == nullptr) || (x->halo_hi[0] == nullptr) != (x->halo_hi[1] == nullptr) ||
+        (x->peer_lo[0] == nullptr) != (x->halo_lo[0] == nullptr) || (x->peer_hi[0] == nullptr) != (x->halo_hi[0] == nullptr))
+        return set_error(ES_ERR_ARG, "halo / peer buffers must come in parity pairs, one per existing neighbour");
+    SeriesSetup S;
+    int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, x->halo_lo[0], x->halo_hi[0], false, ws,
+                            ws_bytes, S, stream, x->halo_lo[1], x->halo_hi[1]);
+    if (rc) return rc;
+    if (!S.pl.tma || S.pl.dim2) return set_error(ES_ERR_ARG, "peer-memory series need the 3D TMA path");
+    if (x->slice_offset < 0 || x->slice_offset + S.pl.nslices > x->total_slices)
+        return set_error(ES_ERR_ARG, "slice offset / total do not cover this slab's %d slices", S.pl.nslices);
+    SeriesParams &hp = S.hp;
+    hp.p2p = 1;
+    hp.nranks = x->nranks;
+    hp.rank = x->rank;
+    hp.slice_off = x->slice_offset;
+    hp.total_slices = x->total_slices;
+    for (int i = 0; i < 2; ++i) {
+        hp.peer_lo[i] = x->peer_lo[i];
+        hp.peer_hi[i] = x->peer_hi[i];
+    }
+    hp.rank_slices = x->rank_slices;
+    hp.rank_arrive = x->rank_arrive;
+    hp.arrive_local = x->arrive_local;
+    hp.base = x->base;
+    hp.timeout_ns = x->timeout_ns > 0 ? x->timeout_ns : 10000000000ll;
+    GraphKernel gk[2] = {{(const void *)S.nf, S.lp.grid, S.lp.block, S.lp.smem},
+                         {(const void *)k_slice_p2p, dim3((unsigned)S.pl.nslices), dim3(256), 0}};
+    unsigned long long handle = 0;
+    cudaGraphExec_t ge = series_graph(gk, 2, S.dparams, &handle);
+    if (ge) hp.cond = handle;
+    k_series_init<<<1, 256, 0, stream>>>(hp, S.dparams);
+    const int64_t plane = d->nx * d->ny;
+    k_p2p_init<<<(unsigned)std::min<int64_t>(std::max<int64_t>(1, (plane / 2 + 255) / 256), 148), 256, 0, stream>>>(
+        S.dparams, plane, d->lz);
+    rc = check_launch("peer-memory series init");
+    if (rc) return rc;
+    if (ge) {
+        if (cudaGraphLaunch(ge, stream) != cudaSuccess) return check_launch("peer-memory series graph");
+    } else {
+        for (int k = 1; k < ndd; ++k) {
+            S.nf<<<S.lp.grid, S.lp.block, S.lp.smem, stream>>>(S.dparams);
+            k_slice_p2p<<<(unsigned)S.pl.nslices, 256, 0, stream>>>(S.dparams);
+        }
+    }
+    k_series_finalize<<<148 * 8, 256, 0, stream>>>(S.dparams, S.n);
+    return check_launch("peer-memory series");
 }
 
 }  // namespace es

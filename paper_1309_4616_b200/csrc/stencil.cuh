@@ -63,6 +63,16 @@ struct SeriesParams {
     const void *maps;  // TmaMaps (workspace) for the TMA node kernel
     unsigned *work;    // dynamic work-item counter of the TMA node kernel
     int dist;          // 1: slab of a multi-GPU series (slices gathered by the caller, k_decide_gathered decides)
+    // peer-memory (NVLink P2P) slab series, es_leja_p2p; p2p == 0 otherwise
+    int p2p;
+    int nranks, rank;
+    int64_t slice_off, total_slices;
+    double *peer_lo[2], *peer_hi[2];    // lower neighbour's halo_hi / upper neighbour's halo_lo, by parity
+    double *const *rank_slices;         // [nranks] -> every rank's slice table [2][total_slices][2]
+    unsigned long long *const *rank_arrive;  // [nranks] -> every rank's arrival counter
+    unsigned long long *arrive_local;
+    unsigned long long base;            // arrival counter before this series
+    long long timeout_ns;
 };
 
 // One pass: what a node (or a plain fused apply) reads and writes.

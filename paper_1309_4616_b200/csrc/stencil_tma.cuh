@@ -40,7 +40,12 @@ constexpr int TMA_THREADS = 32 * (TMA_CONSUMER_WARPS + 1);
 
 // tensor maps of one pass; for 2D, W needs two maps (256-wide and 4-wide
 // boxes: TMA boxes are at most 256 elements per dimension)
-enum { MAP_WA_V = 0, MAP_WB_V, MAP_WA_0, MAP_WB_0, MAP_WA_1, MAP_WB_1, MAP_P_0, MAP_P_1, MAP_G, MAP_HLO, MAP_HHI, MAP_COUNT };
+// MAP_HLO_1 / MAP_HHI_1: the second parity of the peer-memory slab series'
+// double-buffered halo planes (node k reads parity k & 1)
+enum {
+    MAP_WA_V = 0, MAP_WB_V, MAP_WA_0, MAP_WB_0, MAP_WA_1, MAP_WB_1, MAP_P_0, MAP_P_1, MAP_G, MAP_HLO, MAP_HHI,
+    MAP_HLO_1, MAP_HHI_1, MAP_COUNT
+};
 
 struct alignas(64) TmaMaps {
     CUtensorMap m[MAP_COUNT];

@@ -287,17 +287,132 @@ class CudaRowBackend(_CudaSeriesBackend):
         self.comm.exchange(self.source(k), self.op.xg)
 
 
+class PeerSlab:
+    """Peer-memory (NVLink P2P) resources of one rank's slab series
+    (es_leja_p2p): double-buffered halo planes the neighbours write into,
+    the rank-ordered slice table every rank writes into, the arrival
+    counter; peers' buffers mapped through CUDA IPC handles exchanged over
+    torch.distributed.  Construct collectively on every rank."""
+
+    def __init__(self, op: StencilOperator, comm: SlabComm, timeout_s: float = 30.0):
+        self.lib = _lib.load()
+        self.comm = comm
+        c = comm
+        dev = torch.device("cuda", torch.cuda.current_device())
+        plane = c.plane
+        # [lo parity 0, lo parity 1, hi parity 0, hi parity 1]
+        self.halo = torch.zeros(4 * plane, dtype=torch.float64, device=dev)
+        d, keep = op.desc(z0=c.z_lo, lz=c.lz)
+        ns = ctypes.c_int32()
+        _lib.check(self.lib.es_leja_stencil_nslices(ctypes.byref(d), ctypes.byref(ns)), "es_leja_stencil_nslices")
+        counts = [None] * c.world
+        dist.all_gather_object(counts, int(ns.value), group=c.group)
+        self.nslices = int(ns.value)
+        self.slice_offset = sum(counts[: c.rank])
+        self.total_slices = sum(counts)
+        self.slices = torch.zeros(2 * self.total_slices * 2, dtype=torch.float64, device=dev)
+        self.arrive = torch.zeros(1, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize()
+        mine = [self._handle(t) for t in (self.halo, self.slices, self.arrive)]
+        everyone = [None] * c.world
+        dist.all_gather_object(everyone, mine, group=c.group)
+        self._opened = []
+        ptrs = []  # per rank: (halo, slices, arrive) device addresses valid here
+        for q, hs in enumerate(everyone):
+            if q == c.rank:
+                ptrs.append((self.halo.data_ptr(), self.slices.data_ptr(), self.arrive.data_ptr()))
+            else:
+                ptrs.append(tuple(self._open(h) for h in hs))
+        self.rank_slices = torch.tensor([p[1] for p in ptrs], dtype=torch.int64, device=dev)
+        self.rank_arrive = torch.tensor([p[2] for p in ptrs], dtype=torch.int64, device=dev)
+        self.timeout_ns = int(timeout_s * 1e9)
+        self.rounds = 0
+        x = _lib.P2PDesc()
+        x.nranks, x.rank = c.world, c.rank
+        x.slice_offset, x.total_slices = self.slice_offset, self.total_slices
+        base = self.halo.data_ptr()
+        for par in range(2):
+            if c.rank > 0:  # receive from / send to the lower neighbour
+                x.halo_lo[par] = base + 8 * par * plane
+                x.peer_lo[par] = ptrs[c.rank - 1][0] + 8 * (2 + par) * plane  # its halo_hi
+            if c.rank < c.world - 1:
+                x.halo_hi[par] = base + 8 * (2 + par) * plane
+                x.peer_hi[par] = ptrs[c.rank + 1][0] + 8 * par * plane  # its halo_lo
+        x.rank_slices = self.rank_slices.data_ptr()
+        x.rank_arrive = self.rank_arrive.data_ptr()
+        x.arrive_local = self.arrive.data_ptr()
+        x.timeout_ns = self.timeout_ns
+        self.desc = x
+        dist.barrier(group=c.group)
+
+    def _handle(self, t: torch.Tensor):
+        h = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64()
+        _lib.check(self.lib.es_ipc_handle(t.data_ptr(), h, ctypes.byref(off)), "es_ipc_handle")
+        return (h.raw, int(off.value))
+
+    def _open(self, handle):
+        raw, off = handle
+        p = ctypes.c_void_p()
+        _lib.check(self.lib.es_ipc_open(ctypes.create_string_buffer(raw, 64), off, ctypes.byref(p)), "es_ipc_open")
+        self._opened.append(p.value)
+        return int(p.value)
+
+    def enqueue(self, d, v, p_out, dd, xi, alpha, shift, tol, gdiag, ws):
+        """Enqueue the whole series (one graph) on the current stream."""
+        self.desc.base = self.comm.world * self.rounds
+        rc = self.lib.es_leja_p2p(ctypes.byref(d), ctypes.byref(self.desc), ptr(v), ptr(p_out), ptr(dd), ptr(xi),
+                                  dd.numel(), float(alpha), float(shift), float(tol), ptr(gdiag), ptr(ws), ws.numel(),
+                                  stream_handle())
+        _lib.check(rc, "es_leja_p2p")
+
+    def fetch(self, ws):
+        res = _lib.SeriesResult()
+        rc = self.lib.es_leja_fetch(ptr(ws), ctypes.byref(res), stream_handle())
+        if rc != _lib.ES_ERR_NOT_CONVERGED:
+            _lib.check(rc, "es_leja_fetch")
+        self.rounds += int(res.matvecs) + 1  # round 0 + one per node, identical on every rank
+        return res
+
+    def close(self):
+        for p in self._opened:
+            self.lib.es_ipc_close(p)
+        self._opened = []
+
+
 class DistributedStencil:
     """One rank's z-slab of a stencil operator; same operator protocol as
     ``StencilOperator`` (``n`` is the local point count, vectors are the
     local slab, flat x fastest)."""
 
-    def __init__(self, op: StencilOperator, group=None, ledger: Optional[TransferLedger] = None, batch: int = 4):
+    def __init__(self, op: StencilOperator, group=None, ledger: Optional[TransferLedger] = None, batch: int = 4,
+                 exchange: str = "auto"):
+        """exchange: 'p2p' -- the peer-memory series (es_leja_p2p: halo
+        planes and slice sums written over NVLink by the kernels, one graph
+        per series); 'nccl' -- the host-driven series (NCCL send/recv and
+        all-gather per node); 'auto' -- p2p when every rank can map its
+        neighbours' memory (CUDA IPC), else nccl."""
         if op.bc.kind in ("none", "function"):
             raise GridMismatchError("slab series need homogeneous Dirichlet or Neumann boundaries")
+        if exchange not in ("auto", "p2p", "nccl"):
+            raise ValueError(f"unknown exchange {exchange!r}")
         g = op.grid
         self.base_operator = op
         self.comm = SlabComm(g.nx, g.ny, g.nz, group)
+        self.peer = None
+        if exchange != "nccl" and dist.get_backend(group) == "nccl":
+            try:
+                self.peer = PeerSlab(op, self.comm)
+            except Exception:
+                if exchange == "p2p":
+                    raise
+                self.peer = None
+            ok = torch.tensor([0 if self.peer is None else 1], device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)  # every rank takes the same path
+            if int(ok.item()) == 0 and self.peer is not None:
+                self.peer.close()
+                self.peer = None
+        self.exchange = "p2p" if self.peer is not None else "nccl"
         self.ledger = ledger if ledger is not None else TransferLedger()
         self.batch = batch
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -344,6 +459,19 @@ class DistributedStencil:
 
     def _leja(self, v, p_out, dd, xi, alpha, shift, tol, gdiag=None):
         d, keep = self.desc()
+        if self.peer is not None:
+            tm = timing.active()
+            ev0 = timing.event() if tm else None
+            ws = self._workspace()
+            self.peer.enqueue(d, v, p_out, dd, xi, alpha, shift, tol, gdiag, ws)
+            ev1 = timing.event() if tm else None
+            res = self.peer.fetch(ws)
+            for _ in range(int(res.matvecs)):
+                self.ledger.record(self.comm.ledger_scalars(), 8)
+            if tm:
+                tm.add(ev0, ev1, res.matvecs)
+            del keep
+            return res
         be = CudaSlabBackend(self.base_operator, self.comm, self._workspace(), self.halo_lo, self.halo_hi)
         tm = timing.active()
         ev0 = timing.event() if tm else None

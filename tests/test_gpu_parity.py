@@ -592,3 +592,157 @@ def test_complex_series_large_vs_oracle():
     ref, mv_ref = orc.newton_csr_z(oc, it.dd, it.xi, iv.center, iv.halfspan, 1.0 / iv.halfspan, v, 1e-10)
     got, mv = es.newton_apply(a, it, v, 1e-10)
     assert mv == mv_ref and got.tobytes() == ref.tobytes()
+
+
+# ---- peer-memory (NVLink P2P) slab series, emulated ranks on one device -----
+
+
+def _p2p_ranks(op, bounds, timeout_ns=5_000_000_000):
+    """Per-rank buffers and es_p2p_desc of an in-process emulation: every
+    "peer" address is another emulated rank's local buffer."""
+    import ctypes
+
+    from paper_1309_4616_b200 import _lib
+
+    lib = _lib.load()
+    g = op.grid
+    plane = g.nx * g.ny
+    m = len(bounds)
+    counts = []
+    for lo, hi in bounds:
+        d, _ = op.desc(z0=lo, lz=hi - lo)
+        ns = ctypes.c_int32()
+        _lib.check(lib.es_leja_stencil_nslices(ctypes.byref(d), ctypes.byref(ns)))
+        counts.append(ns.value)
+    total = sum(counts)
+    ranks = []
+    for r, (lo, hi) in enumerate(bounds):
+        ranks.append(dict(lo=lo, hi=hi, halo=torch.zeros(4 * plane, dtype=torch.float64, device="cuda"),
+                          slices=torch.zeros(4 * total, dtype=torch.float64, device="cuda"),
+                          arrive=torch.zeros(1, dtype=torch.int64, device="cuda"), off=sum(counts[:r])))
+    rank_slices = torch.tensor([q["slices"].data_ptr() for q in ranks], dtype=torch.int64, device="cuda")
+    rank_arrive = torch.tensor([q["arrive"].data_ptr() for q in ranks], dtype=torch.int64, device="cuda")
+    for r, q in enumerate(ranks):
+        x = _lib.P2PDesc()
+        x.nranks, x.rank, x.slice_offset, x.total_slices = m, r, q["off"], total
+        for par in range(2):
+            if r > 0:
+                x.halo_lo[par] = q["halo"].data_ptr() + 8 * par * plane
+                x.peer_lo[par] = ranks[r - 1]["halo"].data_ptr() + 8 * (2 + par) * plane
+            if r < m - 1:
+                x.halo_hi[par] = q["halo"].data_ptr() + 8 * (2 + par) * plane
+                x.peer_hi[par] = ranks[r + 1]["halo"].data_ptr() + 8 * par * plane
+        x.rank_slices, x.rank_arrive, x.arrive_local = rank_slices.data_ptr(), rank_arrive.data_ptr(), \
+            q["arrive"].data_ptr()
+        x.timeout_ns = timeout_ns
+        q["desc"] = x
+        q["stream"] = torch.cuda.Stream()
+        d, keep = op.desc(z0=q["lo"], lz=q["hi"] - q["lo"])
+        q["d"], q["keep"] = d, keep
+        q["ws"] = torch.empty(int(lib.es_leja_stencil_workspace_bytes(ctypes.byref(d))), dtype=torch.uint8,
+                              device="cuda")
+    return ranks, (rank_slices, rank_arrive)
+
+
+def _p2p_run(op, ranks, it, v, tol, rounds, only=None, gdiag=None):
+    import ctypes
+
+    from paper_1309_4616_b200 import _lib
+    from paper_1309_4616_b200.device import ptr
+
+    lib = _lib.load()
+    plane = op.grid.nx * op.grid.ny
+    dd, xi = it.device_coeffs()
+    vd = torch.from_numpy(v).cuda()
+    gd = None if gdiag is None else torch.from_numpy(gdiag).cuda()
+    launched = []
+    for r, q in enumerate(ranks):
+        if only is not None and r not in only:
+            continue
+        q["v"] = vd[q["lo"] * plane: q["hi"] * plane].clone()
+        q["g"] = None if gd is None else gd[q["lo"] * plane: q["hi"] * plane].clone()
+        q["p"] = torch.empty_like(q["v"])
+        q["desc"].base = len(ranks) * rounds
+        q["stream"].wait_stream(torch.cuda.current_stream())  # no device sync: the ranks must overlap
+        with torch.cuda.stream(q["stream"]):
+            rc = lib.es_leja_p2p(ctypes.byref(q["d"]), ctypes.byref(q["desc"]), ptr(q["v"]), ptr(q["p"]), ptr(dd),
+                                 ptr(xi), dd.numel(), 1.0 / it.interval.halfspan,
+                                 it.interval.center / it.interval.halfspan, tol, ptr(q["g"]), ptr(q["ws"]),
+                                 q["ws"].numel(), q["stream"].cuda_stream)
+            _lib.check(rc, "es_leja_p2p")
+        launched.append(q)
+    out = []
+    for q in launched:
+        res = _lib.SeriesResult()
+        rc = lib.es_leja_fetch(ptr(q["ws"]), ctypes.byref(res), q["stream"].cuda_stream)
+        out.append((rc, res.matvecs, q["p"].cpu().numpy()))
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_p2p_slab_series_emulated_ranks_bitwise(graph, monkeypatch):
+    if not graph:
+        monkeypatch.setenv("ES_NO_GRAPH", "1")
+    g = es.Grid3D(64, 40, 48)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    bounds = [(0, 16), (16, 40), (40, 48)]  # chunk-aligned: decisions bitwise those of one domain
+    ranks, keep = _p2p_ranks(op, bounds)
+    rounds = 0
+    for target, scale, tol in (("exp", -4e-4, 0.0), ("phi1", -3e-4, 1e-8), ("exp", -4e-4, 1e-8)):
+        it = es.make_interpolant(es.gershgorin_interval(op), target, scale, 40, 1e-8)
+        v = np.random.default_rng(21).standard_normal(g.n)
+        ref, mv = es.newton_apply(op, it, v, tol)
+        outs = _p2p_run(op, ranks, it, v, tol, rounds)
+        assert [o[0] for o in outs] == [0, 0, 0]
+        assert [o[1] for o in outs] == [mv] * 3
+        assert np.concatenate([o[2] for o in outs]).tobytes() == ref.tobytes()
+        rounds += mv + 1  # consecutive series continue the counters
+
+
+def test_p2p_slab_series_rosenbrock_diag_and_neumann():
+    g = es.Grid3D(32, 24, 40)
+    op = es.StencilOperator(g, es.BoundaryCondition.neumann())
+    bounds = [(0, 8), (8, 16), (16, 32), (32, 40)]
+    ranks, keep = _p2p_ranks(op, bounds)
+    it = es.make_interpolant(es.gershgorin_interval(op).widened(50.0), "phi1", -5e-4, 50, 1e-8)
+    v = np.random.default_rng(5).standard_normal(g.n)
+    gd = np.random.default_rng(6).random(g.n) * 30.0
+    ref, mv = es.newton_apply(es.RosenbrockOperator(op, torch.from_numpy(gd).cuda()), it, v, 1e-10)
+    outs = _p2p_run(op, ranks, it, v, 1e-10, 0, gdiag=gd)
+    assert [o[1] for o in outs] == [mv] * 4
+    assert np.concatenate([o[2] for o in outs]).tobytes() == np.asarray(ref).tobytes()
+
+
+def test_p2p_missing_peer_times_out_instead_of_hanging():
+    from paper_1309_4616_b200 import _lib
+
+    g = es.Grid3D(32, 16, 16)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    ranks, keep = _p2p_ranks(op, [(0, 8), (8, 16)], timeout_ns=200_000_000)
+    it = es.make_interpolant(es.gershgorin_interval(op), "exp", -1e-3, 20, 1e-8)
+    v = np.random.default_rng(1).standard_normal(g.n)
+    (rc, mv, _), = _p2p_run(op, ranks, it, v, 0.0, 0, only=[0])
+    assert rc == _lib.ES_ERR_CUDA and "peer" in _lib.last_error()
+
+
+def test_distributed_stencil_p2p_world1():
+    import torch.distributed as dist
+
+    from paper_1309_4616_b200.distributed import DistributedStencil
+
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    g = es.Grid3D(64, 32, 24)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    dop = DistributedStencil(op, exchange="p2p")
+    assert dop.exchange == "p2p"
+    v = torch.from_numpy(np.random.default_rng(2).standard_normal(g.n)).cuda()
+    for tol in (1e-8, 0.0, 1e-8):
+        it = es.make_interpolant(es.gershgorin_interval(op), "phi1", -3e-4, 60, 1e-8)
+        ref, mv = es.newton_apply(op, it, v, tol)
+        got, mv2 = es.newton_apply(dop, it, v, tol)
+        assert mv2 == mv and torch.equal(got, ref)
+    dop.peer.close()

@@ -19,7 +19,11 @@ for spec in specs:
     bc = {"neumann": es.BoundaryCondition.neumann(), "homogeneous": es.BoundaryCondition.homogeneous(),
           "none": es.BoundaryCondition.none()}[parts[1] or "homogeneous"]
     g = es.Grid3D(nx, ny, nz)
-    op = es.StencilOperator(g, bc, coeff=es.radial_coeff if parts[2] == "radial" else None)
+    op = es.StencilOperator(g, bc, coeff=es.radial_coeff if parts[2] in ("radial", "array") else None)
+    if parts[2] == "array":  # the same D, staged as a sampled array (ES_COEFF_ARRAY)
+        from paper_1309_4616_b200 import _lib
+
+        op._coeff_kind = _lib.ES_COEFF_ARRAY
     nodes = 24
     it = es.make_interpolant(es.gershgorin_interval(op), "phi1", -1e-7, nodes, 1e-8)
     v = torch.randn(g.n, dtype=torch.float64, device="cuda")
