@@ -212,6 +212,33 @@ int es_leja_p2p(const es_stencil_desc *d, const es_p2p_desc *p2p, const double *
                 double tol, const double *gdiag, void *workspace, size_t workspace_bytes,
                 void *stream);
 
+/* Peer-memory row-block CSR series: the fused compute + all-gather form of
+ * es_leja_csr_dist_*.  Every rank keeps its gathered vector twice
+ * (xg_local[0..1], npad doubles each; rank_xg[q] is rank q's buffer base,
+ * parity 1 at + npad): node k gathers from parity k & 1 and stores each of
+ * its rows' w_k at row_offset + r of EVERY rank's parity (k + 1) & 1
+ * buffer; slices, arrival counters, base and timeout as in es_p2p_desc.
+ * Column indices address the padded gathered layout (rank q's rows at
+ * q * width, like the NCCL form).  Completion / result: es_leja_fetch. */
+typedef struct es_p2p_rows_desc {
+    int32_t nranks, rank;
+    int64_t slice_offset, total_slices;
+    int64_t row_offset, npad;
+    double *xg_local[2];
+    double *const *rank_xg;
+    double *const *rank_slices;
+    unsigned long long *const *rank_arrive;
+    unsigned long long *arrive_local;
+    unsigned long long base;
+    int64_t timeout_ns;
+} es_p2p_rows_desc;
+
+int es_leja_csr_nslices(int64_t n_local, int32_t *nslices_out);
+int es_leja_csr_p2p(int64_t n_local, const int64_t *row_ptr, const int32_t *col_idx,
+                    const double *vals, const es_p2p_rows_desc *p2p, const double *v,
+                    double *p_out, const double *dd, const double *xi, int32_t ndd, double alpha,
+                    double shift, double tol, void *workspace, size_t workspace_bytes, void *stream);
+
 /* CUDA IPC for the peer mappings: a 64-byte handle of a device allocation
  * (cudaIpcGetMemHandle; offset_out = dev_ptr - allocation base) and its
  * mapping in another process (peer access over NVLink). */

@@ -31,7 +31,7 @@ EXPORTS = (
     "es_leja_state_offset", "es_leja_csr_dist_begin", "es_leja_csr_dist_source", "es_leja_csr_dist_nslices",
     "es_leja_csr_dist_node", "es_leja_csr_dist_end", "es_csr_fused_rows_z", "es_leja_csr_z_workspace_bytes",
     "es_leja_csr_z", "es_leja_csr_z_async", "es_leja_stencil_nslices", "es_leja_p2p", "es_ipc_handle",
-    "es_ipc_open", "es_ipc_close",
+    "es_ipc_open", "es_ipc_close", "es_leja_csr_nslices", "es_leja_csr_p2p",
 )
 
 
@@ -51,6 +51,17 @@ class P2PDesc(ctypes.Structure):
         ("slice_offset", ctypes.c_int64), ("total_slices", ctypes.c_int64),
         ("halo_lo", ctypes.c_void_p * 2), ("halo_hi", ctypes.c_void_p * 2),
         ("peer_lo", ctypes.c_void_p * 2), ("peer_hi", ctypes.c_void_p * 2),
+        ("rank_slices", ctypes.c_void_p), ("rank_arrive", ctypes.c_void_p), ("arrive_local", ctypes.c_void_p),
+        ("base", ctypes.c_uint64), ("timeout_ns", ctypes.c_int64),
+    ]
+
+
+class P2PRowsDesc(ctypes.Structure):
+    _fields_ = [
+        ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
+        ("slice_offset", ctypes.c_int64), ("total_slices", ctypes.c_int64),
+        ("row_offset", ctypes.c_int64), ("npad", ctypes.c_int64),
+        ("xg_local", ctypes.c_void_p * 2), ("rank_xg", ctypes.c_void_p),
         ("rank_slices", ctypes.c_void_p), ("rank_arrive", ctypes.c_void_p), ("arrive_local", ctypes.c_void_p),
         ("base", ctypes.c_uint64), ("timeout_ns", ctypes.c_int64),
     ]
@@ -105,6 +116,8 @@ def _declare(lib):
         "es_ipc_handle": ([vp, vp, P(i64)], ctypes.c_int),
         "es_ipc_open": ([vp, i64, P(vp)], ctypes.c_int),
         "es_ipc_close": ([vp], ctypes.c_int),
+        "es_leja_csr_nslices": ([i64, P(i32)], ctypes.c_int),
+        "es_leja_csr_p2p": ([i64, vp, vp, vp, P(P2PRowsDesc), vp, vp, vp, vp, i32, d, d, d, vp, sz, vp], ctypes.c_int),
         "es_leja_csr_z": ([i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, d, d, d, d, vp, sz, P(SeriesResult), vp],
                           ctypes.c_int),
         "es_leja_csr_z_async": ([i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, d, d, d, d, vp, sz, vp],

@@ -332,6 +332,24 @@ static int alloc_base(const void *p, void **base_out) {
     return ES_OK;
 }
 
+extern "C" int es_leja_csr_nslices(int64_t n_local, int32_t *nslices_out) {
+    if (n_local < 0 || !nslices_out) return set_error(ES_ERR_ARG, "bad argument");
+    *nslices_out = csr_nslices(n_local);
+    return ES_OK;
+}
+
+extern "C" int es_leja_csr_p2p(int64_t n_local, const int64_t *row_ptr, const int32_t *col_idx, const double *vals,
+                               const es_p2p_rows_desc *p2p, const double *v, double *p_out, const double *dd,
+                               const double *xi, int32_t ndd, double alpha, double shift, double tol, void *workspace,
+                               size_t workspace_bytes, void *stream) {
+    if (n_local < 1) return set_error(ES_ERR_ARG, "a row block needs at least one row");
+    if (!p2p || !v || !p_out || !dd || !xi || !workspace || !row_ptr || !col_idx || !vals)
+        return set_error(ES_ERR_ARG, "null pointer");
+    if (v == p_out) return set_error(ES_ERR_ARG, "p_out must not alias v");
+    return run_csr_p2p_series(n_local, row_ptr, col_idx, vals, p2p, v, p_out, dd, xi, ndd, alpha, shift, tol,
+                              workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
 extern "C" int es_ipc_handle(const void *dev_ptr, void *handle_out, int64_t *offset_out) {
     if (!dev_ptr || !handle_out || !offset_out) return set_error(ES_ERR_ARG, "null pointer");
     void *base = nullptr;

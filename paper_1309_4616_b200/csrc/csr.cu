@@ -121,7 +121,11 @@ constexpr int W4_WARPS = 4;
 constexpr int W4_T = 32 * W4_WARPS;               // rows per CTA tile
 constexpr int W4_CHB = 16384 / W4_T;              // tiles per 16384-row chunk
 
-template <int G, int MINB, int W4_U>
+// P2P: the peer-memory row-block series' variant: gathers come from this
+// rank's parity buffer xgp[k & 1], and every row's w_k is stored into every
+// rank's gathered vector of parity (k + 1) & 1 -- the all-gather fused into
+// the node, overlapped with its gather-bound sweep.
+template <int G, int MINB, int W4_U, bool P2P = false>
 __global__ void __launch_bounds__(W4_T, MINB) k_csr_node_w4(const SeriesParams *__restrict__ Pp) {
     constexpr int W4_ROUND = 32 * W4_U;
     __shared__ double s_prod[W4_WARPS][W4_ROUND];
@@ -134,8 +138,9 @@ __global__ void __launch_bounds__(W4_T, MINB) k_csr_node_w4(const SeriesParams *
     const int64_t r0 = ((int64_t)blockIdx.x * W4_WARPS + warp) * 32;
     const int64_t r = r0 + lane;
     const bool act = r < n;
-    const double *__restrict__ xs = P.xg ? P.xg : (k == 1 ? P.v : P.wbuf[(k - 1) & 1]);
-    const unsigned long long tex = P.xg ? P.tex[3] : P.tex[k == 1 ? 2 : (k - 1) & 1];
+    const double *__restrict__ xs =
+        P2P ? P.xgp[k & 1] : P.xg ? P.xg : (k == 1 ? P.v : P.wbuf[(k - 1) & 1]);
+    const unsigned long long tex = P2P ? P.tex[k & 1] : P.xg ? P.tex[3] : P.tex[k == 1 ? 2 : (k - 1) & 1];
     double acc = 0.0;
     if (r0 < n) {
         const int64_t *__restrict__ rp = P.row_ptr;
@@ -174,6 +179,11 @@ __global__ void __launch_bounds__(W4_T, MINB) k_csr_node_w4(const SeriesParams *
         __stcs(ps.p_dst + r, pn);
         sw = mul(wn, wn);
         sq = mul(pn, pn);
+        if constexpr (P2P) {
+            const int64_t o = (int64_t)((k + 1) & 1) * P.npad + P.row_off + r;
+            for (int q = 0; q < P.nranks; ++q) P.rank_xg[q][o] = wn;
+            __threadfence_system();
+        }
     }
     sw = warp_sum(sw);
     sq = warp_sum(sq);
@@ -197,6 +207,34 @@ __global__ void __launch_bounds__(256) k_csr_slice_reduce(const SeriesParams *__
     const SeriesParams &P = *Pp;
     if (P.state->done) return;
     slice_reduce_decide(P, P.state->k + 1);
+}
+
+// Peer-memory row-block series: slices into every rank's table, round barrier, decision.
+__global__ void __launch_bounds__(256) k_csr_slice_p2p(const SeriesParams *__restrict__ Pp) {
+    const SeriesParams &P = *Pp;
+    if (P.state->done) {  // ended before this node (round-0 failure): leave the loop
+        if (blockIdx.x == 0 && threadIdx.x == 0 && P.cond)
+            cudaGraphSetConditional((cudaGraphConditionalHandle)P.cond, 0);
+        return;
+    }
+    slice_p2p_decide(P, P.state->k + 1);
+}
+
+// Round 0: v's rows into every rank's gathered vector of parity 1 (read by node 1).
+__global__ void __launch_bounds__(256) k_csr_p2p_init(const SeriesParams *__restrict__ Pp) {
+    __shared__ int s_last;
+    const SeriesParams &P = *Pp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = P.v[i];
+        for (int q = 0; q < P.nranks; ++q) P.rank_xg[q][P.npad + P.row_off + i] = x;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(P.global_cnt, 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    *P.global_cnt = 0u;
+    if (!p2p_round(P, 0)) p2p_fail(P, 0, false);
 }
 
 __global__ void k_csr_scale(const double *x, const double *s, double *out, int64_t n) {
@@ -689,6 +727,72 @@ int run_csr_series_z(int64_t n, const int64_t *row_ptr, const int32_t *col, cons
     if (!res) return ES_OK;
     return read_series_state(hp.state, res, stream);
 }
+
+// ----- peer-memory (NVLink P2P) row-block series -------------------------------
+//
+// One CUDA graph per series and rank: node k gathers from this rank's parity
+// buffer and stores each of its rows' w_k into every rank's gathered vector
+// (the all-gather of decomp.py:304-333, fused into the node); the slice
+// kernel writes the per-chunk sums into every rank's table, joins the round
+// barrier and decides identically on every rank.
+
+int run_csr_p2p_series(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *vals,
+                       const es_p2p_rows_desc *x, const double *v, double *p_out, const double *dd, const double *xi,
+                       int ndd, double alpha, double shift, double tol, void *ws, size_t ws_bytes,
+                       cudaStream_t stream) {
+    if (ndd < 2) return set_error(ES_ERR_ARG, "a peer-memory series needs ndd >= 2");
+    if (x->nranks < 1 || x->rank < 0 || x->rank >= x->nranks || !x->rank_xg || !x->rank_slices ||
+        !x->rank_arrive || !x->arrive_local || !x->xg_local[0] || !x->xg_local[1])
+        return set_error(ES_ERR_ARG, "bad peer-memory row descriptor");
+    if (x->row_offset < 0 || x->row_offset + n > x->npad) return set_error(ES_ERR_ARG, "row block outside npad");
+    CsrSetup S;
+    int rc = csr_prepare(n, row_ptr, col, vals, nullptr, 0, v, p_out, dd, xi, ndd, alpha, shift, tol, false, ws,
+                         ws_bytes, S);
+    if (rc) return rc;
+    SeriesParams &hp = S.hp;
+    if (x->slice_offset < 0 || x->slice_offset + hp.nslices > x->total_slices)
+        return set_error(ES_ERR_ARG, "slice offset / total do not cover this block's %d slices", hp.nslices);
+    hp.p2p = 1;
+    hp.nranks = x->nranks;
+    hp.rank = x->rank;
+    hp.slice_off = x->slice_offset;
+    hp.total_slices = x->total_slices;
+    hp.rank_slices = x->rank_slices;
+    hp.rank_arrive = x->rank_arrive;
+    hp.arrive_local = x->arrive_local;
+    hp.base = x->base;
+    hp.timeout_ns = x->timeout_ns > 0 ? x->timeout_ns : 10000000000ll;
+    hp.xgp[0] = x->xg_local[0];
+    hp.xgp[1] = x->xg_local[1];
+    hp.rank_xg = x->rank_xg;
+    hp.row_off = x->row_offset;
+    hp.npad = x->npad;
+    hp.tex[0] = tex_for(hp.xgp[0], x->npad);
+    hp.tex[1] = tex_for(hp.xgp[1], x->npad);
+    const CsrNodeFn nf = (hp.tex[0] && hp.tex[1]) ? k_csr_node_w4<1, 12, 4, true> : k_csr_node_w4<0, 12, 4, true>;
+    GraphKernel gk[2] = {{(const void *)nf, dim3(S.grid), dim3(W4_T), 0},
+                         {(const void *)k_csr_slice_p2p, dim3(S.nslices), dim3(256), 0}};
+    unsigned long long handle = 0;
+    cudaGraphExec_t ge = series_graph(gk, 2, S.dparams, &handle);
+    if (ge) hp.cond = handle;
+    k_csr_init<<<1, 256, 0, stream>>>(hp, S.dparams);
+    k_csr_p2p_init<<<(unsigned)std::min<int64_t>(std::max<int64_t>(1, (n + 255) / 256), 148 * 4), 256, 0, stream>>>(
+        S.dparams);
+    rc = check_launch("peer-memory csr init");
+    if (rc) return rc;
+    if (ge) {
+        if (cudaGraphLaunch(ge, stream) != cudaSuccess) return check_launch("peer-memory csr graph");
+    } else {
+        for (int k = 1; k < ndd; ++k) {
+            nf<<<S.grid, W4_T, 0, stream>>>(S.dparams);
+            k_csr_slice_p2p<<<S.nslices, 256, 0, stream>>>(S.dparams);
+        }
+    }
+    k_csr_finalize<<<148 * 8, 256, 0, stream>>>(S.dparams, n);
+    return check_launch("peer-memory csr series");
+}
+
+int csr_nslices(int64_t n) { return csr_layout(n).nchunks; }
 
 // ----- multi-GPU row-block series (decomp.py:285-345 on one rank per GPU) ----
 //

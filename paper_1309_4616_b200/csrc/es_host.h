@@ -85,6 +85,11 @@ int stencil_nslices(const es_stencil_desc *d);
 int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double *v, double *p_out, const double *dd,
                    const double *xi, int ndd, double alpha, double shift, double tol, const double *gdiag, void *ws,
                    size_t ws_bytes, cudaStream_t stream);
+int csr_nslices(int64_t n);
+int run_csr_p2p_series(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *vals,
+                       const es_p2p_rows_desc *x, const double *v, double *p_out, const double *dd, const double *xi,
+                       int ndd, double alpha, double shift, double tol, void *ws, size_t ws_bytes,
+                       cudaStream_t stream);
 int csr_dist_begin(int64_t n_local, const int64_t *row_ptr, const int32_t *col, const double *vals, const double *xg,
                    int64_t n_xg, const double *v, double *p_out, const double *dd, const double *xi, int ndd, double alpha,
                    double shift, double tol, void *ws, size_t ws_bytes, cudaStream_t stream);

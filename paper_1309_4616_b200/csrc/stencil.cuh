@@ -73,6 +73,10 @@ struct SeriesParams {
     unsigned long long *arrive_local;
     unsigned long long base;            // arrival counter before this series
     long long timeout_ns;
+    // peer-memory row-block CSR series (es_leja_csr_p2p)
+    double *xgp[2];                     // this rank's gathered vector by parity (node k gathers from xgp[k & 1])
+    double *const *rank_xg;             // [nranks] -> every rank's gathered-vector buffer (parity 1 at + npad)
+    int64_t row_off, npad;
 };
 
 // One pass: what a node (or a plain fused apply) reads and writes.

@@ -287,63 +287,49 @@ class CudaRowBackend(_CudaSeriesBackend):
         self.comm.exchange(self.source(k), self.op.xg)
 
 
-class PeerSlab:
-    """Peer-memory (NVLink P2P) resources of one rank's slab series
-    (es_leja_p2p): double-buffered halo planes the neighbours write into,
-    the rank-ordered slice table every rank writes into, the arrival
-    counter; peers' buffers mapped through CUDA IPC handles exchanged over
-    torch.distributed.  Construct collectively on every rank."""
+def _peer_or_none(make, exchange: str, group):
+    """The peer-memory resources when requested / possible on EVERY rank
+    (collective; 'auto' falls back to the NCCL-driven series together)."""
+    if exchange == "nccl" or dist.get_backend(group) != "nccl":
+        if exchange == "p2p":
+            raise RuntimeError("exchange='p2p' needs the NCCL backend (one CUDA device per rank)")
+        return None
+    peer, err = None, None
+    try:
+        peer = make()
+    except Exception as e:  # IPC mapping impossible on this node
+        err = e
+    ok = torch.tensor([0 if peer is None else 1], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)  # every rank takes the same path
+    if int(ok.item()) == 0:
+        if peer is not None:
+            peer.close()
+        if exchange == "p2p":
+            raise RuntimeError(f"peer-memory exchange unavailable: {err}")
+        return None
+    return peer
 
-    def __init__(self, op: StencilOperator, comm: SlabComm, timeout_s: float = 30.0):
+
+class _PeerMemory:
+    """CUDA IPC plumbing shared by the peer-memory series: publish this
+    rank's buffers, map every other rank's, fetch / count rounds."""
+
+    def _exchange(self, comm, tensors):
+        """Device addresses, valid in this process, of every rank's copy of
+        `tensors` (rank order)."""
         self.lib = _lib.load()
-        self.comm = comm
-        c = comm
-        dev = torch.device("cuda", torch.cuda.current_device())
-        plane = c.plane
-        # [lo parity 0, lo parity 1, hi parity 0, hi parity 1]
-        self.halo = torch.zeros(4 * plane, dtype=torch.float64, device=dev)
-        d, keep = op.desc(z0=c.z_lo, lz=c.lz)
-        ns = ctypes.c_int32()
-        _lib.check(self.lib.es_leja_stencil_nslices(ctypes.byref(d), ctypes.byref(ns)), "es_leja_stencil_nslices")
-        counts = [None] * c.world
-        dist.all_gather_object(counts, int(ns.value), group=c.group)
-        self.nslices = int(ns.value)
-        self.slice_offset = sum(counts[: c.rank])
-        self.total_slices = sum(counts)
-        self.slices = torch.zeros(2 * self.total_slices * 2, dtype=torch.float64, device=dev)
-        self.arrive = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._opened = getattr(self, "_opened", [])
         torch.cuda.synchronize()
-        mine = [self._handle(t) for t in (self.halo, self.slices, self.arrive)]
-        everyone = [None] * c.world
-        dist.all_gather_object(everyone, mine, group=c.group)
-        self._opened = []
-        ptrs = []  # per rank: (halo, slices, arrive) device addresses valid here
+        mine = [self._handle(t) for t in tensors]
+        everyone = [None] * comm.world
+        dist.all_gather_object(everyone, mine, group=comm.group)
+        out = []
         for q, hs in enumerate(everyone):
-            if q == c.rank:
-                ptrs.append((self.halo.data_ptr(), self.slices.data_ptr(), self.arrive.data_ptr()))
+            if q == comm.rank:
+                out.append(tuple(t.data_ptr() for t in tensors))
             else:
-                ptrs.append(tuple(self._open(h) for h in hs))
-        self.rank_slices = torch.tensor([p[1] for p in ptrs], dtype=torch.int64, device=dev)
-        self.rank_arrive = torch.tensor([p[2] for p in ptrs], dtype=torch.int64, device=dev)
-        self.timeout_ns = int(timeout_s * 1e9)
-        self.rounds = 0
-        x = _lib.P2PDesc()
-        x.nranks, x.rank = c.world, c.rank
-        x.slice_offset, x.total_slices = self.slice_offset, self.total_slices
-        base = self.halo.data_ptr()
-        for par in range(2):
-            if c.rank > 0:  # receive from / send to the lower neighbour
-                x.halo_lo[par] = base + 8 * par * plane
-                x.peer_lo[par] = ptrs[c.rank - 1][0] + 8 * (2 + par) * plane  # its halo_hi
-            if c.rank < c.world - 1:
-                x.halo_hi[par] = base + 8 * (2 + par) * plane
-                x.peer_hi[par] = ptrs[c.rank + 1][0] + 8 * par * plane  # its halo_lo
-        x.rank_slices = self.rank_slices.data_ptr()
-        x.rank_arrive = self.rank_arrive.data_ptr()
-        x.arrive_local = self.arrive.data_ptr()
-        x.timeout_ns = self.timeout_ns
-        self.desc = x
-        dist.barrier(group=c.group)
+                out.append(tuple(self._open(h) for h in hs))
+        return out
 
     def _handle(self, t: torch.Tensor):
         h = ctypes.create_string_buffer(64)
@@ -358,14 +344,6 @@ class PeerSlab:
         self._opened.append(p.value)
         return int(p.value)
 
-    def enqueue(self, d, v, p_out, dd, xi, alpha, shift, tol, gdiag, ws):
-        """Enqueue the whole series (one graph) on the current stream."""
-        self.desc.base = self.comm.world * self.rounds
-        rc = self.lib.es_leja_p2p(ctypes.byref(d), ctypes.byref(self.desc), ptr(v), ptr(p_out), ptr(dd), ptr(xi),
-                                  dd.numel(), float(alpha), float(shift), float(tol), ptr(gdiag), ptr(ws), ws.numel(),
-                                  stream_handle())
-        _lib.check(rc, "es_leja_p2p")
-
     def fetch(self, ws):
         res = _lib.SeriesResult()
         rc = self.lib.es_leja_fetch(ptr(ws), ctypes.byref(res), stream_handle())
@@ -375,9 +353,103 @@ class PeerSlab:
         return res
 
     def close(self):
-        for p in self._opened:
+        for p in getattr(self, "_opened", []):
             self.lib.es_ipc_close(p)
         self._opened = []
+
+
+class PeerSlab(_PeerMemory):
+    """Peer-memory (NVLink P2P) resources of one rank's slab series
+    (es_leja_p2p): double-buffered halo planes the neighbours write into,
+    the rank-ordered slice table every rank writes into, the arrival
+    counter; peers' buffers mapped through CUDA IPC handles exchanged over
+    torch.distributed.  Construct collectively on every rank."""
+
+    def __init__(self, op: StencilOperator, comm: SlabComm, timeout_s: float = 30.0):
+        self.lib = _lib.load()
+        self.comm = c = comm
+        dev = torch.device("cuda", torch.cuda.current_device())
+        plane = c.plane
+        # [lo parity 0, lo parity 1, hi parity 0, hi parity 1]
+        self.halo = torch.zeros(4 * plane, dtype=torch.float64, device=dev)
+        d, keep = op.desc(z0=c.z_lo, lz=c.lz)
+        ns = ctypes.c_int32()
+        _lib.check(self.lib.es_leja_stencil_nslices(ctypes.byref(d), ctypes.byref(ns)), "es_leja_stencil_nslices")
+        counts = [None] * c.world
+        dist.all_gather_object(counts, int(ns.value), group=c.group)
+        self.slices = torch.zeros(2 * sum(counts) * 2, dtype=torch.float64, device=dev)
+        self.arrive = torch.zeros(1, dtype=torch.int64, device=dev)
+        ptrs = self._exchange(c, (self.halo, self.slices, self.arrive))  # per rank: (halo, slices, arrive)
+        self.rank_slices = torch.tensor([p[1] for p in ptrs], dtype=torch.int64, device=dev)
+        self.rank_arrive = torch.tensor([p[2] for p in ptrs], dtype=torch.int64, device=dev)
+        self.rounds = 0
+        x = _lib.P2PDesc()
+        x.nranks, x.rank = c.world, c.rank
+        x.slice_offset, x.total_slices = sum(counts[: c.rank]), sum(counts)
+        base = self.halo.data_ptr()
+        for par in range(2):
+            if c.rank > 0:  # receive from / send to the lower neighbour
+                x.halo_lo[par] = base + 8 * par * plane
+                x.peer_lo[par] = ptrs[c.rank - 1][0] + 8 * (2 + par) * plane  # its halo_hi
+            if c.rank < c.world - 1:
+                x.halo_hi[par] = base + 8 * (2 + par) * plane
+                x.peer_hi[par] = ptrs[c.rank + 1][0] + 8 * par * plane  # its halo_lo
+        x.rank_slices, x.rank_arrive = self.rank_slices.data_ptr(), self.rank_arrive.data_ptr()
+        x.arrive_local = self.arrive.data_ptr()
+        x.timeout_ns = int(timeout_s * 1e9)
+        self.desc = x
+        dist.barrier(group=c.group)
+
+    def enqueue(self, d, v, p_out, dd, xi, alpha, shift, tol, gdiag, ws):
+        """Enqueue the whole series (one graph) on the current stream."""
+        self.desc.base = self.comm.world * self.rounds
+        rc = self.lib.es_leja_p2p(ctypes.byref(d), ctypes.byref(self.desc), ptr(v), ptr(p_out), ptr(dd), ptr(xi),
+                                  dd.numel(), float(alpha), float(shift), float(tol), ptr(gdiag), ptr(ws), ws.numel(),
+                                  stream_handle())
+        _lib.check(rc, "es_leja_p2p")
+
+
+class PeerRows(_PeerMemory):
+    """Peer-memory resources of one rank's row-block CSR series
+    (es_leja_csr_p2p): the gathered vector twice (by node parity), the slice
+    table and the arrival counter, peers mapped through CUDA IPC.  Construct
+    collectively on every rank."""
+
+    def __init__(self, op: "DistributedCsr", timeout_s: float = 30.0):
+        self.lib = _lib.load()
+        self.comm = c = op.comm
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.xg2 = torch.zeros(2 * c.padded, dtype=torch.float64, device=dev)
+        ns = ctypes.c_int32()
+        _lib.check(self.lib.es_leja_csr_nslices(op.n, ctypes.byref(ns)), "es_leja_csr_nslices")
+        counts = [None] * c.world
+        dist.all_gather_object(counts, int(ns.value), group=c.group)
+        self.slices = torch.zeros(2 * sum(counts) * 2, dtype=torch.float64, device=dev)
+        self.arrive = torch.zeros(1, dtype=torch.int64, device=dev)
+        ptrs = self._exchange(c, (self.xg2, self.slices, self.arrive))
+        self.rank_xg = torch.tensor([p[0] for p in ptrs], dtype=torch.int64, device=dev)
+        self.rank_slices = torch.tensor([p[1] for p in ptrs], dtype=torch.int64, device=dev)
+        self.rank_arrive = torch.tensor([p[2] for p in ptrs], dtype=torch.int64, device=dev)
+        self.rounds = 0
+        x = _lib.P2PRowsDesc()
+        x.nranks, x.rank = c.world, c.rank
+        x.slice_offset, x.total_slices = sum(counts[: c.rank]), sum(counts)
+        x.row_offset, x.npad = c.rank * c.width, c.padded
+        x.xg_local[0] = self.xg2.data_ptr()
+        x.xg_local[1] = self.xg2.data_ptr() + 8 * c.padded
+        x.rank_xg, x.rank_slices = self.rank_xg.data_ptr(), self.rank_slices.data_ptr()
+        x.rank_arrive, x.arrive_local = self.rank_arrive.data_ptr(), self.arrive.data_ptr()
+        x.timeout_ns = int(timeout_s * 1e9)
+        self.desc = x
+        dist.barrier(group=c.group)
+
+    def enqueue(self, op, v, p_out, dd, xi, alpha, shift, tol, ws):
+        self.desc.base = self.comm.world * self.rounds
+        rp, col, vals = op.device_arrays()
+        rc = self.lib.es_leja_csr_p2p(op.n, ptr(rp), ptr(col), ptr(vals), ctypes.byref(self.desc), ptr(v),
+                                      ptr(p_out), ptr(dd), ptr(xi), dd.numel(), float(alpha), float(shift),
+                                      float(tol), ptr(ws), ws.numel(), stream_handle())
+        _lib.check(rc, "es_leja_csr_p2p")
 
 
 class DistributedStencil:
@@ -399,19 +471,7 @@ class DistributedStencil:
         g = op.grid
         self.base_operator = op
         self.comm = SlabComm(g.nx, g.ny, g.nz, group)
-        self.peer = None
-        if exchange != "nccl" and dist.get_backend(group) == "nccl":
-            try:
-                self.peer = PeerSlab(op, self.comm)
-            except Exception:
-                if exchange == "p2p":
-                    raise
-                self.peer = None
-            ok = torch.tensor([0 if self.peer is None else 1], device="cuda")
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)  # every rank takes the same path
-            if int(ok.item()) == 0 and self.peer is not None:
-                self.peer.close()
-                self.peer = None
+        self.peer = _peer_or_none(lambda: PeerSlab(op, self.comm), exchange, group)
         self.exchange = "p2p" if self.peer is not None else "nccl"
         self.ledger = ledger if ledger is not None else TransferLedger()
         self.batch = batch
@@ -494,7 +554,13 @@ class DistributedCsr:
     (the multi-process form of decomp.PartitionedCsr); same operator
     protocol, vectors are the local rows (``n`` = local row count)."""
 
-    def __init__(self, a, group=None, ledger: Optional[TransferLedger] = None, batch: int = 4):
+    def __init__(self, a, group=None, ledger: Optional[TransferLedger] = None, batch: int = 4,
+                 exchange: str = "auto"):
+        """exchange: 'p2p' (es_leja_csr_p2p: every node stores its rows into
+        every rank's gathered vector over NVLink), 'nccl' (host-driven
+        all-gather per node), 'auto' (p2p when CUDA IPC works on all ranks)."""
+        if exchange not in ("auto", "p2p", "nccl"):
+            raise ValueError(f"unknown exchange {exchange!r}")
         if a.nrows != a.ncols:
             raise ValueError("partitioned apply requires a square matrix")
         if a.vals.dtype != np.float64:
@@ -513,6 +579,8 @@ class DistributedCsr:
         self._dev = None
         self._ws = None
         self._xg = None
+        self.peer = _peer_or_none(lambda: PeerRows(self), exchange, group)
+        self.exchange = "p2p" if self.peer is not None else "nccl"
 
     @property
     def n(self) -> int:
@@ -557,6 +625,18 @@ class DistributedCsr:
     def _leja(self, v, p_out, dd, xi, alpha, shift, tol, gdiag=None):
         if gdiag is not None:
             raise NotImplementedError("a Jacobian diagonal is defined for stencil operators only")
+        if self.peer is not None:
+            tm = timing.active()
+            ev0 = timing.event() if tm else None
+            ws = self._workspace()
+            self.peer.enqueue(self, v, p_out, dd, xi, alpha, shift, tol, ws)
+            ev1 = timing.event() if tm else None
+            res = self.peer.fetch(ws)
+            for _ in range(int(res.matvecs)):
+                self.ledger.record(self.comm.ledger_scalars(), 8)
+            if tm:
+                tm.add(ev0, ev1, res.matvecs)
+            return res
         be = CudaRowBackend(self, self._workspace())
         tm = timing.active()
         ev0 = timing.event() if tm else None

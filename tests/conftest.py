@@ -1,6 +1,11 @@
 import os
 import sys
 
+# The emulated multi-rank peer-memory tests run several ranks' series on one
+# device, each on its own stream, and the ranks spin-wait on each other: their
+# streams must not share a hardware work queue (read at CUDA context creation).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 import pytest
 
@@ -33,6 +38,17 @@ def oracle():
 
     orc.lib()
     return orc
+
+
+def fresh_stream():
+    """A newly created non-blocking CUDA stream (not one of torch's pooled
+    streams, which may share a hardware queue with earlier work)."""
+    import torch
+    from cuda.bindings import runtime as rt
+
+    err, s = rt.cudaStreamCreateWithFlags(rt.cudaStreamNonBlocking)
+    assert err == rt.cudaError_t.cudaSuccess, err
+    return torch.cuda.ExternalStream(int(s))
 
 
 def coeff_d(x, y, z):

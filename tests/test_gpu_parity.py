@@ -17,7 +17,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_1309_4616_b200 as es  # noqa: E402
 from oracle import oracle as orc  # noqa: E402
 
-from conftest import coeff_d  # noqa: E402
+from conftest import coeff_d, fresh_stream  # noqa: E402
 
 BCS = {"none": es.BoundaryCondition.none(), "homogeneous": es.BoundaryCondition.homogeneous(),
        "neumann": es.BoundaryCondition.neumann()}
@@ -636,12 +636,55 @@ def _p2p_ranks(op, bounds, timeout_ns=5_000_000_000):
             q["arrive"].data_ptr()
         x.timeout_ns = timeout_ns
         q["desc"] = x
-        q["stream"] = torch.cuda.Stream()
+        q["stream"] = fresh_stream()
         d, keep = op.desc(z0=q["lo"], lz=q["hi"] - q["lo"])
         q["d"], q["keep"] = d, keep
         q["ws"] = torch.empty(int(lib.es_leja_stencil_workspace_bytes(ctypes.byref(d))), dtype=torch.uint8,
                               device="cuda")
+    it0 = es.make_interpolant(es.gershgorin_interval(op), "exp", -1e-4, 3, 1e-8)
+    dd0, xi0 = it0.device_coeffs()
+    v0 = torch.zeros(g.n, dtype=torch.float64, device="cuda")
+    gd0 = torch.zeros(g.n, dtype=torch.float64, device="cuda")
+
+    def launch(q, gd=None):
+        sl = slice(q["lo"] * plane, q["hi"] * plane)
+        q["p0"] = torch.empty(sl.stop - sl.start, dtype=torch.float64, device="cuda")
+        with torch.cuda.stream(q["stream"]):
+            lib.es_leja_p2p(ctypes.byref(q["d"]), ctypes.byref(q["desc"]), v0[sl].data_ptr(), q["p0"].data_ptr(),
+                            dd0.data_ptr(), xi0.data_ptr(), 3, 1.0, 0.0, 0.0, None if gd is None else gd[sl].data_ptr(),
+                            q["ws"].data_ptr(), q["ws"].numel(), q["stream"].cuda_stream)
+
+    _p2p_warm(ranks, launch)
+    _p2p_warm(ranks, lambda q: launch(q, gd0))  # the Rosenbrock (g') node variant too
     return ranks, (rank_slices, rank_arrive)
+
+
+def _p2p_warm(ranks, launch):
+    """Emulation only: build and upload every rank's series graph before the
+    ranks run together.  On one device a graph instantiated while another
+    emulated rank already spins can be held up behind it (in a real run each
+    rank's graph is built in its own process, against its own GPU).  Each
+    rank runs alone with a short timeout, then counters and tables are
+    cleared."""
+    import ctypes
+
+    from paper_1309_4616_b200 import _lib
+    from paper_1309_4616_b200.device import ptr
+
+    lib = _lib.load()
+    for q in ranks:
+        keep = q["desc"].timeout_ns
+        q["desc"].timeout_ns = 50_000_000
+        q["desc"].base = 0
+        launch(q)
+        res = _lib.SeriesResult()
+        lib.es_leja_fetch(ptr(q["ws"]), ctypes.byref(res), q["stream"].cuda_stream)
+        q["desc"].timeout_ns = keep
+        torch.cuda.synchronize()
+        for r in ranks:
+            r["arrive"].zero_()
+            r["slices"].zero_()
+    torch.cuda.synchronize()
 
 
 def _p2p_run(op, ranks, it, v, tol, rounds, only=None, gdiag=None):
@@ -655,22 +698,20 @@ def _p2p_run(op, ranks, it, v, tol, rounds, only=None, gdiag=None):
     dd, xi = it.device_coeffs()
     vd = torch.from_numpy(v).cuda()
     gd = None if gdiag is None else torch.from_numpy(gdiag).cuda()
-    launched = []
-    for r, q in enumerate(ranks):
-        if only is not None and r not in only:
-            continue
+    launched = [q for r, q in enumerate(ranks) if only is None or r in only]
+    for q in launched:  # all host-side preparation before any rank starts spinning
         q["v"] = vd[q["lo"] * plane: q["hi"] * plane].clone()
         q["g"] = None if gd is None else gd[q["lo"] * plane: q["hi"] * plane].clone()
         q["p"] = torch.empty_like(q["v"])
         q["desc"].base = len(ranks) * rounds
-        q["stream"].wait_stream(torch.cuda.current_stream())  # no device sync: the ranks must overlap
+    torch.cuda.synchronize()
+    for q in launched:
         with torch.cuda.stream(q["stream"]):
             rc = lib.es_leja_p2p(ctypes.byref(q["d"]), ctypes.byref(q["desc"]), ptr(q["v"]), ptr(q["p"]), ptr(dd),
                                  ptr(xi), dd.numel(), 1.0 / it.interval.halfspan,
                                  it.interval.center / it.interval.halfspan, tol, ptr(q["g"]), ptr(q["ws"]),
                                  q["ws"].numel(), q["stream"].cuda_stream)
             _lib.check(rc, "es_leja_p2p")
-        launched.append(q)
     out = []
     for q in launched:
         res = _lib.SeriesResult()
@@ -743,6 +784,126 @@ def test_distributed_stencil_p2p_world1():
     for tol in (1e-8, 0.0, 1e-8):
         it = es.make_interpolant(es.gershgorin_interval(op), "phi1", -3e-4, 60, 1e-8)
         ref, mv = es.newton_apply(op, it, v, tol)
+        got, mv2 = es.newton_apply(dop, it, v, tol)
+        assert mv2 == mv and torch.equal(got, ref)
+    dop.peer.close()
+
+
+def _emulated_csr_p2p(a, it, v, tol, bounds, timeout_ns=5_000_000_000, rounds=0, ranks=None):
+    """es_leja_csr_p2p for several row blocks of one matrix, each on its own
+    stream of this device; peers' gathered vectors are the other emulated
+    ranks' local buffers.  Unpadded layout (row_offset = lo, npad = n)."""
+    import ctypes
+
+    from paper_1309_4616_b200 import _lib
+    from paper_1309_4616_b200.device import ptr
+
+    lib = _lib.load()
+    n = a.nrows
+    m = len(bounds)
+    if ranks is None:
+        counts = []
+        for lo, hi in bounds:
+            ns = ctypes.c_int32()
+            _lib.check(lib.es_leja_csr_nslices(hi - lo, ctypes.byref(ns)))
+            counts.append(ns.value)
+        ranks = []
+        for r, (lo, hi) in enumerate(bounds):
+            k0, k1 = int(a.row_ptr[lo]), int(a.row_ptr[hi])
+            ranks.append(dict(lo=lo, hi=hi, off=sum(counts[:r]),
+                              rp=torch.from_numpy(a.row_ptr[lo: hi + 1] - k0).cuda(),
+                              col=torch.from_numpy(a.col_idx[k0:k1].astype(np.int32)).cuda(),
+                              vals=torch.from_numpy(a.vals[k0:k1].copy()).cuda(),
+                              xg2=torch.zeros(2 * n, dtype=torch.float64, device="cuda"),
+                              slices=torch.zeros(4 * sum(counts), dtype=torch.float64, device="cuda"),
+                              arrive=torch.zeros(1, dtype=torch.int64, device="cuda"),
+                              stream=fresh_stream(),
+                              ws=torch.empty(int(lib.es_leja_csr_workspace_bytes(hi - lo)), dtype=torch.uint8,
+                                             device="cuda")))
+        tabs = {key: torch.tensor([q[key].data_ptr() for q in ranks], dtype=torch.int64, device="cuda")
+                for key in ("xg2", "slices", "arrive")}
+        for r, q in enumerate(ranks):
+            x = _lib.P2PRowsDesc()
+            x.nranks, x.rank, x.slice_offset, x.total_slices = m, r, q["off"], sum(counts)
+            x.row_offset, x.npad = q["lo"], n
+            x.xg_local[0], x.xg_local[1] = q["xg2"].data_ptr(), q["xg2"].data_ptr() + 8 * n
+            x.rank_xg, x.rank_slices = tabs["xg2"].data_ptr(), tabs["slices"].data_ptr()
+            x.rank_arrive, x.arrive_local = tabs["arrive"].data_ptr(), q["arrive"].data_ptr()
+            x.timeout_ns = timeout_ns
+            q["desc"], q["tabs"] = x, tabs
+        v0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+        dd0, xi0 = es.make_interpolant(es.gershgorin_interval(a), "exp", -0.1, 3, 1e-8).device_coeffs()
+
+        def launch(q):
+            q["p0"] = torch.empty(q["hi"] - q["lo"], dtype=torch.float64, device="cuda")
+            with torch.cuda.stream(q["stream"]):
+                lib.es_leja_csr_p2p(q["hi"] - q["lo"], ptr(q["rp"]), ptr(q["col"]), ptr(q["vals"]),
+                                    ctypes.byref(q["desc"]), v0[q["lo"]: q["hi"]].data_ptr(), ptr(q["p0"]),
+                                    ptr(dd0), ptr(xi0), 3, 1.0, 0.0, 0.0, ptr(q["ws"]), q["ws"].numel(),
+                                    q["stream"].cuda_stream)
+
+        _p2p_warm(ranks, launch)
+    dd, xi = it.device_coeffs()
+    vd = torch.from_numpy(v).cuda()
+    for q in ranks:  # all host-side preparation before any rank starts spinning
+        q["v"] = vd[q["lo"]: q["hi"]].clone()
+        q["p"] = torch.empty_like(q["v"])
+        q["desc"].base = m * rounds
+    torch.cuda.synchronize()
+    for q in ranks:
+        with torch.cuda.stream(q["stream"]):
+            _lib.check(lib.es_leja_csr_p2p(q["hi"] - q["lo"], ptr(q["rp"]), ptr(q["col"]), ptr(q["vals"]),
+                                           ctypes.byref(q["desc"]), ptr(q["v"]), ptr(q["p"]), ptr(dd), ptr(xi),
+                                           dd.numel(), 1.0 / it.interval.halfspan,
+                                           it.interval.center / it.interval.halfspan, tol, ptr(q["ws"]),
+                                           q["ws"].numel(), q["stream"].cuda_stream), "es_leja_csr_p2p")
+    outs = []
+    for q in ranks:
+        res = _lib.SeriesResult()
+        rc = lib.es_leja_fetch(ptr(q["ws"]), ctypes.byref(res), q["stream"].cuda_stream)
+        outs.append((rc, res.matvecs, q["p"].cpu().numpy()))
+    torch.cuda.synchronize()
+    return outs, ranks
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_csr_p2p_row_blocks_emulated_bitwise(graph, monkeypatch):
+    if not graph:
+        monkeypatch.setenv("ES_NO_GRAPH", "1")
+    from paper_1309_4616_b200.sparse import synthetic_symmetric
+
+    n = 3 * 16384 + 777
+    a = synthetic_symmetric(n, 5, seed=2)
+    bounds = [(0, 16384), (16384, 49152), (49152, n)]
+    ranks, rounds = None, 0
+    for target, scale, tol in (("phi1", -0.7, 0.0), ("exp", -0.5, 1e-8), ("phi1", -0.7, 1e-8)):
+        it = es.make_interpolant(es.gershgorin_interval(a), target, scale, 50, 1e-8)
+        v = np.random.default_rng(3).standard_normal(n)
+        ref, mv = es.newton_apply(a, it, v, tol)
+        outs, ranks = _emulated_csr_p2p(a, it, v, tol, bounds, rounds=rounds, ranks=ranks)
+        assert [o[0] for o in outs] == [0, 0, 0]
+        assert [o[1] for o in outs] == [mv] * 3
+        assert np.concatenate([o[2] for o in outs]).tobytes() == ref.tobytes()
+        rounds += mv + 1
+
+
+def test_distributed_csr_p2p_world1():
+    import torch.distributed as dist
+
+    from paper_1309_4616_b200.distributed import DistributedCsr
+    from paper_1309_4616_b200.sparse import synthetic_symmetric
+
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    a = synthetic_symmetric(70_000, 6, seed=4)
+    dop = DistributedCsr(a, exchange="p2p")
+    assert dop.exchange == "p2p"
+    v = torch.from_numpy(np.random.default_rng(2).standard_normal(a.nrows)).cuda()
+    for tol in (1e-8, 0.0, 1e-8):
+        it = es.make_interpolant(es.gershgorin_interval(a), "phi1", -1.0, 80, 1e-8)
+        ref, mv = es.newton_apply(a, it, v, tol)
         got, mv2 = es.newton_apply(dop, it, v, tol)
         assert mv2 == mv and torch.equal(got, ref)
     dop.peer.close()
