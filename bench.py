@@ -98,6 +98,22 @@ def parse():
     return ap.parse_args()
 
 
+class _StdoutToStderr:
+    """NCCL may print its version banner on stdout at communicator set-up;
+    keep stdout for the one JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -373,8 +389,12 @@ class CsrStepper:
         return p, StepStats(matvecs=mv)
 
     def launches(self, stats) -> int:
-        # init + (node + slice reduce) per matvec + finalize; the row-block driver adds a decide per node
-        return 3 * stats.matvecs + 2 if self.dist else 2 * stats.matvecs + 2
+        # init + (node + slice reduce) per matvec + finalize; + round-0 kernel (p2p);
+        # the NCCL row-block driver adds a decide per node
+        ex = getattr(self.op, "exchange", "none")
+        if ex == "nccl":
+            return 3 * stats.matvecs + 2
+        return 2 * stats.matvecs + (3 if ex == "p2p" else 2)
 
 
 class Stepper:
@@ -402,10 +422,10 @@ class Stepper:
         """Kernels this step launched (counted from the code path).
         A TMA series = publish maps + init + (node + slice reduce) per node + finalize."""
         m = stats.matvecs
-        op = self.problem.operator
-        if self.dist and getattr(op, "exchange", "nccl") == "p2p":
+        ex = getattr(self.problem.operator, "exchange", "none")
+        if self.dist and ex == "p2p":
             series = 2 * m + 4  # + the round-0 halo kernel; no NCCL per node
-        elif self.dist:
+        elif self.dist and ex == "nccl":
             series = 3 * m + 3  # node + slice reduce + decide per node (NCCL kernels not counted)
         else:
             series = 2 * m + 3
@@ -437,18 +457,22 @@ def profiled_traffic(cfg_name: str):
         return None
 
 
-def config_block(args, cfg, n, world, nnz=None):
+def config_block(args, cfg, n, world, nnz=None, replicas=False, exchange="p2p"):
     c = {"workload": cfg["workload"], "config": args.config, "method": cfg["method"], "h": cfg["h"],
          "tol": cfg["tol"]}
+    via = ("NVLink peer memory, fused into the node kernels" if exchange == "p2p"
+           else "NCCL, host-driven per node")
     if nnz is not None:
         c.update({"rows": n, "nnz": nnz,
-                  "parallelism": f"row blocks x{world} (NCCL all-gather of w)" if world > 1 else "single",
+                  "parallelism": f"row blocks x{world} (all-gather of w over {via})" if world > 1 else "single",
                   "l2": f"matrix ({12 * nnz / 2**20:.0f} MiB of vals+col) streams from HBM, larger than L2; "
                         f"the {8 * n / 2**20:.0f} MiB vectors are L2-resident by design (no flush)"})
         return c
     c.update({"grid": list(cfg["dims"]), "bc": cfg["bc"], "coeff": cfg["coeff"],
-              "parallelism": (f"z-slabs x{world} (halo planes and norm slices over NVLink peer memory, "
-                              f"fused into the node kernels)" if world > 1 else "single"),
+              "parallelism": ("single" if world == 1 else
+                              f"replicas x{world} (a single-plane grid cannot be slab-partitioned, "
+                              f"decomp.py:76-77)" if replicas else
+                              f"z-slabs x{world} (halo planes and norm slices over {via})"),
               "l2": f"inputs larger than L2 ({8 * n / 2**20:.0f} MiB per vector)" if 8 * n >= 2**27
               else "working set inside L2 (no flush)"})
     return c
@@ -464,10 +488,15 @@ def run_b200(args, cfg):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     use_dist = world > 1 or args.force_dist
+    # single-plane grids (C1, C2) cannot be slab-partitioned (decomp.py:76-77):
+    # every rank runs the whole problem as an independent replica
+    replicas = world > 1 and not is_csr(cfg) and cfg["dims"][2] == 1
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29541")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        with _StdoutToStderr():
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+            dist.barrier()
     nx, ny, nz = cfg["dims"]
     n = nx * ny * nz  # global points (rows for CSR)
     if is_csr(cfg):
@@ -477,8 +506,8 @@ def run_b200(args, cfg):
         bytes_node = csr_node_bytes(u0.numel(), nnz_local)
         nnz_total = csr_matrix(cfg).nnz
     else:
-        problem, u0 = make_problem(cfg, es, world, use_dist)
-        step = Stepper(cfg, es, problem, use_dist)
+        problem, u0 = make_problem(cfg, es, world, use_dist and not replicas)
+        step = Stepper(cfg, es, problem, use_dist and not replicas)
         bytes_node = cfg["bytes_per_node"] * u0.numel()
     n_local = u0.numel()
 
@@ -556,13 +585,14 @@ def run_b200(args, cfg):
         e1.record()
         barrier()
         e_el = e0.elapsed_time(e1) * 1e-3
-        e_units = float(n) * mv_e2e
+        e_units = float(n) * mv_e2e * (world if replicas else 1)
         if world > 1:
             b = torch.tensor([e_el], dtype=torch.float64, device="cuda")
             dist.all_reduce(b, op=dist.ReduceOp.MAX)
             e_el = float(b.item())
-        e2e = {"value": e_units / e_el / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-               "d2h_bytes_per_step": 8 * n, "steps": e2e_steps, "ms_per_step": 1e3 * e_el / e2e_steps}
+        nb = 8 * n * (world if replicas else 1)
+        e2e = {"value": e_units / e_el / 1e9, "unit": UNIT, "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb, "steps": e2e_steps, "ms_per_step": 1e3 * e_el / e2e_steps}
         if is_csr(cfg):
             e2e["note"] = "the matrix is uploaded once (operator set-up); each step copies v in and p out"
         if world > 1:
@@ -579,13 +609,14 @@ def run_b200(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if world > 1 and not replicas else "weak", "vs_baseline": None, "dtype": "f64",
             "data": ("synthetic: seeded symmetric CSR (default_rng(1234)), v ~ N(0,1) default_rng(1234)"
                      if is_csr(cfg) else
                      "synthetic: fixed v ~ N(0,1), numpy default_rng(1234)" if cfg["method"] == "linear" else
                      "synthetic: u0 = 1 + 0.1 U[0,1), numpy default_rng(1234) over the global grid" if n <= 2**28
                      else "synthetic: u0 = 1 + 0.1 hash(global index)"),
-            "config": config_block(args, cfg, n, world, nnz_total if is_csr(cfg) else None),
+            "config": config_block(args, cfg, n, world, nnz_total if is_csr(cfg) else None, replicas,
+                                   getattr(step.op if is_csr(cfg) else step.problem.operator, "exchange", "p2p")),
             "matvecs_per_step": matvecs / args.steps, "steps_per_s": args.steps / t_max,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             "gpu_launches": launches,

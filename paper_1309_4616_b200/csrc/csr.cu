@@ -182,7 +182,6 @@ __global__ void __launch_bounds__(W4_T, MINB) k_csr_node_w4(const SeriesParams *
         if constexpr (P2P) {
             const int64_t o = (int64_t)((k + 1) & 1) * P.npad + P.row_off + r;
             for (int q = 0; q < P.nranks; ++q) P.rank_xg[q][o] = wn;
-            __threadfence_system();
         }
     }
     sw = warp_sum(sw);
@@ -193,6 +192,9 @@ __global__ void __launch_bounds__(W4_T, MINB) k_csr_node_w4(const SeriesParams *
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        // P2P: one system-scope fence per CTA, cumulative over the CTA's peer
+        // stores ordered before it by the barrier above
+        if constexpr (P2P) __threadfence_system();
         double aw = s_red[0][0], ap = s_red[0][1];
         for (int w = 1; w < W4_WARPS; ++w) {
             aw = add(aw, s_red[w][0]);

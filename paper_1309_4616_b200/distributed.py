@@ -294,6 +294,8 @@ def _peer_or_none(make, exchange: str, group):
         if exchange == "p2p":
             raise RuntimeError("exchange='p2p' needs the NCCL backend (one CUDA device per rank)")
         return None
+    if exchange == "auto" and dist.get_world_size(group) == 1:
+        return None  # nothing to exchange: the caller runs the single-device series
     peer, err = None, None
     try:
         peer = make()
@@ -471,8 +473,13 @@ class DistributedStencil:
         g = op.grid
         self.base_operator = op
         self.comm = SlabComm(g.nx, g.ny, g.nz, group)
-        self.peer = _peer_or_none(lambda: PeerSlab(op, self.comm), exchange, group)
-        self.exchange = "p2p" if self.peer is not None else "nccl"
+        # a single-plane grid has one slab (make_partition refuses m > nz,
+        # decomp.py:76-77): world 1 runs the plain device series
+        self.whole = g.nz == 1
+        self.peer = None if self.whole else _peer_or_none(lambda: PeerSlab(op, self.comm), exchange, group)
+        # one rank and no exchange requested: the single-device series
+        self.whole = self.whole or (self.peer is None and exchange == "auto" and self.comm.world == 1)
+        self.exchange = "none" if self.whole else "p2p" if self.peer is not None else "nccl"
         self.ledger = ledger if ledger is not None else TransferLedger()
         self.batch = batch
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -518,6 +525,8 @@ class DistributedStencil:
         return self._ws
 
     def _leja(self, v, p_out, dd, xi, alpha, shift, tol, gdiag=None):
+        if self.whole:
+            return self.base_operator._leja(v, p_out, dd, xi, alpha, shift, tol, gdiag=gdiag)
         d, keep = self.desc()
         if self.peer is not None:
             tm = timing.active()
@@ -580,7 +589,8 @@ class DistributedCsr:
         self._ws = None
         self._xg = None
         self.peer = _peer_or_none(lambda: PeerRows(self), exchange, group)
-        self.exchange = "p2p" if self.peer is not None else "nccl"
+        self.whole = self.peer is None and exchange == "auto" and c.world == 1
+        self.exchange = "none" if self.whole else "p2p" if self.peer is not None else "nccl"
 
     @property
     def n(self) -> int:
@@ -625,6 +635,8 @@ class DistributedCsr:
     def _leja(self, v, p_out, dd, xi, alpha, shift, tol, gdiag=None):
         if gdiag is not None:
             raise NotImplementedError("a Jacobian diagonal is defined for stencil operators only")
+        if self.whole:  # one rank: the local block is the whole matrix (unpadded, global columns)
+            return self.base_operator._leja(v, p_out, dd, xi, alpha, shift, tol)
         if self.peer is not None:
             tm = timing.active()
             ev0 = timing.event() if tm else None
