@@ -351,6 +351,27 @@ def combustion_cases():
     save("combustion", u=u, g=combustion_g(u))
 
 
+def field_cases():
+    """Field binary files as the reference writes them (grid.py:178-206)."""
+    import tempfile
+
+    from expstencil.grid import write_field_binary
+
+    rng = np.random.default_rng(109)
+    out = {}
+    cases = {"f64": (Grid3D(5, 4, 3), rng.standard_normal(60)),
+             "f32": (Grid3D(7, 1, 2), rng.standard_normal(14).astype(np.float32)),
+             "c128": (Grid3D(3, 3, 1), rng.standard_normal(9) + 1j * rng.standard_normal(9))}
+    with tempfile.TemporaryDirectory() as tmp:
+        for kind, (g, v) in cases.items():
+            path = os.path.join(tmp, kind + ".bin")
+            write_field_binary(Field(g, v), path)
+            out[f"{kind}_dims"] = np.array([g.nx, g.ny, g.nz])
+            out[f"{kind}_values"] = v
+            out[f"{kind}_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    save("field_binary", **out)
+
+
 if __name__ == "__main__":
     stencil_cases()
     slab_cases()
@@ -361,3 +382,4 @@ if __name__ == "__main__":
     csr_cases()
     combustion_cases()
     csr_complex_cases()
+    field_cases()
