@@ -516,6 +516,9 @@ def run_b200(args, cfg):
             dist.barrier()
         torch.cuda.synchronize()
 
+    dist_op = step.op if is_csr(cfg) else step.problem.operator
+    ledger = getattr(dist_op, "ledger", None) if use_dist and not replicas else None
+
     u = u0.clone()
     t = 0.0
     for _ in range(args.warmup):
@@ -525,6 +528,7 @@ def run_b200(args, cfg):
     barrier()
     # ---- device-resident timed region ----
     matvecs, launches = 0, 0
+    moved0 = ledger.bytes_total if ledger is not None else 0
     with ClockSampler(local) as clocks, timing.SeriesTimer() as tm:
         barrier()
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -550,6 +554,16 @@ def run_b200(args, cfg):
         dist.all_reduce(usum, op=dist.ReduceOp.SUM)
         t_max, units = float(tmax.item()), float(usum.item())
     value = units / t_max / 1e9
+    # inter-GPU traffic of the timed region: the reference's ledger formula
+    # (2 (m-1) nx ny halo / (m-1) n all-gather scalars per node), whole job
+    nvlink = None
+    if ledger is not None and world > 1:
+        moved = float(ledger.bytes_total - moved0)
+        peer_gbs = 900.0  # NVLink 5 per GPU per direction
+        nvlink = {"bytes_per_step": moved / args.steps, "GB/s": moved / t_max / 1e9,
+                  "per_gpu_GB/s": moved / t_max / 1e9 / world,
+                  "frac_of_900GBs_per_gpu": moved / t_max / 1e9 / world / peer_gbs,
+                  "note": "ledger bytes (halo planes / gathered vector slices) over the device-timed region"}
 
     # roofline of the dominant kernel: the fused node (series time / nodes)
     node_s = series_s / max(series_mv, 1)
@@ -620,6 +634,7 @@ def run_b200(args, cfg):
             "matvecs_per_step": matvecs / args.steps, "steps_per_s": args.steps / t_max,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             "gpu_launches": launches,
+            "nvlink": nvlink,
         }
         print(json.dumps(line), flush=True)
     if use_dist:
