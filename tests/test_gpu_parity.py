@@ -907,3 +907,58 @@ def test_distributed_csr_p2p_world1():
         got, mv2 = es.newton_apply(dop, it, v, tol)
         assert mv2 == mv and torch.equal(got, ref)
     dop.peer.close()
+
+
+# ---- edge cases (empty / degenerate / zero inputs), reference semantics ------
+
+
+def test_zero_vector_series_stops_after_two_nodes():
+    # |dd_k| ||w|| = 0 <= tol ||p|| = 0 holds at k = 1 and 2 (matfunc.py:302-311)
+    g = es.Grid3D(32, 16, 8)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    it = es.make_interpolant(es.gershgorin_interval(op), "exp", -1e-3, 40, 1e-8)
+    p, mv = es.newton_apply(op, it, np.zeros(g.n), 1e-8)
+    assert mv == 2 and not p.any()
+    from paper_1309_4616_b200.sparse import synthetic_symmetric
+
+    a = synthetic_symmetric(1000, 3, seed=1)
+    it = es.make_interpolant(es.gershgorin_interval(a), "phi1", -0.5, 40, 1e-8)
+    p, mv = es.newton_apply(a, it, np.zeros(1000), 1e-8)
+    assert mv == 2 and not p.any()
+    pz, mvz = es.newton_apply(a, it, np.zeros(1000, dtype=np.complex128), 1e-8)
+    assert mvz == 2 and not pz.any()
+
+
+def test_degenerate_intervals_return_dd0_v():
+    # a == b: one node, dd_0 v, zero matvecs (matfunc.py:285-286)
+    g = es.Grid3D(1, 1, 1)
+    op = es.StencilOperator(g, es.BoundaryCondition.neumann())
+    iv = es.gershgorin_interval(op)
+    assert iv.a == iv.b == 0.0
+    it = es.make_interpolant(iv, "phi1", -0.3, 20, 1e-8)
+    p, mv = es.newton_apply(op, it, np.array([2.5]), 1e-8)
+    assert mv == 0 and p.tobytes() == (it.dd[0] * np.array([2.5])).tobytes()
+    empty = es.CsrMatrix(0, 0, np.zeros(1, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0))
+    it = es.make_interpolant(es.gershgorin_interval(empty), "exp", -1.0, 20, 1e-8)
+    p, mv = es.newton_apply(empty, it, np.zeros(0), 1e-8)
+    assert mv == 0 and p.shape == (0,)
+    diag = es.CsrMatrix.from_dense(np.diag([3.0, 3.0, 3.0]))
+    it = es.make_interpolant(es.gershgorin_interval(diag), "exp", -0.5j, 20, 1e-8)  # complex dd_0
+    v = np.array([1.0, -2.0, 0.5])
+    p, mv = es.newton_apply(diag, it, v, 1e-8)
+    assert mv == 0 and p.tobytes() == (it.dd[0] * v).tobytes()
+
+
+def test_convergence_error_carries_residual_and_degree():
+    g = es.Grid3D(24, 24, 24)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    it = es.make_interpolant(es.gershgorin_interval(op), "exp", -5e-3, 6, 1e-12)  # far too few nodes
+    v = np.random.default_rng(0).standard_normal(g.n)
+    with pytest.raises(es.ConvergenceError) as ei:
+        es.newton_apply(op, it, v, 1e-12)
+    spec = orc.StencilSpec(24, 24, 24)
+    lo, hi = spec.gershgorin()
+    with pytest.raises(orc.OracleConvergenceError) as eo:
+        orc.newton_stencil(spec, orc.Interp(lo, hi, "exp", -5e-3, it.xi, it.dd), v, 1e-12)
+    assert ei.value.degree == eo.value.degree == 6
+    assert ei.value.residual == pytest.approx(eo.value.residual, rel=1e-12)
