@@ -1,10 +1,14 @@
 // The device-side series loop: a CUDA graph whose single conditional WHILE
 // node runs the node kernel(s) of a Newton-Leja series until the deciding
 // CTA clears the condition (cudaGraphSetConditional in series.cuh:decide).
-// One graph launch per series, no host round trip per node, no wasted
-// launches after convergence.  Instantiated graphs are cached per (kernels,
+// One graph launch per series, no host round trip per node.  The loop body
+// holds UNROLL copies of the node's kernels: one WHILE iteration costs
+// ~5.4 us on B200 whatever the body (tools/graph_probe.cu), so unrolling
+// amortises it; copies after the decision return at their first load of
+// the series state.  Instantiated graphs are cached per (kernels,
 // launch shapes, device-parameter slot, device): every series re-publishes
 // its parameters into the same workspace slot, so a cached graph stays valid.
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -23,7 +27,7 @@ struct Entry {
 std::mutex g_mu;
 std::map<std::vector<unsigned long long>, Entry> g_cache;
 
-bool build(const GraphKernel *ks, int nk, const void *dparams, Entry &e) {
+bool build(const GraphKernel *ks, int nk, int unroll, const void *dparams, Entry &e) {
     cudaGraph_t graph = nullptr;
     if (cudaGraphCreate(&graph, 0) != cudaSuccess) return false;
     bool ok = false;
@@ -40,12 +44,13 @@ bool build(const GraphKernel *ks, int nk, const void *dparams, Entry &e) {
         void *args[] = {(void *)&dparams};
         cudaGraphNode_t prev = nullptr;
         bool added = true;
-        for (int i = 0; i < nk && added; ++i) {
+        for (int i = 0; i < nk * unroll && added; ++i) {
             cudaKernelNodeParams kp = {};
-            kp.func = const_cast<void *>(ks[i].fn);
-            kp.gridDim = ks[i].grid;
-            kp.blockDim = ks[i].block;
-            kp.sharedMemBytes = (unsigned)ks[i].smem;
+            const GraphKernel &kk = ks[i % nk];
+            kp.func = const_cast<void *>(kk.fn);
+            kp.gridDim = kk.grid;
+            kp.blockDim = kk.block;
+            kp.sharedMemBytes = (unsigned)kk.smem;
             kp.kernelParams = args;
             cudaGraphNode_t node;
             added = cudaGraphAddKernelNode(&node, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp) == cudaSuccess;
@@ -62,8 +67,10 @@ bool build(const GraphKernel *ks, int nk, const void *dparams, Entry &e) {
 
 cudaGraphExec_t series_graph(const GraphKernel *ks, int nk, const void *dparams, unsigned long long *handle) {
     if (env_int("ES_NO_GRAPH", 0)) return nullptr;
+    const int unroll = std::max(1, env_int("ES_GRAPH_UNROLL", 4));
     std::vector<unsigned long long> key;
     key.push_back((unsigned long long)(uintptr_t)dparams);
+    key.push_back((unsigned long long)unroll);
     key.push_back((unsigned long long)current_device());
     for (int i = 0; i < nk; ++i) {
         key.push_back((unsigned long long)(uintptr_t)ks[i].fn);
@@ -77,7 +84,7 @@ cudaGraphExec_t series_graph(const GraphKernel *ks, int nk, const void *dparams,
     auto it = g_cache.find(key);
     if (it == g_cache.end()) {
         Entry e;
-        if (!build(ks, nk, dparams, e)) {
+        if (!build(ks, nk, unroll, dparams, e)) {
             cudaGetLastError();  // graphs unavailable: the caller launches the nodes itself
             return nullptr;
         }
