@@ -85,6 +85,18 @@ int es_csr_fused_rows(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr,
                       const int32_t *col_idx, const double *vals, const double *x, double *y,
                       double alpha, double beta, int32_t use_beta, void *stream);
 
+/* Single-precision twins of the two plain applies (_core.pyx instantiates
+ * its stencil and combustion kernels for float too): weights, alpha, beta
+ * are cast to float and every operation rounds in float.  d->coeff_kind /
+ * d->coeff / d->faces are ignored: the float coefficient (slab-local,
+ * nullable) and the six float face arrays (ES_MODE_FACES) come separately.
+ * The combustion twin does NOT check the domain (callers do, as the
+ * reference's integrator.py:43-49) and uses CUDA expf (<= 2 ulp from libm). */
+int es_stencil_fused_slab_f32(const es_stencil_desc *d, const float *u, float *out, double alpha,
+                              double beta, const float *coeff, const float *const *faces,
+                              const float *halo_lo, const float *halo_hi, void *stream);
+int es_combustion_pointwise_f32(const float *u, float *out, int64_t n, void *stream);
+
 /* out = (2 - u)/4 * exp(20 (1 - 1/u)); if any u <= 0 returns ES_ERR_DOMAIN
  * with the first offending index in *first_bad_host (integrator.py:35-54,
  * _core.pyx:341-348).  Synchronises the stream. */

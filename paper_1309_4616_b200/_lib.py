@@ -31,7 +31,8 @@ EXPORTS = (
     "es_leja_state_offset", "es_leja_csr_dist_begin", "es_leja_csr_dist_source", "es_leja_csr_dist_nslices",
     "es_leja_csr_dist_node", "es_leja_csr_dist_end", "es_csr_fused_rows_z", "es_leja_csr_z_workspace_bytes",
     "es_leja_csr_z", "es_leja_csr_z_async", "es_leja_stencil_nslices", "es_leja_p2p", "es_ipc_handle",
-    "es_ipc_open", "es_ipc_close", "es_leja_csr_nslices", "es_leja_csr_p2p",
+    "es_ipc_open", "es_ipc_close", "es_leja_csr_nslices", "es_leja_csr_p2p", "es_stencil_fused_slab_f32",
+    "es_combustion_pointwise_f32",
 )
 
 
@@ -117,6 +118,8 @@ def _declare(lib):
         "es_ipc_open": ([vp, i64, P(vp)], ctypes.c_int),
         "es_ipc_close": ([vp], ctypes.c_int),
         "es_leja_csr_nslices": ([i64, P(i32)], ctypes.c_int),
+        "es_stencil_fused_slab_f32": ([P(StencilDesc), vp, vp, d, d, vp, vp, vp, vp, vp], ctypes.c_int),
+        "es_combustion_pointwise_f32": ([vp, vp, i64, vp], ctypes.c_int),
         "es_leja_csr_p2p": ([i64, vp, vp, vp, P(P2PRowsDesc), vp, vp, vp, vp, i32, d, d, d, vp, sz, vp], ctypes.c_int),
         "es_leja_csr_z": ([i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, d, d, d, d, vp, sz, P(SeriesResult), vp],
                           ctypes.c_int),

@@ -62,7 +62,9 @@ int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaS
     return ES_OK;
 }
 
-static int check_desc(const es_stencil_desc *d) {
+// pointers = false: only extents / mode / kind are checked (the f32 entry
+// passes its coefficient and faces separately from the descriptor)
+static int check_desc(const es_stencil_desc *d, bool pointers = true) {
     if (!d) return set_error(ES_ERR_ARG, "null descriptor");
     if (d->nx < 1 || d->ny < 1 || d->lz < 0 || d->z0 < 0 || d->z0 + d->lz > d->nz_total)
         return set_error(ES_ERR_ARG, "bad slab extents nx=%lld ny=%lld lz=%lld z0=%lld nz=%lld",
@@ -71,12 +73,13 @@ static int check_desc(const es_stencil_desc *d) {
     if (d->mode < ES_MODE_ZERO || d->mode > ES_MODE_NEUMANN) return set_error(ES_ERR_ARG, "bad mode %d", d->mode);
     if (d->mode == ES_MODE_PERIODIC && (d->z0 != 0 || d->lz != d->nz_total))
         return set_error(ES_ERR_ARG, "periodic wraparound is not defined on a partitioned slab");
-    if (d->mode == ES_MODE_FACES)
+    if (d->mode == ES_MODE_FACES && pointers)
         for (int i = 0; i < 6; ++i)
             if (!d->faces[i]) return set_error(ES_ERR_ARG, "faces mode needs six face arrays");
     if (d->coeff_kind < ES_COEFF_NONE || d->coeff_kind > ES_COEFF_ARRAY)
         return set_error(ES_ERR_ARG, "bad coefficient kind %d", d->coeff_kind);
-    if (d->coeff_kind == ES_COEFF_ARRAY && !d->coeff) return set_error(ES_ERR_ARG, "coefficient array missing");
+    if (d->coeff_kind == ES_COEFF_ARRAY && !d->coeff && pointers)
+        return set_error(ES_ERR_ARG, "coefficient array missing");
     return ES_OK;
 }
 
@@ -381,6 +384,20 @@ extern "C" int es_ipc_close(void *dev_ptr) {
     if (rc) return rc;
     if (cudaIpcCloseMemHandle(base) != cudaSuccess) return check_launch("cudaIpcCloseMemHandle");
     return ES_OK;
+}
+
+extern "C" int es_stencil_fused_slab_f32(const es_stencil_desc *d, const float *u, float *out, double alpha,
+                                         double beta, const float *coeff, const float *const *faces,
+                                         const float *halo_lo, const float *halo_hi, void *stream) {
+    int rc = check_desc(d, false);
+    if (rc) return rc;
+    if (d->nx * d->ny * d->lz > 0 && (!u || !out)) return set_error(ES_ERR_ARG, "null pointer");
+    return launch_stencil_f32(d, u, out, alpha, beta, coeff, faces, halo_lo, halo_hi, (cudaStream_t)stream);
+}
+
+extern "C" int es_combustion_pointwise_f32(const float *u, float *out, int64_t n, void *stream) {
+    if (n < 0 || (n > 0 && (!u || !out))) return set_error(ES_ERR_ARG, "bad argument");
+    return launch_combustion_f32(u, out, n, (cudaStream_t)stream);
 }
 
 extern "C" size_t es_leja_state_offset(void) { return series_state_offset(); }

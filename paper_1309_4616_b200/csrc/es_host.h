@@ -82,6 +82,10 @@ int run_csr_series_z(int64_t n, const int64_t *row_ptr, const int32_t *col, cons
                      double alpha_re, double alpha_im, double shift, double tol, void *ws, size_t ws_bytes,
                      es_series_result *res, cudaStream_t stream);
 int stencil_nslices(const es_stencil_desc *d);
+int launch_stencil_f32(const es_stencil_desc *d, const float *u, float *out, double alpha, double beta,
+                       const float *coeff, const float *const *faces, const float *halo_lo, const float *halo_hi,
+                       cudaStream_t stream);
+int launch_combustion_f32(const float *u, float *out, int64_t n, cudaStream_t stream);
 int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double *v, double *p_out, const double *dd,
                    const double *xi, int ndd, double alpha, double shift, double tol, const double *gdiag, void *ws,
                    size_t ws_bytes, cudaStream_t stream);

@@ -48,8 +48,11 @@ def combustion_g(u, t=None, backend: str = "auto"):
     binds t to `backend` and crashes)."""
     vals = _values(u)
     host = is_host(vals)
-    if (np.asarray(vals).dtype.kind == "c") if host else vals.is_complex():
+    dt = np.asarray(vals).dtype if host else vals.dtype
+    if dt not in (np.float32, np.float64, torch.float32, torch.float64):
         raise DomainError("combustion nonlinearity is real-valued")
+    if dt in (np.float32, torch.float32):  # the reference's float kernel (expf)
+        return _combustion_f32(u, vals, host)
     ud = to_device(vals)
     out = empty(ud.numel())
     bad = ctypes.c_int64(-1)
@@ -58,6 +61,19 @@ def combustion_g(u, t=None, backend: str = "auto"):
         i = int(bad.value)
         raise DomainError(f"combustion nonlinearity undefined at index {i} (u={float(ud[i])!r} <= 0)", index=i)
     _lib.check(rc, "es_combustion_pointwise")
+    res = like_input(out, host)
+    return Field(u.grid, res) if isinstance(u, Field) else res
+
+
+def _combustion_f32(u, vals, host):
+    ud = torch.from_numpy(np.ascontiguousarray(vals)).cuda() if host else vals.contiguous()
+    bad = torch.nonzero(ud <= 0)
+    if bad.numel():  # first u <= 0, like integrator.py:43-49
+        i = int(bad[0, 0])
+        raise DomainError(f"combustion nonlinearity undefined at index {i} (u={float(ud[i])!r} <= 0)", index=i)
+    out = torch.empty_like(ud)
+    _lib.check(_lib.load().es_combustion_pointwise_f32(ptr(ud), ptr(out), ud.numel(), stream_handle()),
+               "es_combustion_pointwise_f32")
     res = like_input(out, host)
     return Field(u.grid, res) if isinstance(u, Field) else res
 

@@ -129,13 +129,14 @@ class CsrMatrix:
         uploaded once."""
         dev = torch.cuda.current_device()
         if dev not in self._dev:
-            if self.vals.dtype not in (np.float64, np.complex128):
-                raise NotImplementedError("device CSR supports fp64 or complex128 values")
             if self.col_idx.dtype != np.int32:
                 raise NotImplementedError("device CSR needs 32-bit column indices")
+            # f32 values are widened exactly: the reference promotes a float32
+            # matrix times a float64-typed product to float64 (sparse.py:163-174)
+            vals = self.vals.astype(np.float64) if self.vals.dtype == np.float32 else self.vals
             self._dev[dev] = (torch.from_numpy(self.row_ptr).to("cuda"),
                               torch.from_numpy(self.col_idx).to("cuda"),
-                              torch.from_numpy(self.vals).to("cuda"))
+                              torch.from_numpy(np.ascontiguousarray(vals)).to("cuda"))
         return self._dev[dev]
 
     def fused_apply_flat(self, alpha, beta, x):

@@ -160,11 +160,13 @@ class StencilOperator:
                 self._coeff_kind = _lib.ES_COEFF_RADIAL if same else _lib.ES_COEFF_ARRAY
         return self._coeff_kind
 
-    def _coeff_device(self) -> torch.Tensor:
-        dev = torch.cuda.current_device()
-        if dev not in self._coeff_dev:
-            self._coeff_dev[dev] = to_device(self.coeff_values("f64").reshape(-1))
-        return self._coeff_dev[dev]
+    def _coeff_device(self, kind: str = "f64") -> torch.Tensor:
+        key = (torch.cuda.current_device(), kind)
+        if key not in self._coeff_dev:
+            vals = self.coeff_values(kind).reshape(-1)
+            self._coeff_dev[key] = (to_device(vals) if kind == "f64"
+                                    else torch.from_numpy(np.ascontiguousarray(vals)).cuda())
+        return self._coeff_dev[key]
 
     def desc(self, z0: int = 0, lz: Optional[int] = None, faces=None):
         """es_stencil_desc of the slab [z0, z0+lz) plus the tensors it points at."""
@@ -273,11 +275,34 @@ def fused_slab(op: StencilOperator, alpha, beta, x3, out3, halo_lo=None, halo_hi
         raise BoundaryKindError("periodic wraparound is not defined on a partitioned slab")
     if kind == "function" and faces is None:
         raise BoundaryKindError("Dirichlet-function apply needs precomputed face values")
+    if x3.dtype == torch.float32:
+        return _fused_slab_f32(op, alpha, beta, x3, out3, halo_lo, halo_hi, z0, lz, faces)
     dfaces = None if faces is None else [to_device(np.asarray(f).reshape(-1)) for f in faces]
     d, keep = op.desc(z0=z0, lz=lz, faces=dfaces)
     rc = _lib.load().es_stencil_fused_slab(ctypes.byref(d), ptr(x3), ptr(out3), float(alpha), float(beta),
                                            ptr(halo_lo), ptr(halo_hi), stream_handle())
     _lib.check(rc, "es_stencil_fused_slab")
+    del keep
+
+
+def _fused_slab_f32(op: StencilOperator, alpha, beta, x3, out3, halo_lo, halo_hi, z0, lz, faces) -> None:
+    """Single precision, like the reference's `_stencil_impl[float]`
+    (weights / alpha / beta cast to float, float arithmetic throughout)."""
+    g = op.grid
+    d, _ = op.desc(z0=z0, lz=lz)
+    coeff = None
+    if op.coeff is not None:
+        coeff = op._coeff_device("f32")[z0 * g.nx * g.ny:(z0 + lz) * g.nx * g.ny]
+    keep = []
+    face_ptrs = None
+    if faces is not None:
+        keep = [torch.from_numpy(np.ascontiguousarray(f, dtype=np.float32).reshape(-1)).cuda() for f in faces]
+        table = (ctypes.c_void_p * 6)(*[f.data_ptr() for f in keep])  # host array of 6 device pointers
+        keep.append(table)
+        face_ptrs = ctypes.cast(table, ctypes.c_void_p)
+    rc = _lib.load().es_stencil_fused_slab_f32(ctypes.byref(d), ptr(x3), ptr(out3), float(alpha), float(beta),
+                                               ptr(coeff), face_ptrs, ptr(halo_lo), ptr(halo_hi), stream_handle())
+    _lib.check(rc, "es_stencil_fused_slab_f32")
     del keep
 
 
@@ -291,10 +316,15 @@ def _fused_flat(op: StencilOperator, alpha, beta, x, faces):
         re = _fused_flat(op, 1.0, 0.0, x.real.copy() if host else x.real.contiguous(), faces)
         im = _fused_flat(op, 1.0, 0.0, x.imag.copy() if host else x.imag.contiguous(), faces)
         return alpha * (re + 1j * im) + beta * x
-    if host and np.asarray(x).dtype == np.float32:
-        raise TypeError("expstencil_b200 computes in fp64; pass f64 data")
-    xd = to_device(x)
-    out = empty(g.n)
+    f32 = (np.asarray(x).dtype == np.float32) if host else x.dtype == torch.float32
+    if f32:  # the reference's float kernel: float in, float out
+        xd = torch.from_numpy(np.ascontiguousarray(x)).cuda() if host else x.contiguous()
+        out = torch.empty(g.n, dtype=torch.float32, device=xd.device)
+    elif not host and x.dtype != torch.float64 or host and np.asarray(x).dtype != np.float64:
+        raise TypeError(f"stencil kernels support f32/f64, got {x.dtype}")
+    else:
+        xd = to_device(x)
+        out = empty(g.n)
     fused_slab(op, alpha, beta, xd, out, faces=faces)
     return like_input(out, host)
 
@@ -305,7 +335,9 @@ def apply(op: StencilOperator, u: Field) -> Field:
         raise GridMismatchError("field is bound to a different grid")
     faces = None
     if op.bc.kind == "function":
-        faces = boundary_faces(op, np.float64)
+        if (np.iscomplexobj(u.values) if is_host(u.values) else u.values.is_complex()):
+            raise BoundaryKindError("Dirichlet-function boundaries are real-valued")
+        faces = boundary_faces(op, np.float32 if u.kind == "f32" else np.float64)
     return Field(u.grid, _fused_flat(op, 1.0, 0.0, u.values, faces))
 
 
@@ -325,7 +357,8 @@ def boundary_source_field(op: StencilOperator, kind: str = "f64") -> Field:
     if op.bc.kind != "function":
         raise BoundaryKindError("boundary source requires a Dirichlet-function boundary")
     zero = zeros_field(op.grid, kind=kind)
-    return Field(op.grid, _fused_flat(op, 1.0, 0.0, zero.values, boundary_faces(op)))
+    faces = boundary_faces(op, np.float32 if kind == "f32" else np.float64)
+    return Field(op.grid, _fused_flat(op, 1.0, 0.0, zero.values, faces))
 
 
 def apply_affine_split(op: StencilOperator, u: Field):
@@ -335,7 +368,7 @@ def apply_affine_split(op: StencilOperator, u: Field):
     if u.grid != op.grid:
         raise GridMismatchError("field is bound to a different grid")
     hom = Field(u.grid, _fused_flat(homogeneous_part(op), 1.0, 0.0, u.values, None))
-    return hom, boundary_source_field(op)
+    return hom, boundary_source_field(op, u.kind)
 
 
 def gershgorin_bounds(op: StencilOperator, gdiag_range=None):

@@ -372,6 +372,58 @@ def field_cases():
     save("field_binary", **out)
 
 
+def f32_cases():
+    """The reference's float kernels: fused stencil applies on f32 fields
+    (all boundary kinds, coefficient, slab + halos through the kernel
+    module), combustion on f32, and a float32 CSR matrix (promoted to f64)."""
+    from expstencil.sparse import fused_spmv
+
+    k = _kernels.get_kernels("compiled")
+    rng = np.random.default_rng(110)
+    out = {}
+    cases = []
+    for dims in ((12, 10, 8), (16, 16, 1), (7, 5, 3), (1, 4, 6)):
+        for bc in ("none", "homogeneous", "poly"):
+            for coeff in (False, True):
+                cases.append((dims, bc, coeff))
+    for i, (dims, bc, coeff) in enumerate(cases):
+        g = Grid3D(*dims)
+        op = StencilOperator(g, bc_of(bc), coeff=coeff_d if coeff else None)
+        x = rng.standard_normal(g.n).astype(np.float32)
+        if bc == "poly":
+            y = apply(op, Field(g, x)).values
+            ab = (1.0, 0.0)
+        else:
+            ab = (float(rng.uniform(0.1, 3.0)), float(rng.uniform(-2.0, 2.0)))
+            y = op.fused_apply_flat(ab[0], ab[1], x)
+        assert y.dtype == np.float32
+        out[f"c{i}_dims"], out[f"c{i}_bc"], out[f"c{i}_coeff"] = np.array(dims), np.array(bc), np.array(coeff)
+        out[f"c{i}_ab"], out[f"c{i}_x"], out[f"c{i}_y"] = np.array(ab), x, y
+    out["ncases"] = np.array(len(cases))
+    # slab with halos, float
+    g = Grid3D(11, 9, 12)
+    op = StencilOperator(g, BoundaryCondition.homogeneous(), coeff=coeff_d)
+    x = rng.standard_normal(g.n).astype(np.float32)
+    x3 = x.reshape(g.shape)
+    z0, lz = 5, 4
+    o3 = np.empty((lz, g.ny, g.nx), dtype=np.float32)
+    c3 = op.coeff_values("f32")[z0:z0 + lz].copy()
+    k.stencil_fused_slab(x3[z0:z0 + lz].copy(), o3, 1.5, -0.25, op.weights(), 0, halo_lo=x3[z0 - 1].copy(),
+                         halo_hi=x3[z0 + lz].copy(), z0=z0, nz_total=g.nz, coeff3=c3)
+    out["slab_x"], out["slab_y"] = x, o3.reshape(-1)
+    # combustion on float32
+    u = rng.uniform(0.05, 2.5, 4000).astype(np.float32)
+    out["comb_u"], out["comb_g"] = u, combustion_g(u)
+    # float32 CSR values
+    n = 500
+    dense = (rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.03)).astype(np.float32)
+    a = CsrMatrix.from_dense(dense)
+    xv = rng.standard_normal(n)
+    out["csr_row_ptr"], out["csr_col"], out["csr_vals"], out["csr_x"] = a.row_ptr, a.col_idx, a.vals, xv
+    out["csr_y"] = fused_spmv(a, 0.7, -1.3, xv)
+    save("f32", **out)
+
+
 if __name__ == "__main__":
     stencil_cases()
     slab_cases()
@@ -383,3 +435,4 @@ if __name__ == "__main__":
     combustion_cases()
     csr_complex_cases()
     field_cases()
+    f32_cases()

@@ -962,3 +962,54 @@ def test_convergence_error_carries_residual_and_degree():
         orc.newton_stencil(spec, orc.Interp(lo, hi, "exp", -5e-3, it.xi, it.dd), v, 1e-12)
     assert ei.value.degree == eo.value.degree == 6
     assert ei.value.residual == pytest.approx(eo.value.residual, rel=1e-12)
+
+
+# ---- single precision plain applies (the reference's float kernels) --------
+
+
+def test_f32_stencil_applies_bitwise(golden):
+    d = golden("f32")
+    for i in range(int(d["ncases"])):
+        g = es.Grid3D(*(int(v) for v in d[f"c{i}_dims"]))
+        bc = str(d[f"c{i}_bc"])
+        bco = (es.BoundaryCondition.function(lambda x, y, z: z * (1 - z) * x * y, "poly") if bc == "poly"
+               else BCS[bc])
+        op = es.StencilOperator(g, bco, coeff=coeff_d if bool(d[f"c{i}_coeff"]) else None)
+        x = d[f"c{i}_x"]
+        if bc == "poly":
+            got = es.apply(op, es.Field(g, x)).values
+        else:
+            a, b = d[f"c{i}_ab"]
+            got = op.fused_apply_flat(float(a), float(b), x)
+        assert got.dtype == np.float32
+        assert got.tobytes() == d[f"c{i}_y"].tobytes(), (i, tuple(d[f"c{i}_dims"]), bc)
+
+
+def test_f32_slab_with_halos_and_coefficient_bitwise(golden):
+    d = golden("f32")
+    g = es.Grid3D(11, 9, 12)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous(), coeff=coeff_d)
+    x3 = torch.from_numpy(d["slab_x"]).cuda().view(g.shape)
+    out = torch.empty((4, g.ny, g.nx), dtype=torch.float32, device="cuda")
+    es.fused_slab(op, 1.5, -0.25, x3[5:9].contiguous(), out, halo_lo=x3[4].contiguous(), halo_hi=x3[9].contiguous(),
+                  z0=5)
+    assert out.cpu().numpy().reshape(-1).tobytes() == d["slab_y"].tobytes()
+
+
+def test_f32_combustion_and_f32_csr(golden):
+    d = golden("f32")
+    g = es.combustion_g(d["comb_u"])
+    assert g.dtype == np.float32
+    # CUDA expf vs libm expf: <= 2 ulp (and a few ulp of float subnormals)
+    np.testing.assert_allclose(g, d["comb_g"], rtol=4e-7, atol=1e-43)
+    with pytest.raises(es.DomainError) as ei:
+        es.combustion_g(np.array([1.0, 0.5, -1.0], dtype=np.float32))
+    assert ei.value.index == 2
+    n = len(d["csr_row_ptr"]) - 1
+    a = es.CsrMatrix(n, n, d["csr_row_ptr"], d["csr_col"], d["csr_vals"])
+    y = es.fused_spmv(a, 0.7, -1.3, d["csr_x"])
+    # the reference promotes to f64 and, with no compiled f32/f64 combo, falls
+    # back to its numpy twin, whose np.add.reduce sums rows pairwise; the
+    # device sums in storage order like every other CSR path (1e-14)
+    assert y.dtype == np.float64
+    np.testing.assert_allclose(y, d["csr_y"], rtol=1e-13, atol=1e-13 * np.max(np.abs(d["csr_y"])))
