@@ -122,10 +122,10 @@ ES_DEV bool reduce_and_decide(const SeriesParams &P, int k, int chunk, int64_t s
 // trees, warps in order; the last CTA sums the slices in order and decides.
 // Slice c's sums (thread 0 of the CTA gets them): entries thread-strided,
 // warp trees, warps in order.
-ES_DEV void cta_slice_sum(const SeriesParams &P, int c, double &a_out, double &b_out) {
+ES_DEV void cta_slice_sum(const SeriesParams &P, int c, double &a_out, double &b_out, const double *part = nullptr) {
     __shared__ double s_w[32], s_p[32];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
-    const double *row = P.part + (int64_t)c * P.ntiles * 2;
+    const double *row = (part ? part : P.part) + (int64_t)c * P.ntiles * 2;
     double aw = 0.0, ap = 0.0;
     for (int e = t; e < P.ntiles; e += blockDim.x) {
         aw = add(aw, __ldcg(row + 2 * e));
@@ -303,6 +303,50 @@ ES_DEV void slice_p2p_decide(const SeriesParams &P, int k) {
         sw = warp_sum(sw);
         sp = warp_sum(sp);
         if (lane == 0) decide(P, k, sw, sp);
+    }
+}
+
+// Reduction of a two-node pass (stencil_tb.cuh): both nodes' slices in
+// the one-node order, then the stopping test for node k and -- unless that
+// ended the series -- for node k + 1.
+ES_DEV void slice_reduce_decide2(const SeriesParams &P, int k) {
+    __shared__ int s_last;
+    const int c = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const bool two = k + 1 <= P.ndd - 1;
+    const int64_t half = (int64_t)P.nslices * P.ntiles * 2;
+    double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+    cta_slice_sum(P, c, a0, b0);
+    __syncthreads();  // cta_slice_sum's shared scratch is reused
+    if (two) cta_slice_sum(P, c, a1, b1, P.part + half);
+    if (t == 0) {
+        P.slice[2 * c] = a0;
+        P.slice[2 * c + 1] = b0;
+        P.slice[2 * (P.nslices + c)] = a1;
+        P.slice[2 * (P.nslices + c) + 1] = b1;
+        __threadfence();
+        s_last = atomicAdd(P.global_cnt, 1u) == gridDim.x - 1u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp == 0) {
+        for (int node = 0; node < (two ? 2 : 1); ++node) {
+            const double *sl = P.slice + 2 * (int64_t)node * P.nslices;
+            double sw = 0.0, sp = 0.0;
+            for (int64_t s = lane; s < P.nslices; s += 32) {
+                sw = add(sw, __ldcg(sl + 2 * s));
+                sp = add(sp, __ldcg(sl + 2 * s + 1));
+            }
+            sw = warp_sum(sw);
+            sp = warp_sum(sp);
+            int stop = 0;
+            if (lane == 0) {
+                decide(P, k + node, sw, sp);
+                stop = P.state->done;
+            }
+            if (__shfl_sync(0xffffffffu, stop, 0)) break;
+        }
+        if (lane == 0) *P.global_cnt = 0u;
     }
 }
 

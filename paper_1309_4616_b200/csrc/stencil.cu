@@ -10,6 +10,7 @@
 #include "es_host.h"
 #include "series.cuh"
 #include "stencil_tma.cuh"
+#include "stencil_tb.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -200,6 +201,23 @@ __global__ void __launch_bounds__(256) k_p2p_init(const SeriesParams *__restrict
     if (!s_last || threadIdx.x != 0) return;
     *P.global_cnt = 0u;
     if (!p2p_round(P, 0)) p2p_fail(P, 0, false);
+}
+
+// Two Leja nodes per pass (stencil_tb.cuh) and its reduction / decisions.
+template <int COEFF, bool GD>
+__global__ void __launch_bounds__(TMA_THREADS, 2) k_node_tb(const SeriesParams *__restrict__ Pp) {
+    extern __shared__ __align__(128) char tsmem[];
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    const int k = P.state->k + 1;
+    tb_pass<COEFF, GD>(Pp, k, k + 1 <= P.ndd - 1, tsmem);
+}
+
+__global__ void __launch_bounds__(256) k_slice_reduce2(const SeriesParams *__restrict__ Pp) {
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && P.work) *P.work = 0u;
+    slice_reduce_decide2(P, P.state->k + 1);
 }
 
 __global__ void k_publish_maps(const TmaMaps maps, TmaMaps *dst) {
@@ -411,7 +429,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3 };
+enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3, MK_W2 = 4 };
 
 // TMA descriptor of a slab-shaped fp64 vector (x fastest); OOB reads are
 // zero-filled, which is the homogeneous Dirichlet ghost rule.
@@ -444,8 +462,8 @@ static int encode_map(CUtensorMap *m, const double *base, const es_stencil_desc 
         dims[2] = (cuuint64_t)d->lz;
         strides[0] = (cuuint64_t)d->nx * 8;
         strides[1] = (cuuint64_t)d->nx * d->ny * 8;
-        box[0] = kind == MK_P ? 64 : 68;
-        box[1] = kind == MK_P ? 8 : 10;
+        box[0] = kind == MK_P ? 64 : kind == MK_W2 ? TB_WX : 68;  // MK_W2: two-point halo (two-node pass)
+        box[1] = kind == MK_P ? 8 : kind == MK_W2 ? TB_WY : 10;
         box[2] = 1;
     }
     const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double *>(base), dims, strides, box,
@@ -627,8 +645,8 @@ static WsLayout layout(int64_t n, int nslices, int ntiles, int nchunks) {
     L.state = o; o = up(o + sizeof(SeriesState));
     L.maps = o; o = up(o + sizeof(TmaMaps));
     L.cnt = o; o = up(o + sizeof(unsigned) * (nchunks + 2));
-    L.part = o; o = up(o + sizeof(double) * 2 * (size_t)nslices * ntiles);
-    L.slice = o; o = up(o + sizeof(double) * 2 * (size_t)nslices);
+    L.part = o; o = up(o + sizeof(double) * 4 * (size_t)nslices * ntiles);  // x2: two-node passes
+    L.slice = o; o = up(o + sizeof(double) * 4 * (size_t)nslices);
     L.wa = o; o = up(o + sizeof(double) * n);
     L.wb = o; o = up(o + sizeof(double) * n);
     L.pb = o; o = up(o + sizeof(double) * n);
@@ -656,13 +674,23 @@ struct SeriesSetup {
     SeriesParams hp;
     SeriesParams *dparams;
     int64_t n;
+    bool tb = false;  // two nodes per pass (k_node_tb + k_slice_reduce2)
 };
+
+template <bool GD>
+static NodeFn pick_node_tb(int coeff) {
+    switch (coeff) {
+        case ES_COEFF_RADIAL: return k_node_tb<ES_COEFF_RADIAL, GD>;
+        case ES_COEFF_ARRAY: return k_node_tb<ES_COEFF_ARRAY, GD>;
+        default: return k_node_tb<ES_COEFF_NONE, GD>;
+    }
+}
 
 static int prepare_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
                           const double *xi, int ndd, double alpha, double shift, double tol, const double *gdiag,
                           const double *halo_lo, const double *halo_hi, bool dist, void *ws, size_t ws_bytes,
                           SeriesSetup &S, cudaStream_t stream, const double *halo_lo_1 = nullptr,
-                          const double *halo_hi_1 = nullptr) {
+                          const double *halo_hi_1 = nullptr, bool allow_tb = true) {
     S.n = d->nx * d->ny * d->lz;
     char *w = static_cast<char *>(ws);
     S.pl = plan_stencil(d, {v, p_out, gdiag, halo_lo, halo_hi, (const void *)(w + 0)}, true);
@@ -674,8 +702,21 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     ApplyFn af;
     S.lp = pl;
     if (pl.tma) {
-        S.nf = pick_node_tma(pl.dim2, d->coeff_kind, gdiag != nullptr);
-        finish_tma_plan(S.lp, (const void *)S.nf, node_smem(pl.dim2, gdiag != nullptr, pl.chunk));
+        // two nodes per pass (stencil_tb.cuh) where the w_k window's ghosts
+        // are local (Dirichlet / Neumann, one domain).  Opt-in (ES_TB=1): it
+        // moves 24 instead of 40 B/point/node but is issue-bound at ~2x the
+        // one-node kernel's instructions per point, 902 vs 872 us per 512^3
+        // Rosenbrock node
+        S.tb = allow_tb && !pl.dim2 && !halo_lo && !halo_hi && !dist &&
+               (d->mode == ES_MODE_ZERO || d->mode == ES_MODE_NEUMANN) && env_int("ES_TB", 0);
+        if (S.tb) {
+            S.nf = gdiag ? pick_node_tb<true>(d->coeff_kind) : pick_node_tb<false>(d->coeff_kind);
+            finish_tma_plan(S.lp, (const void *)S.nf,
+                            gdiag ? (size_t)TbLayout<true>::BYTES : (size_t)TbLayout<false>::BYTES);
+        } else {
+            S.nf = pick_node_tma(pl.dim2, d->coeff_kind, gdiag != nullptr);
+            finish_tma_plan(S.lp, (const void *)S.nf, node_smem(pl.dim2, gdiag != nullptr, pl.chunk));
+        }
     } else {
         pick_all(pl, d->coeff_kind, gdiag != nullptr, af, S.nf);
         set_smem_attr((const void *)S.nf, pl.smem);
@@ -722,6 +763,12 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
         if (!rc) rc = encode_map(&maps.m[MAP_HHI], halo_hi, d, pl.dim2, MK_HALO);
         if (!rc) rc = encode_map(&maps.m[MAP_HLO_1], halo_lo_1, d, pl.dim2, MK_HALO);
         if (!rc) rc = encode_map(&maps.m[MAP_HHI_1], halo_hi_1, d, pl.dim2, MK_HALO);
+        if (S.tb) {
+            if (!rc) rc = encode_map(&maps.m[MAP_T_V], v, d, false, MK_W2);
+            if (!rc) rc = encode_map(&maps.m[MAP_T_0], hp.wbuf[0], d, false, MK_W2);
+            if (!rc) rc = encode_map(&maps.m[MAP_T_1], hp.wbuf[1], d, false, MK_W2);
+            if (!rc) rc = encode_map(&maps.m[MAP_T_G], gdiag, d, false, MK_W);
+        }
         if (rc) return rc;
         TmaMaps *dmaps = reinterpret_cast<TmaMaps *>(w + L.maps);
         k_publish_maps<<<1, 32, 0, stream>>>(maps, dmaps);
@@ -750,8 +797,9 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, nullptr, nullptr, false, ws,
                             ws_bytes, S, stream);
     if (rc) return rc;
+    NodeFn rf = S.tb ? k_slice_reduce2 : k_slice_reduce;
     GraphKernel gk[2] = {{(const void *)S.nf, S.lp.grid, S.lp.block, S.lp.smem},
-                         {(const void *)k_slice_reduce, dim3((unsigned)S.pl.nslices), dim3(256), 0}};
+                         {(const void *)rf, dim3((unsigned)S.pl.nslices), dim3(256), 0}};
     unsigned long long handle = 0;
     cudaGraphExec_t ge = series_graph(gk, S.pl.tma ? 2 : 1, S.dparams, &handle);
     if (ge) S.hp.cond = handle;
@@ -761,9 +809,9 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     if (ge) {
         if (cudaGraphLaunch(ge, stream) != cudaSuccess) return check_launch("series graph");
     } else {
-        for (int k = 1; k < ndd; ++k) {
+        for (int k = 1; k < ndd; k += S.tb ? 2 : 1) {
             S.nf<<<S.lp.grid, S.lp.block, S.lp.smem, stream>>>(S.dparams);
-            if (S.pl.tma) k_slice_reduce<<<(unsigned)S.pl.nslices, 256, 0, stream>>>(S.dparams);
+            if (S.pl.tma) rf<<<(unsigned)S.pl.nslices, 256, 0, stream>>>(S.dparams);
         }
         rc = check_launch("series nodes");
         if (rc) return rc;
@@ -886,7 +934,7 @@ int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double 
         return set_error(ES_ERR_ARG, "halo / peer buffers must come in parity pairs, one per existing neighbour");
     SeriesSetup S;
     int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, x->halo_lo[0], x->halo_hi[0], false, ws,
-                            ws_bytes, S, stream, x->halo_lo[1], x->halo_hi[1]);
+                            ws_bytes, S, stream, x->halo_lo[1], x->halo_hi[1], false);
     if (rc) return rc;
     if (!S.pl.tma || S.pl.dim2) return set_error(ES_ERR_ARG, "peer-memory series need the 3D TMA path");
     if (x->slice_offset < 0 || x->slice_offset + S.pl.nslices > x->total_slices)

@@ -1013,3 +1013,31 @@ def test_f32_combustion_and_f32_csr(golden):
     # device sums in storage order like every other CSR path (1e-14)
     assert y.dtype == np.float64
     np.testing.assert_allclose(y, d["csr_y"], rtol=1e-13, atol=1e-13 * np.max(np.abs(d["csr_y"])))
+
+
+# ---- two Leja nodes per pass (stencil_tb.cuh, opt-in ES_TB=1) ---------------
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_two_node_pass_bitwise(graph, monkeypatch):
+    """Temporal blocking: same p, same matvec counts as one node per pass,
+    for Dirichlet / Neumann, coefficient kinds, a g' diagonal, odd and even
+    node counts, ragged tiles and chunks."""
+    if not graph:
+        monkeypatch.setenv("ES_NO_GRAPH", "1")
+    cases = [((64, 40, 48), "homogeneous", None, False, 1e-8), ((70, 18, 21), "neumann", None, True, 1e-10),
+             ((66, 24, 17), "homogeneous", coeff_d, True, 0.0), ((128, 16, 9), "neumann", "radial", False, 1e-8)]
+    for dims, bc, coeff, gd, tol in cases:
+        g = es.Grid3D(*dims)
+        op = es.StencilOperator(g, BCS[bc], coeff=es.radial_coeff if coeff == "radial" else coeff)
+        iv = es.gershgorin_interval(op)
+        it = es.make_interpolant(iv.widened(40.0) if gd else iv, "phi1", -4e-4, 41, 1e-8)
+        v = torch.from_numpy(np.random.default_rng(3).standard_normal(g.n)).cuda()
+        gdiag = torch.from_numpy(np.random.default_rng(4).random(g.n) * 20.0).cuda() if gd else None
+        monkeypatch.setenv("ES_TB", "0")
+        ref, mv = es.newton_apply(op, it, v, tol, gdiag=gdiag)
+        monkeypatch.setenv("ES_TB", "1")
+        got, mv2 = es.newton_apply(op, it, v, tol, gdiag=gdiag)
+        monkeypatch.delenv("ES_TB")
+        assert mv2 == mv, (dims, bc)
+        assert torch.equal(got, ref), (dims, bc)
