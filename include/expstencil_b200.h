@@ -310,6 +310,59 @@ int es_rosenbrock_prologue(const es_stencil_desc *d, const double *u, double *F,
 /* max |x| (integrator.py:236 observer) into *out_dev. */
 int es_max_abs(const double *x, int64_t n, double *out_dev, void *stream);
 
+/* ---- fused integrator steps (the stage helpers) ----
+ * One C call per step, stream-ordered, one host synchronisation at the end.
+ * They replace the Python orchestration of integrator.py:177-189
+ * (_StepWorkspace.step: exp series, g(u) - b, phi1 series, y + h z) and of the
+ * build-defined exponential Rosenbrock step. */
+#define ES_ERR_RANGE 5 /* es_exprb_step: the interval of M = A - diag(g') differs */
+
+#define ES_NONLIN_NONE 0       /* g = 0 (g_n = -source, or no phi1 series) */
+#define ES_NONLIN_COMBUSTION 1 /* g(u) = (2 - u)/4 exp(20 (1 - 1/u)) */
+
+typedef struct es_step_result {
+    es_series_result exp_series;  /* y = exp(-h A) u (exp-Euler only) */
+    es_series_result phi1_series; /* z = phi1(-h A) g_n  /  phi1(-h M) F */
+    int32_t status_exp, status_phi1; /* ES_OK / ES_ERR_NOT_CONVERGED per series */
+    int64_t first_bad;            /* first index with u <= 0, else -1 */
+    double gprime_min, gprime_max; /* Rosenbrock: range of g'(u) */
+    double lo, hi;                /* Rosenbrock: snapped interval the step needs */
+    float series_ms;              /* device time of the series (fork to join) */
+} es_step_result;
+
+/* Exponential Euler step u_out = exp(-hA) u + h phi1(-hA) g_n with
+ * g_n = g(u) - source (integrator.py:177-189).  The exp and phi1 series share
+ * the nodes xi, alpha and shift (one interval, one h) and run CONCURRENTLY
+ * (the phi1 series on an internal stream forked from `stream`).
+ * scratch: 2 n doubles (g_n, z); ws_exp / ws_phi: two series workspaces of
+ * es_leja_stencil_workspace_bytes each.  u_out must not alias u.
+ * Returns ES_ERR_DOMAIN (first_bad) if any u <= 0 with combustion, or
+ * ES_ERR_NOT_CONVERGED with status_exp / status_phi1 telling which series
+ * ran out of nodes: u_out then holds y (when the exp series converged) and
+ * scratch holds g_n and z, so the caller can run the halving rescue
+ * (matfunc.py:328-373) for that series only. */
+int es_expeuler_step(const es_stencil_desc *d, const double *u, double *u_out, const double *dd_exp,
+                     int32_t ndd_exp, const double *dd_phi, int32_t ndd_phi, const double *xi, double alpha,
+                     double shift, double tol, double h, int32_t nonlinearity, const double *source,
+                     double *scratch, void *ws_exp, void *ws_phi, size_t ws_bytes, es_step_result *result_host,
+                     void *stream);
+
+/* Exponential Rosenbrock-Euler step (build-defined) for the combustion term:
+ * fused prologue F = g(u) - A u, g' = g'(u); the interval of M = A - diag(g')
+ * is [a - max g', b - min g'] snapped outward to multiples of (b - a)/1024
+ * ([a, b]: A's Gershgorin interval).  If it equals [lo, hi] (the interval dd
+ * was built for), runs z = phi1(-hM) F and u_out = u + h z; otherwise returns
+ * ES_ERR_RANGE with the snapped interval in result->lo/hi and F, g' kept in
+ * scratch (2 n doubles) for es_exprb_finish with the right dd.
+ * aux_dev: 4 x u64 device scratch. */
+int es_exprb_step(const es_stencil_desc *d, const double *u, double *u_out, const double *dd, const double *xi,
+                  int32_t ndd, double alpha, double shift, double tol, double h, double a, double b, double lo,
+                  double hi, double *scratch, void *aux_dev, void *workspace, size_t workspace_bytes,
+                  es_step_result *result_host, void *stream);
+int es_exprb_finish(const es_stencil_desc *d, const double *u, double *u_out, const double *dd, const double *xi,
+                    int32_t ndd, double alpha, double shift, double tol, double h, const double *scratch,
+                    void *workspace, size_t workspace_bytes, es_step_result *result_host, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

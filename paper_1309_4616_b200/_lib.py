@@ -16,7 +16,8 @@ from .errors import ConvergenceError, DomainError, ExpStencilError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libexpstencil_b200.so")
 
-ES_OK, ES_ERR_ARG, ES_ERR_NOT_CONVERGED, ES_ERR_DOMAIN, ES_ERR_CUDA = 0, 1, 2, 3, 4
+ES_OK, ES_ERR_ARG, ES_ERR_NOT_CONVERGED, ES_ERR_DOMAIN, ES_ERR_CUDA, ES_ERR_RANGE = 0, 1, 2, 3, 4, 5
+ES_NONLIN_NONE, ES_NONLIN_COMBUSTION = 0, 1
 ES_MODE_ZERO, ES_MODE_PERIODIC, ES_MODE_FACES, ES_MODE_NEUMANN = 0, 1, 2, 3
 ES_COEFF_NONE, ES_COEFF_RADIAL, ES_COEFF_ARRAY = 0, 1, 2
 
@@ -32,7 +33,7 @@ EXPORTS = (
     "es_leja_csr_dist_node", "es_leja_csr_dist_end", "es_csr_fused_rows_z", "es_leja_csr_z_workspace_bytes",
     "es_leja_csr_z", "es_leja_csr_z_async", "es_leja_stencil_nslices", "es_leja_p2p", "es_ipc_handle",
     "es_ipc_open", "es_ipc_close", "es_leja_csr_nslices", "es_leja_csr_p2p", "es_stencil_fused_slab_f32",
-    "es_combustion_pointwise_f32",
+    "es_combustion_pointwise_f32", "es_expeuler_step", "es_exprb_step", "es_exprb_finish",
 )
 
 
@@ -72,6 +73,15 @@ class SeriesResult(ctypes.Structure):
     _fields_ = [
         ("matvecs", ctypes.c_int32), ("converged", ctypes.c_int32),
         ("last_term", ctypes.c_double), ("last_pnorm", ctypes.c_double),
+    ]
+
+
+class StepResult(ctypes.Structure):
+    _fields_ = [
+        ("exp_series", SeriesResult), ("phi1_series", SeriesResult),
+        ("status_exp", ctypes.c_int32), ("status_phi1", ctypes.c_int32), ("first_bad", ctypes.c_int64),
+        ("gprime_min", ctypes.c_double), ("gprime_max", ctypes.c_double),
+        ("lo", ctypes.c_double), ("hi", ctypes.c_double), ("series_ms", ctypes.c_float),
     ]
 
 
@@ -133,6 +143,12 @@ def _declare(lib):
         "es_half_sum": ([vp, vp, vp, i64, vp], ctypes.c_int),
         "es_combustion_jacobian": ([vp, vp, vp, i64, vp], ctypes.c_int),
         "es_max_abs": ([vp, i64, vp, vp], ctypes.c_int),
+        "es_expeuler_step": ([P(StencilDesc), vp, vp, vp, i32, vp, i32, vp, d, d, d, d, i32, vp, vp, vp, vp, sz,
+                              P(StepResult), vp], ctypes.c_int),
+        "es_exprb_step": ([P(StencilDesc), vp, vp, vp, vp, i32, d, d, d, d, d, d, d, d, vp, vp, vp, sz,
+                           P(StepResult), vp], ctypes.c_int),
+        "es_exprb_finish": ([P(StencilDesc), vp, vp, vp, vp, i32, d, d, d, d, vp, vp, sz, P(StepResult), vp],
+                            ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -21,7 +21,7 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libexpstencil_b200.so")
-SOURCES = ["capi.cu", "stencil.cu", "csr.cu", "pointwise.cu", "graph.cu", "f32.cu"]
+SOURCES = ["capi.cu", "stencil.cu", "csr.cu", "pointwise.cu", "graph.cu", "f32.cu", "step.cu"]
 HEADERS = ["es_common.cuh", "es_host.h", "stencil.cuh", "series.cuh", "stencil_tma.cuh", "stencil_tb.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmds, objs = [], []
     for src in SOURCES:
         obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
-        cmd = [cc, *ARCH, *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-c",
+        cmd = [cc, *ARCH, *NVCC_FLAGS, *os.environ.get("ES_NVCC_EXTRA", "").split(), "-I", os.path.join(REPO, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

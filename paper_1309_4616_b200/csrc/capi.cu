@@ -401,3 +401,53 @@ extern "C" int es_combustion_pointwise_f32(const float *u, float *out, int64_t n
 }
 
 extern "C" size_t es_leja_state_offset(void) { return series_state_offset(); }
+
+// ----- fused integrator steps (step.cu) ---------------------------------------
+
+static int check_step(const es_stencil_desc *d, const double *u, const double *u_out, const void *scratch,
+                      const void *ws, const es_step_result *res) {
+    int rc = check_desc(d);
+    if (rc) return rc;
+    if (d->mode == ES_MODE_FACES) return set_error(ES_ERR_ARG, "fused step needs a linear operator (faces mode)");
+    if (!u || !u_out || !scratch || !ws || !res) return set_error(ES_ERR_ARG, "null pointer");
+    if (u == u_out) return set_error(ES_ERR_ARG, "u_out must not alias u");
+    return ES_OK;
+}
+
+extern "C" int es_expeuler_step(const es_stencil_desc *d, const double *u, double *u_out, const double *dd_exp,
+                                int32_t ndd_exp, const double *dd_phi, int32_t ndd_phi, const double *xi,
+                                double alpha, double shift, double tol, double h, int32_t nonlinearity,
+                                const double *source, double *scratch, void *ws_exp, void *ws_phi, size_t ws_bytes,
+                                es_step_result *result_host, void *stream) {
+    int rc = check_step(d, u, u_out, scratch, ws_exp, result_host);
+    if (rc) return rc;
+    if (nonlinearity != ES_NONLIN_NONE && nonlinearity != ES_NONLIN_COMBUSTION)
+        return set_error(ES_ERR_ARG, "unknown nonlinearity %d", nonlinearity);
+    const bool phi = nonlinearity == ES_NONLIN_COMBUSTION || source;
+    if (!dd_exp || !xi || (phi && (!dd_phi || !ws_phi))) return set_error(ES_ERR_ARG, "null pointer");
+    if (phi && ws_phi == ws_exp) return set_error(ES_ERR_ARG, "the two series need separate workspaces");
+    return run_expeuler_step(d, u, u_out, dd_exp, ndd_exp, dd_phi, ndd_phi, xi, alpha, shift, tol, h, nonlinearity,
+                             source, scratch, ws_exp, ws_phi, ws_bytes, result_host, (cudaStream_t)stream);
+}
+
+extern "C" int es_exprb_step(const es_stencil_desc *d, const double *u, double *u_out, const double *dd,
+                             const double *xi, int32_t ndd, double alpha, double shift, double tol, double h,
+                             double a, double b, double lo, double hi, double *scratch, void *aux_dev,
+                             void *workspace, size_t workspace_bytes, es_step_result *result_host, void *stream) {
+    int rc = check_step(d, u, u_out, scratch, workspace, result_host);
+    if (rc) return rc;
+    if (!dd || !xi || !aux_dev) return set_error(ES_ERR_ARG, "null pointer");
+    return run_exprb_step(d, u, u_out, dd, xi, ndd, alpha, shift, tol, h, a, b, lo, hi, scratch, aux_dev, workspace,
+                          workspace_bytes, result_host, (cudaStream_t)stream);
+}
+
+extern "C" int es_exprb_finish(const es_stencil_desc *d, const double *u, double *u_out, const double *dd,
+                               const double *xi, int32_t ndd, double alpha, double shift, double tol, double h,
+                               const double *scratch, void *workspace, size_t workspace_bytes,
+                               es_step_result *result_host, void *stream) {
+    int rc = check_step(d, u, u_out, scratch, workspace, result_host);
+    if (rc) return rc;
+    if (!dd || !xi) return set_error(ES_ERR_ARG, "null pointer");
+    return run_exprb_finish(d, u, u_out, dd, xi, ndd, alpha, shift, tol, h, scratch, workspace, workspace_bytes,
+                            result_host, (cudaStream_t)stream);
+}

@@ -85,6 +85,19 @@ int stencil_nslices(const es_stencil_desc *d);
 int launch_stencil_f32(const es_stencil_desc *d, const float *u, float *out, double alpha, double beta,
                        const float *coeff, const float *const *faces, const float *halo_lo, const float *halo_hi,
                        cudaStream_t stream);
+int run_expeuler_step(const es_stencil_desc *d, const double *u, double *u_out, const double *dd_exp, int ndd_exp,
+                      const double *dd_phi, int ndd_phi, const double *xi, double alpha, double shift, double tol,
+                      double h, int nonlin, const double *source, double *scratch, void *ws_exp, void *ws_phi,
+                      size_t ws_bytes, es_step_result *res, cudaStream_t s);
+int run_exprb_step(const es_stencil_desc *d, const double *u, double *u_out, const double *dd, const double *xi,
+                   int ndd, double alpha, double shift, double tol, double h, double a, double b, double lo, double hi,
+                   double *scratch, void *aux, void *ws, size_t ws_bytes, es_step_result *res, cudaStream_t s);
+int run_exprb_finish(const es_stencil_desc *d, const double *u, double *u_out, const double *dd, const double *xi,
+                     int ndd, double alpha, double shift, double tol, double h, const double *scratch, void *ws,
+                     size_t ws_bytes, es_step_result *res, cudaStream_t s);
+int launch_combustion(const double *u, double *out, int64_t n, unsigned long long *bad_dev, cudaStream_t st);
+int launch_axpy(const double *y, const double *z, double h, double *out, int64_t n, cudaStream_t st);
+int launch_scale(const double *x, double s, double *out, int64_t n, cudaStream_t st);
 int launch_combustion_f32(const float *u, float *out, int64_t n, cudaStream_t stream);
 int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double *v, double *p_out, const double *dd,
                    const double *xi, int ndd, double alpha, double shift, double tol, const double *gdiag, void *ws,

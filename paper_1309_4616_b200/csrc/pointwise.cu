@@ -98,6 +98,23 @@ __global__ void k_fill_u64(unsigned long long *p, unsigned long long a, unsigned
     if (threadIdx.x == 1) p[1] = b;
 }
 
+// host launchers for the fused steps (step.cu)
+int launch_combustion(const double *u, double *out, int64_t n, unsigned long long *bad_dev, cudaStream_t st) {
+    k_fill_u64<<<1, 32, 0, st>>>(bad_dev, (unsigned long long)n, 0ull);
+    if (n > 0) k_combustion<<<grid_for(n), 256, 0, st>>>(u, out, n, bad_dev);
+    return check_launch("combustion");
+}
+
+int launch_axpy(const double *y, const double *z, double h, double *out, int64_t n, cudaStream_t st) {
+    if (n > 0) k_axpy<<<grid_for(n), 256, 0, st>>>(y, z, h, out, n);
+    return check_launch("axpy");
+}
+
+int launch_scale(const double *x, double s, double *out, int64_t n, cudaStream_t st) {
+    if (n > 0) k_scale<<<grid_for(n), 256, 0, st>>>(x, s, out, n);
+    return check_launch("scale");
+}
+
 // ----- per-thread scratch (device word pair + pinned host pair) --------------
 
 struct Scratch {

@@ -23,7 +23,7 @@ from typing import Callable, Optional, Union
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, timing
 from .device import empty, is_host, like_input, ptr, stream_handle, to_device
 from .errors import ConvergenceError, DomainError
 from .grid import Field
@@ -187,6 +187,13 @@ class StepStats:
     halvings: int = 0
 
 
+def _plain_stencil(op) -> bool:
+    """A single-device stencil operator the fused step entries accept."""
+    from .stencil import StencilOperator
+
+    return type(op) is StencilOperator and op.bc.kind != "function"
+
+
 class _StepWorkspace:
     """Interpolants for one (A, h), reused across steps."""
 
@@ -195,6 +202,56 @@ class _StepWorkspace:
         iv = problem.interval
         self.exp_interp = make_interpolant(iv, "exp", -h, max_degree, tol)
         self.phi_interp = make_interpolant(iv, "phi1", -h, max_degree, tol)
+        ei, pi = self.exp_interp, self.phi_interp
+        # one C call per step (es_expeuler_step) where the operator, the
+        # nonlinearity and the interpolants allow it
+        self._fused = (_plain_stencil(problem.operator) and problem.nonlinearity in (None, combustion_g)
+                       and iv.axis == "real" and len(ei.dd) > 1 and len(ei.dd) == len(pi.dd)
+                       and not np.iscomplexobj(ei.dd) and not np.iscomplexobj(pi.dd)
+                       and np.array_equal(ei.xi, pi.xi))
+        self._ws_phi = None
+        self._scratch = None
+
+    def _fused_step(self, u: torch.Tensor):
+        """Both series concurrently, g_n and y + h z on the device, one host
+        sync.  None when a series ran out of nodes or u left the domain: the
+        step is then re-run through the reference's orchestration below, which
+        raises or rescues exactly as integrator.py:169-189 does."""
+        from .device import Workspace
+
+        pr, op, lib = self.problem, self.problem.operator, _lib.load()
+        n = u.numel()
+        if n != op.n:
+            return None
+        d, keep = op.desc()
+        nbytes = lib.es_leja_stencil_workspace_bytes(ctypes.byref(d))
+        if self._ws_phi is None:
+            self._ws_phi = Workspace()
+        if self._scratch is None or self._scratch.numel() < 2 * n:
+            self._scratch = empty(2 * n)
+        ws_exp, ws_phi = op._ws.get(nbytes), self._ws_phi.get(nbytes)
+        dde, xi = self.exp_interp.device_coeffs()
+        ddp, _ = self.phi_interp.device_coeffs()
+        iv = self.exp_interp.interval
+        gamma = iv.halfspan
+        nonlin = _lib.ES_NONLIN_COMBUSTION if pr.nonlinearity is combustion_g else _lib.ES_NONLIN_NONE
+        src = pr._b_dev if pr.boundary_source is not None else None
+        out = empty(n)
+        res = _lib.StepResult()
+        rc = lib.es_expeuler_step(ctypes.byref(d), ptr(u), ptr(out), ptr(dde), dde.numel(), ptr(ddp), ddp.numel(),
+                                  ptr(xi), 1.0 / gamma, iv.center / gamma, float(self.tol), float(self.h), nonlin,
+                                  ptr(src), ptr(self._scratch), ptr(ws_exp), ptr(ws_phi), nbytes,
+                                  ctypes.byref(res), stream_handle())
+        del keep
+        if rc in (_lib.ES_ERR_DOMAIN, _lib.ES_ERR_NOT_CONVERGED):
+            return None
+        _lib.check(rc, "es_expeuler_step")
+        mv_e, mv_p = int(res.exp_series.matvecs), int(res.phi1_series.matvecs)
+        tm = timing.active()
+        if tm:
+            tm.add_ms(res.series_ms, mv_e + mv_p)
+        st = StepStats(matvecs=mv_e + mv_p, matvecs_exp=mv_e, matvecs_phi1=mv_p, degree_exp=mv_e, degree_phi1=mv_p)
+        return out, st
 
     def _series(self, target, interp, v):
         a = self.problem.operator
@@ -206,6 +263,10 @@ class _StepWorkspace:
             return apply_matfunc(a, v, target, -self.h, self.problem.interval, self.tol, self.max_degree)
 
     def step(self, u: torch.Tensor, t: float):
+        if self._fused:
+            r = self._fused_step(u)
+            if r is not None:
+                return r
         st = StepStats()
         y, s1 = self._series("exp", self.exp_interp, u)
         st.matvecs_exp, st.degree_exp, st.halvings = s1.matvecs, s1.degree, s1.halvings
@@ -319,6 +380,9 @@ class RosenbrockStepper:
         self._interp: dict = {}
         self._fused = None  # None: try the fused prologue; False: not eligible
         self._aux = None
+        self._one_call = True  # es_exprb_step until it reports the grid ineligible
+        self._last = None  # snapped interval of the previous step
+        self._scratch = None
 
     def interpolant(self, lo: float, hi: float, h: float):
         key = (lo, hi, h)
@@ -378,9 +442,79 @@ class RosenbrockStepper:
         gmin, gmax = (float(v) for v in mm.cpu())
         return f, gp, gmin, gmax
 
+    def _one_call_step(self, u: torch.Tensor, h: float):
+        """es_exprb_step: prologue, interval check, series and u + h z in one
+        C call (one more, es_exprb_finish, when the snapped interval moved).
+        None when the fused path does not apply (odd nx, unaligned, ...)."""
+        from .device import Workspace
+
+        pr, op, lib = self.problem, self.problem.operator, _lib.load()
+        n = u.numel()
+        if n != op.n:
+            return None
+        d, keep = op.desc()
+        nbytes = lib.es_leja_stencil_workspace_bytes(ctypes.byref(d))
+        ws = op._ws.get(nbytes)
+        if self._scratch is None or self._scratch.numel() < 2 * n:
+            self._scratch = empty(2 * n)
+        if self._aux is None:
+            self._aux = torch.empty(4, dtype=torch.int64, device=u.device)
+        out = empty(n)
+        res = _lib.StepResult()
+        a, b = pr.interval.a, pr.interval.b
+
+        def coeffs(lo, hi):
+            it = self.interpolant(lo, hi, h)
+            dd, xi = it.device_coeffs()
+            iv = it.interval
+            return it, dd, xi, 1.0 / iv.halfspan, iv.center / iv.halfspan
+
+        lo, hi = self._last if self._last is not None else (math.nan, math.nan)
+        if self._last is not None:
+            it, dd, xi, alpha, shift = coeffs(lo, hi)
+        else:  # no interval yet: the call stops after the prologue with ES_ERR_RANGE
+            it, dd, xi, alpha, shift = None, self._aux, self._aux, 1.0, 0.0
+        args = (ptr(dd), ptr(xi), dd.numel() if it is not None else 2, alpha, shift, float(self.tol), float(h))
+        rc = lib.es_exprb_step(ctypes.byref(d), ptr(u), ptr(out), *args, a, b, lo, hi, ptr(self._scratch),
+                               ptr(self._aux), ptr(ws), nbytes, ctypes.byref(res), stream_handle())
+        if rc == _lib.ES_ERR_RANGE:
+            lo, hi = res.lo, res.hi
+            it, dd, xi, alpha, shift = coeffs(lo, hi)
+            if len(it.dd) == 1:  # degenerate interval: newton_apply's scaling path
+                return None
+            rc = lib.es_exprb_finish(ctypes.byref(d), ptr(u), ptr(out), ptr(dd), ptr(xi), dd.numel(), alpha, shift,
+                                     float(self.tol), float(h), ptr(self._scratch), ptr(ws), nbytes,
+                                     ctypes.byref(res), stream_handle())
+        del keep
+        if rc == _lib.ES_ERR_DOMAIN:
+            i = int(res.first_bad)
+            raise DomainError(f"combustion nonlinearity undefined at index {i} (u <= 0)", index=i)
+        self._last = (lo, hi)
+        if rc == _lib.ES_ERR_NOT_CONVERGED:  # the halving rescue on the kept F, g'
+            f, gp = self._scratch[:n], self._scratch[n:2 * n]
+            z, st = _rescued(RosenbrockOperator(op, gp), it, f, self.tol, h, SpectralInterval(lo, hi),
+                             self.max_degree)
+            return _axpy(u, z, h), RosenbrockStats(matvecs=st.matvecs, matvecs_phi1=st.matvecs, degree_phi1=st.degree,
+                                                   halvings=st.halvings, interval=(lo, hi))
+        _lib.check(rc, "es_exprb_step")
+        mv = int(res.phi1_series.matvecs)
+        tm = timing.active()
+        if tm:
+            tm.add_ms(res.series_ms, mv)
+        return out, RosenbrockStats(matvecs=mv, matvecs_phi1=mv, degree_phi1=mv, interval=(lo, hi))
+
     def step(self, u: torch.Tensor, t: float, h: float):
         pr = self.problem
         op = pr.operator
+        if (self._one_call and pr.nonlinearity is combustion_g and pr.boundary_source is None
+                and _plain_stencil(op) and pr.interval.axis == "real"):
+            try:
+                r = self._one_call_step(u, h)
+            except ValueError:  # ES_ERR_ARG: not eligible for the fused kernels
+                r = None
+            if r is not None:
+                return r
+            self._one_call = False
         f, gp, gmin, gmax = self._prologue(u, t)
         lo, hi = snap_interval(pr.interval.a - gmax, pr.interval.b - gmin, pr.interval)
         interp = self.interpolant(lo, hi, h)

@@ -12,6 +12,7 @@ _active = None
 class SeriesTimer:
     def __init__(self):
         self.records: list[tuple[torch.cuda.Event, torch.cuda.Event, int]] = []
+        self.device_ms: list[tuple[float, int]] = []  # series timed inside a fused step call
 
     def __enter__(self):
         global _active
@@ -25,11 +26,14 @@ class SeriesTimer:
     def add(self, start, end, matvecs: int) -> None:
         self.records.append((start, end, int(matvecs)))
 
+    def add_ms(self, ms: float, matvecs: int) -> None:
+        self.device_ms.append((float(ms), int(matvecs)))
+
     def totals(self):
         """(seconds spent in series, matvecs) over all recorded series."""
         torch.cuda.synchronize()
-        ms = sum(s.elapsed_time(e) for s, e, _ in self.records)
-        return ms * 1e-3, sum(m for _, _, m in self.records)
+        ms = sum(s.elapsed_time(e) for s, e, _ in self.records) + sum(t for t, _ in self.device_ms)
+        return ms * 1e-3, sum(m for _, _, m in self.records) + sum(m for _, m in self.device_ms)
 
 
 def active():

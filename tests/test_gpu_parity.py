@@ -250,6 +250,7 @@ def test_rosenbrock_fused_prologue_matches_generic_path():
     fused = es.RosenbrockStepper(prob, 1e-6)
     generic = es.RosenbrockStepper(prob, 1e-6)
     generic._fused = False
+    fused._one_call = generic._one_call = False  # the Python-orchestrated steps (es_exprb_step: test_gpu_steps.py)
     f1, g1, lo1, hi1 = fused._prologue(u0, 0.0)
     f2, g2, lo2, hi2 = generic._prologue(u0, 0.0)
     assert fused._fused is True
