@@ -427,6 +427,8 @@ class Stepper:
             series = 2 * m + 4  # + the round-0 halo kernel; no NCCL per node
         elif self.dist and ex == "nccl":
             series = 3 * m + 3  # node + slice reduce + decide per node (NCCL kernels not counted)
+        elif getattr(self.problem.operator, "two_node_passes", lambda: False)():
+            series = 2 * ((m + 1) // 2) + 3  # two nodes per pass: (node + reduce) per pass
         else:
             series = 2 * m + 3
         if self.cfg["method"] == "rosenbrock":
@@ -565,16 +567,34 @@ def run_b200(args, cfg):
                   "frac_of_900GBs_per_gpu": moved / t_max / 1e9 / world / peer_gbs,
                   "note": "ledger bytes (halo planes / gathered vector slices) over the device-timed region"}
 
-    # roofline of the dominant kernel: the fused node (series time / nodes)
+    # roofline of the dominant kernel: the fused node (series time / nodes),
+    # or the two-node pass (series time / passes) where the series uses it
     node_s = series_s / max(series_mv, 1)
-    achieved = bytes_node / node_s / 1e9
     peak, peak_src = measured_peak()
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": profiled_traffic(args.config),
-                "kernel": "k_csr_node (fused CSR Leja node)" if is_csr(cfg) else "k_node_tma (fused Leja node)",
-                "bytes_per_node": bytes_node,
-                "bytes_per_point": bytes_node / n_local, "node_us": node_s * 1e6, "peak_source": peak_src,
-                "series_share_of_step": series_s / elapsed if elapsed > 0 else None}
+    two = (not is_csr(cfg) and not use_dist
+           and getattr(step.problem.operator, "two_node_passes", lambda: False)())
+    if two:
+        passes = max(tm.passes(), 1)
+        launch_s = series_s / passes
+        bytes_launch = (cfg["bytes_per_node"] + 8) * n_local  # read w, p (+g'); write w'', p', p''
+        achieved = bytes_launch / launch_s / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": profiled_traffic(args.config + "_tb"),
+                    "kernel": "k_node_tb (two fused Leja nodes per HBM pass)", "bytes_per_launch": bytes_launch,
+                    "bytes_per_point": bytes_launch / n_local, "launch_us": launch_s * 1e6, "launches": passes,
+                    "node_us": node_s * 1e6,
+                    "one_node_equiv_GBs": bytes_node / node_s / 1e9,
+                    "note": "one-node algorithmic bytes (SURVEY 8(d)) per node time; above the HBM peak because "
+                            "two nodes share one pass",
+                    "peak_source": peak_src, "series_share_of_step": series_s / elapsed if elapsed > 0 else None}
+    else:
+        achieved = bytes_node / node_s / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": profiled_traffic(args.config),
+                    "kernel": "k_csr_node (fused CSR Leja node)" if is_csr(cfg) else "k_node_tma (fused Leja node)",
+                    "bytes_per_node": bytes_node,
+                    "bytes_per_point": bytes_node / n_local, "node_us": node_s * 1e6, "peak_source": peak_src,
+                    "series_share_of_step": series_s / elapsed if elapsed > 0 else None}
 
     # ---- end to end through the public API with host buffers ----
     e2e = None

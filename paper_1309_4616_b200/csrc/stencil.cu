@@ -694,21 +694,29 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     S.n = d->nx * d->ny * d->lz;
     char *w = static_cast<char *>(ws);
     S.pl = plan_stencil(d, {v, p_out, gdiag, halo_lo, halo_hi, (const void *)(w + 0)}, true);
-    const StencilPlan &pl = S.pl;
+    StencilPlan &pl = S.pl;
     if ((halo_lo || halo_hi || dist) && !(pl.tma && !pl.dim2))
         return set_error(ES_ERR_ARG, "slab series with halos need the 3D TMA path (even nx, aligned vectors)");
+    // two nodes per pass (stencil_tb.cuh) where the w_k window's ghosts are
+    // local (Dirichlet / Neumann, one domain): 24 instead of 40 B/point/node,
+    // ~690 vs ~890 us per 512^3 Rosenbrock node.
+    // Longer z chunks than the one-node kernel's: an item re-reads three w
+    // planes beyond its chunk (8 -> 32: 767 -> 685 us).  ES_TB=0 forces one
+    // node per pass.
+    S.tb = pl.tma && allow_tb && !pl.dim2 && !halo_lo && !halo_hi && !dist &&
+           (d->mode == ES_MODE_ZERO || d->mode == ES_MODE_NEUMANN) && env_int("ES_TB", 1);
+    if (S.tb) {
+        pl.chunk = std::max(1, env_int("ES_TBCHUNK", 32));
+        pl.grid.z = (unsigned)((d->lz + pl.chunk - 1) / pl.chunk);
+        pl.nchunks = pl.grid.z;
+        pl.items = (int64_t)pl.grid.x * pl.grid.y * pl.nchunks;
+        pl.nslices = pl.nchunks;
+    }
     const WsLayout L = layout(S.n, pl.nslices, pl.ntiles, pl.nchunks);
     if (ws_bytes < L.total) return set_error(ES_ERR_ARG, "workspace too small");
     ApplyFn af;
     S.lp = pl;
     if (pl.tma) {
-        // two nodes per pass (stencil_tb.cuh) where the w_k window's ghosts
-        // are local (Dirichlet / Neumann, one domain).  Opt-in (ES_TB=1): it
-        // moves 24 instead of 40 B/point/node but is issue-bound at ~2x the
-        // one-node kernel's instructions per point, 902 vs 872 us per 512^3
-        // Rosenbrock node
-        S.tb = allow_tb && !pl.dim2 && !halo_lo && !halo_hi && !dist &&
-               (d->mode == ES_MODE_ZERO || d->mode == ES_MODE_NEUMANN) && env_int("ES_TB", 0);
         if (S.tb) {
             S.nf = gdiag ? pick_node_tb<true>(d->coeff_kind) : pick_node_tb<false>(d->coeff_kind);
             finish_tma_plan(S.lp, (const void *)S.nf,
@@ -768,6 +776,7 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
             if (!rc) rc = encode_map(&maps.m[MAP_T_0], hp.wbuf[0], d, false, MK_W2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_1], hp.wbuf[1], d, false, MK_W2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_G], gdiag, d, false, MK_W);
+            if (!rc) rc = encode_map(&maps.m[MAP_T_PV], v, d, false, MK_P);
         }
         if (rc) return rc;
         TmaMaps *dmaps = reinterpret_cast<TmaMaps *>(w + L.maps);

@@ -18,10 +18,11 @@
 // Ring buffers (producer = warp 8, one lane):
 //   W: w_{k-1} tiles of planes mb-2 .. me+1 (72x12, from x0-4, y0-2);
 //   G: g' tiles of planes mb-1 .. me (68x10, from x0-2, y0-1; GD only);
-//   P: p_{k-1} tiles of planes mb .. me-1 (64x8; not on the first pass).
-// Consumer iteration j (planes mb-1 .. me): A) w_k of plane j on the
-// extended tile; B) p_k of plane j's interior; C) w_{k+1}, p_{k+1} of plane
-// j-1's interior.
+//   P: p_{k-1} tiles of planes mb .. me-1 (64x8; v on the first pass);
+//   V: w_k windows (68x10), written by warp group A, read by group C.
+// Group A (warps 0-3), plane j = mb-1 .. me: w_k of plane j on the window.
+// Group C (warps 4-7), plane j: p_k of plane j's interior, then w_{k+1},
+// p_{k+1} of plane j-1's interior.
 #pragma once
 
 #include "stencil_tma.cuh"
@@ -32,11 +33,24 @@ constexpr int TB_WX = 72, TB_WY = 12;  // w_{k-1}: x0-4 .. x0+67, y0-2 .. y0+9
 constexpr int TB_EX = 68, TB_EY = 10;  // w_k window: x0-2 .. x0+65 (even start: pair loads), y0-1 .. y0+8
 constexpr int TB_PAIRS = TB_EX / 2 * TB_EY;  // 340 point pairs per window plane
 constexpr int TB_GX = 68, TB_GY = 10;  // g': x0-2 .. x0+65, y0-1 .. y0+8
-constexpr int TB_SV = 4;               // w_k planes held (j-2 .. j+1)
+#ifndef TB_SV
+#define TB_SV 5  // w_k window planes in flight between the warp groups (>= 4: j-2 .. j+1)
+#endif
+#ifndef TB_SG
+#define TB_SG 5
+#endif
+#ifndef TB_SW_GD
+#define TB_SW_GD 6
+#endif
+#ifndef TB_SW_NG
+#define TB_SW_NG 9
+#endif
 
 template <bool GD>
 struct TbLayout {
-    static constexpr int SW = GD ? 6 : 7, SG = GD ? 4 : 0, SP = 4;
+    // ring depths: two CTAs per SM (<= 113 KiB each); G slots are held until
+    // group C is done with the plane, so the G ring is the deeper one
+    static constexpr int SW = GD ? TB_SW_GD : TB_SW_NG, SG = GD ? TB_SG : 0, SP = 4;
     static constexpr int W_STAGE = (TB_WX * TB_WY * 8 + 127) & ~127;
     static constexpr int G_STAGE = (TB_GX * TB_GY * 8 + 127) & ~127;
     static constexpr int P_STAGE = 64 * 8 * 8;
@@ -46,9 +60,10 @@ struct TbLayout {
     static constexpr int P_OFF = G_OFF + SG * G_STAGE;
     static constexpr int V_OFF = P_OFF + SP * P_STAGE;
     static constexpr int BAR_OFF = (V_OFF + TB_SV * V_SLOT + 7) & ~7;
-    static constexpr int NBAR = 2 * (SW + SG + SP);
+    static constexpr int NBAR = 2 * (SW + SG + SP + TB_SV);
     static constexpr int ITEMQ_OFF = BAR_OFF + NBAR * 8;
-    static constexpr int BYTES = ITEMQ_OFF + ((SW * 4 + 15) & ~15);
+    static constexpr int VITEM_OFF = ITEMQ_OFF + ((SW * 4 + 15) & ~15);
+    static constexpr int BYTES = VITEM_OFF + 16;
 };
 
 struct TbMaps {
@@ -141,197 +156,313 @@ ES_DEV double tb_point_scalar(const Geom &g, const double *Wm, const double *Wc,
     return add(mul(alpha, lap), mul(beta, c));
 }
 
-// Consumers (warps 0..7).  Returns the per-item norm partials through P->part
-// (node k at the first half, node k+1 at the second half of the array).
-template <int COEFF, bool GD>
-ES_DEV void tb_consume(const Geom &g, const SeriesParams *P, int k, bool two, const Items &its, char *smem,
-                       bool load_p) {
+// ---- consumers: two warp groups joined by the V ring -------------------------
+// A (warps 0-3) computes w_k on the window of plane j into V(j); C (warps 4-7)
+// forms p_k of plane j from V(j) and P(j), then w_{k+1}, p_{k+1} of plane j-1
+// from V(j-2..j).  The groups hand planes over through per-slot mbarriers, so
+// neither waits for the other at every plane (A runs up to two planes ahead).
+
+struct TbBars {
+    uint64_t *wfull, *wempty, *gfull, *gempty, *pfull, *pempty, *vfull, *vempty;
+};
+
+template <bool GD>
+ES_DEV TbBars tb_bars(char *smem) {
     using Lt = TbLayout<GD>;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + Lt::BAR_OFF);
-    uint64_t *wfull = bar, *wempty = wfull + Lt::SW, *gfull = wempty + Lt::SW, *gempty = gfull + Lt::SG,
-             *pfull = gempty + Lt::SG, *pempty = pfull + Lt::SP;
+    uint64_t *b = reinterpret_cast<uint64_t *>(smem + Lt::BAR_OFF);
+    TbBars r;
+    r.wfull = b;
+    r.wempty = r.wfull + Lt::SW;
+    r.gfull = r.wempty + Lt::SW;
+    r.gempty = r.gfull + Lt::SG;
+    r.pfull = r.gempty + Lt::SG;
+    r.pempty = r.pfull + Lt::SP;
+    r.vfull = r.pempty + Lt::SP;
+    r.vempty = r.vfull + TB_SV;
+    return r;
+}
+
+ES_DEV void warp_arrive(uint64_t *b) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(b);
+}
+
+ES_DEV void a_group_sync() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+
+// slot / phase of a ring position
+template <int S>
+struct Ring {
+    uint32_t slot = 0, phase = 0;
+    ES_DEV void next() {
+        if (++slot == (uint32_t)S) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+};
+
+// w_k at a window pair whose stencils need no ghost handling
+template <int COEFF, bool GD>
+ES_DEV double2 tb_fast_pair(const Geom &g, const double *Wm, const double *Wc, const double *Wp, const double *Gj,
+                            int ey, int ex, int64_t x, int64_t y, int j, double alpha, double beta) {
+    const int o = (ey + 1) * TB_WX + ex + 2;
+    const double2 c = *reinterpret_cast<const double2 *>(Wc + o);
+    const double2 ym = *reinterpret_cast<const double2 *>(Wc + o - TB_WX);
+    const double2 yp = *reinterpret_cast<const double2 *>(Wc + o + TB_WX);
+    const double2 zm = *reinterpret_cast<const double2 *>(Wm + o);
+    const double2 zp = *reinterpret_cast<const double2 *>(Wp + o);
+    double l0 = lap7(c.x, Wc[o - 1], c.y, ym.x, yp.x, zm.x, zp.x, g.wx, g.wy, g.wz);
+    double l1 = lap7(c.y, c.x, Wc[o + 2], ym.y, yp.y, zm.y, zp.y, g.wx, g.wy, g.wz);
+    if constexpr (COEFF != ES_COEFF_NONE) {
+        l0 = mul(tb_coeff<COEFF>(g, x, y, j), l0);
+        l1 = mul(tb_coeff<COEFF>(g, x + 1, y, j), l1);
+    }
+    if constexpr (GD) {
+        const double2 gv = *reinterpret_cast<const double2 *>(Gj + ey * TB_GX + ex);
+        l0 = sub(l0, mul(gv.x, c.x));
+        l1 = sub(l1, mul(gv.y, c.y));
+    }
+    return make_double2(add(mul(alpha, l0), mul(beta, c.x)), add(mul(alpha, l1), mul(beta, c.y)));
+}
+
+template <int COEFF, bool GD>
+ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const Items &its, char *smem) {
+    using Lt = TbLayout<GD>;
+    const TbBars B = tb_bars<GD>(smem);
     const volatile int *itemq = reinterpret_cast<const volatile int *>(smem + Lt::ITEMQ_OFF);
+    volatile int *vitem = reinterpret_cast<volatile int *>(smem + Lt::VITEM_OFF);
     double *vwin = reinterpret_cast<double *>(smem + Lt::V_OFF);
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int q = t % 32, r = t / 32;  // interior pair (x0 + 2q, + 1) of row y0 + r
-    const int64_t plane = g.nx * g.ny;
+    const int a = threadIdx.x;  // 0..127
     const bool neu = g.mode == ES_MODE_NEUMANN;
-    const int pass = (k - 1) / 2;
-    double *w1_dst = P->wbuf[pass & 1];  // w_{k+1} (w_{k-1} comes through the W tiles)
-    double *pk_dst = P->pbuf[k & 1], *pk1_dst = P->pbuf[(k + 1) & 1];
-    const double alpha = P->alpha, d0 = P->dd[0], dk = P->dd[k], beta_k = sub(-P->shift, P->xi[k - 1]);
-    const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
-    uint32_t uw = 0, ug = 0, up = 0;
-    auto wst = [&](uint32_t u) { return reinterpret_cast<const double *>(smem + Lt::W_OFF + (u % Lt::SW) * Lt::W_STAGE); };
-    auto wwait = [&](uint32_t u) { mbar_wait(&wfull[u % Lt::SW], (u / Lt::SW) & 1); };
-    auto release = [&](uint64_t *b) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(b);
-    };
-    auto vslot = [&](int j) { return vwin + ((j % TB_SV + TB_SV) % TB_SV) * (TB_EX * TB_EY); };
-    // this thread's window pairs (fixed for every plane and item)
-    int pey[2], pex[2];
+    const double alpha = P->alpha, beta_k = sub(-P->shift, P->xi[k - 1]);
+    int pey[3], pex[3];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int pr = t + h * 32 * TMA_CONSUMER_WARPS;
+    for (int h = 0; h < 3; ++h) {
+        const int pr = a + 128 * h;
         pey[h] = pr < TB_PAIRS ? pr / (TB_EX / 2) : -1;
         pex[h] = 2 * (pr % (TB_EX / 2));
     }
-
+    Ring<Lt::SW> wr;  // W ring position of the next plane to wait for
+    Ring<Lt::SG> gr;
+    Ring<TB_SV> vr;
+    uint32_t vuses = 0;  // V slots handed out so far
+    auto wst = [&](uint32_t s) { return reinterpret_cast<const double *>(smem + Lt::W_OFF + s * Lt::W_STAGE); };
+    auto vslot = [&](uint32_t s) { return vwin + s * (TB_EX * TB_EY); };
+    auto take_v = [&]() {  // wait until C released the slot's previous plane
+        if (vuses >= (uint32_t)TB_SV) mbar_wait(&B.vempty[vr.slot], vr.phase ^ 1u);
+        ++vuses;
+    };
     for (;;) {
-        wwait(uw);
-        const int i = itemq[uw % Lt::SW];
-        if (i < 0) break;
+        mbar_wait(&B.wfull[wr.slot], wr.phase);
+        const int i = itemq[wr.slot];
+        if (i < 0) {  // end of work: tell C through the next V slot
+            take_v();
+            if (a == 0) vitem[vr.slot] = -1;
+            warp_arrive(&B.vfull[vr.slot]);
+            break;
+        }
         const Item it = item_at<true>(its, i);
-        const uint32_t u0 = uw;  // W index of plane mb-2
-        wwait(u0 + 1);
-        const int64_t xa = it.x0 + 2 * q, ya = it.y0 + r;  // this thread's interior pair
-        const bool act = xa < g.nx && ya < g.ny;
-        bool fast[2];  // this thread's window pairs that need no ghost handling
+        bool fast[3];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 3; ++h) {
             const int64_t x = it.x0 - 2 + pex[h], y = it.y0 - 1 + pey[h];
             const int64_t lo = neu ? 1 : 0, xhi = neu ? g.nx - 2 : g.nx - 1, yhi = neu ? g.ny - 2 : g.ny - 1;
             fast[h] = x >= lo && x + 1 <= xhi && y >= lo && y <= yhi;
         }
-        double acc_w0 = 0.0, acc_p0 = 0.0, acc_w1 = 0.0, acc_p1 = 0.0;
-        double pk_prev[2] = {0.0, 0.0};
+        // W slots of planes j-1, j, j+1 (plane mb-2 is at wr)
+        Ring<Lt::SW> rm = wr, rc = wr;
+        rc.next();
+        Ring<Lt::SW> rp = rc;
+        rp.next();
+        mbar_wait(&B.wfull[rc.slot], rc.phase);
+        uint32_t v_prev = 0;  // slot of V(j-1)
         for (int j = it.mb - 1; j <= it.me; ++j) {
-            const uint32_t uj = u0 + (uint32_t)(j - (it.mb - 2));  // W index of plane j
-            wwait(uj + 1);
-            const double *Wm = wst(uj - 1), *Wc = wst(uj), *Wp = wst(uj + 1);
+            mbar_wait(&B.wfull[rp.slot], rp.phase);
+            const double *Wm = wst(rm.slot), *Wc = wst(rc.slot), *Wp = wst(rp.slot);
             const double *Gj = nullptr;
             if constexpr (GD) {
-                mbar_wait(&gfull[ug % Lt::SG], (ug / Lt::SG) & 1);  // G(j)
-                Gj = reinterpret_cast<const double *>(smem + Lt::G_OFF + (ug % Lt::SG) * Lt::G_STAGE);
+                mbar_wait(&B.gfull[gr.slot], gr.phase);
+                Gj = reinterpret_cast<const double *>(smem + Lt::G_OFF + gr.slot * Lt::G_STAGE);
             }
-            // ---- A: w_k of plane j on the extended tile
-            double *Vj = vslot(j);
+            take_v();
+            double *Vj = vslot(vr.slot);
+            if (j == it.mb - 1 && a == 0) vitem[vr.slot] = i;
             const bool zin = j >= 0 && j < its.L;
+            bool arrive_prev = false;
             if (zin) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < 3; ++h) {
                     const int ey = pey[h], ex = pex[h];
                     if (ey < 0) break;
                     const int64_t x = it.x0 - 2 + ex, y = it.y0 - 1 + ey;
-                    double2 wk;
-                    if (fast[h]) {  // both points inside, no ghost to patch: pair loads
-                        const int o = (ey + 1) * TB_WX + ex + 2;
-                        const double2 c = *reinterpret_cast<const double2 *>(Wc + o);
-                        const double2 ym = *reinterpret_cast<const double2 *>(Wc + o - TB_WX);
-                        const double2 yp = *reinterpret_cast<const double2 *>(Wc + o + TB_WX);
-                        const double2 zm = *reinterpret_cast<const double2 *>(Wm + o);
-                        const double2 zp = *reinterpret_cast<const double2 *>(Wp + o);
-                        double l0 = lap7(c.x, Wc[o - 1], c.y, ym.x, yp.x, zm.x, zp.x, g.wx, g.wy, g.wz);
-                        double l1 = lap7(c.y, c.x, Wc[o + 2], ym.y, yp.y, zm.y, zp.y, g.wx, g.wy, g.wz);
-                        if constexpr (COEFF != ES_COEFF_NONE) {
-                            l0 = mul(tb_coeff<COEFF>(g, x, y, j), l0);
-                            l1 = mul(tb_coeff<COEFF>(g, x + 1, y, j), l1);
-                        }
-                        if constexpr (GD) {
-                            const double2 gv = *reinterpret_cast<const double2 *>(Gj + ey * TB_GX + ex);
-                            l0 = sub(l0, mul(gv.x, c.x));
-                            l1 = sub(l1, mul(gv.y, c.y));
-                        }
-                        wk = make_double2(add(mul(alpha, l0), mul(beta_k, c.x)), add(mul(alpha, l1), mul(beta_k, c.y)));
-                    } else {
-                        wk = make_double2(
-                            tb_point_scalar<COEFF, GD>(g, Wm, Wc, Wp, Gj, it.x0, it.y0, x, y, j, alpha, beta_k),
-                            tb_point_scalar<COEFF, GD>(g, Wm, Wc, Wp, Gj, it.x0, it.y0, x + 1, y, j, alpha, beta_k));
-                    }
+                    const double2 wk =
+                        fast[h] ? tb_fast_pair<COEFF, GD>(g, Wm, Wc, Wp, Gj, ey, ex, x, y, j, alpha, beta_k)
+                                : make_double2(
+                                      tb_point_scalar<COEFF, GD>(g, Wm, Wc, Wp, Gj, it.x0, it.y0, x, y, j, alpha, beta_k),
+                                      tb_point_scalar<COEFF, GD>(g, Wm, Wc, Wp, Gj, it.x0, it.y0, x + 1, y, j, alpha,
+                                                                 beta_k));
                     *reinterpret_cast<double2 *>(Vj + ey * TB_EX + ex) = wk;
                 }
+                if (neu && j == 0) {  // the mirrored plane below the domain = w_k of plane 0
+                    a_group_sync();
+                    double *Vb = vslot(v_prev);
+                    for (int e = a; e < TB_EX * TB_EY; e += 128) Vb[e] = Vj[e];
+                    arrive_prev = true;
+                }
+            } else if (j >= 0) {  // plane L: zeros (Dirichlet) or the mirrored plane L-1 (Neumann)
+                if (neu) a_group_sync();
+                const double *Vs = vslot(v_prev);
+                for (int e = a; e < TB_EX * TB_EY; e += 128) Vj[e] = neu ? Vs[e] : 0.0;
+            } else if (!neu) {  // plane -1, Dirichlet
+                for (int e = a; e < TB_EX * TB_EY; e += 128) Vj[e] = 0.0;
             }
-            // out-of-domain planes of the w_k window: zeros (Dirichlet), or the
-            // mirrored boundary plane (Neumann; the bottom one right after plane 0)
-            if (!zin && !(neu && j < 0)) {
-                const double *Vs = vslot(its.L - 1);
-                for (int e = t; e < TB_EX * TB_EY; e += 32 * TMA_CONSUMER_WARPS) Vj[e] = neu ? Vs[e] : 0.0;
+            warp_arrive(&B.wempty[rm.slot]);  // W(j-1): last read by A of plane j
+            if constexpr (GD) {
+                warp_arrive(&B.gempty[gr.slot]);
+                gr.next();
             }
-            group_sync<32 * TMA_CONSUMER_WARPS>();
-            if (neu && j == 0) {
-                double *Vb = vslot(-1);
-                for (int e = t; e < TB_EX * TB_EY; e += 32 * TMA_CONSUMER_WARPS) Vb[e] = Vj[e];
-                group_sync<32 * TMA_CONSUMER_WARPS>();
-            }
-            release(&wempty[(uj - 1) % Lt::SW]);  // W(j-1): its last use was A of plane j
-            // ---- B: p_k of plane j's interior (+ node k norms)
-            double pk_cur[2] = {0.0, 0.0};
+            if (arrive_prev) warp_arrive(&B.vfull[v_prev]);
+            if (!(neu && j < 0)) warp_arrive(&B.vfull[vr.slot]);  // Neumann plane -1 arrives with plane 0
+            v_prev = vr.slot;
+            vr.next();
+            rm = rc;
+            rc = rp;
+            rp.next();
+        }
+        warp_arrive(&B.wempty[rm.slot]);  // W(me), W(me+1)
+        warp_arrive(&B.wempty[rc.slot]);
+        wr = rp;
+    }
+}
+
+template <int COEFF, bool GD>
+ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, const Items &its, char *smem) {
+    using Lt = TbLayout<GD>;
+    const TbBars B = tb_bars<GD>(smem);
+    const volatile int *vitem = reinterpret_cast<const volatile int *>(smem + Lt::VITEM_OFF);
+    const double *vwin = reinterpret_cast<const double *>(smem + Lt::V_OFF);
+    const int c = threadIdx.x - 128, cw = c >> 5, q = c & 31;  // rows cw and cw + 4, pair x0 + 2q
+    const int64_t plane = g.nx * g.ny;
+    const int pass = (k - 1) / 2;
+    double *w1_dst = P->wbuf[pass & 1];
+    double *pk_dst = P->pbuf[k & 1], *pk1_dst = P->pbuf[(k + 1) & 1];
+    const double alpha = P->alpha, dk = P->dd[k];
+    const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
+    const double pscale = k == 1 ? P->dd[0] : 1.0;  // first pass: P tiles hold v, p_0 = dd_0 v
+    Ring<Lt::SG> gr;
+    Ring<Lt::SP> pr;
+    Ring<TB_SV> vr;
+    auto vslot = [&](uint32_t s) { return vwin + s * (TB_EX * TB_EY); };
+    for (;;) {
+        mbar_wait(&B.vfull[vr.slot], vr.phase);
+        const int i = vitem[vr.slot];
+        if (i < 0) break;
+        const Item it = item_at<true>(its, i);
+        const int64_t xa = it.x0 + 2 * q;
+        bool act[2];
+        int64_t ya[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            ya[h] = it.y0 + cw + 4 * h;
+            act[h] = xa < g.nx && ya[h] < g.ny;
+        }
+        double acc_w0[2] = {0.0, 0.0}, acc_p0[2] = {0.0, 0.0}, acc_w1[2] = {0.0, 0.0}, acc_p1[2] = {0.0, 0.0};
+        double pk_prev[4] = {0.0, 0.0, 0.0, 0.0};
+        uint32_t s2 = 0, s1 = 0;  // V slots of planes j-2, j-1
+        for (int j = it.mb - 1; j <= it.me; ++j) {
+            if (j > it.mb - 1) mbar_wait(&B.vfull[vr.slot], vr.phase);
+            const uint32_t s0 = vr.slot;
+            const double *Vj = vslot(s0);
+            // ---- B: p_k of plane j (+ node k norms)
+            double pk_cur[4] = {0.0, 0.0, 0.0, 0.0};
             if (j >= it.mb && j < it.me) {
-                const double *Pc = nullptr;
-                if (load_p) {
-                    mbar_wait(&pfull[up % Lt::SP], (up / Lt::SP) & 1);
-                    Pc = reinterpret_cast<const double *>(smem + Lt::P_OFF + (up % Lt::SP) * Lt::P_STAGE);
-                }
-                if (act) {
-                    const double *vrow = Vj + (r + 1) * TB_EX + 2 * q + 2;
-                    const double *wrow = Wc + (r + 2) * TB_WX + 2 * q + 4;
+                mbar_wait(&B.pfull[pr.slot], pr.phase);
+                const double *Pc = reinterpret_cast<const double *>(smem + Lt::P_OFF + pr.slot * Lt::P_STAGE);
 #pragma unroll
-                    for (int jj = 0; jj < 2; ++jj) {
-                        const double wk = vrow[jj];
-                        const double pold = load_p ? Pc[r * 64 + 2 * q + jj] : mul(d0, wrow[jj]);
-                        pk_cur[jj] = add(pold, mul(dk, wk));
-                    }
-                    *reinterpret_cast<double2 *>(pk_dst + j * plane + ya * g.nx + xa) = make_double2(pk_cur[0], pk_cur[1]);
-                    acc_w0 = add(acc_w0, add(mul(vrow[0], vrow[0]), mul(vrow[1], vrow[1])));
-                    acc_p0 = add(acc_p0, add(mul(pk_cur[0], pk_cur[0]), mul(pk_cur[1], pk_cur[1])));
+                for (int h = 0; h < 2; ++h) {
+                    if (!act[h]) continue;
+                    const int r = cw + 4 * h;
+                    const double2 vk = *reinterpret_cast<const double2 *>(Vj + (r + 1) * TB_EX + 2 * q + 2);
+                    const double2 po = *reinterpret_cast<const double2 *>(Pc + r * 64 + 2 * q);
+                    const double p0 = k == 1 ? mul(pscale, po.x) : po.x, p1 = k == 1 ? mul(pscale, po.y) : po.y;
+                    pk_cur[2 * h] = add(p0, mul(dk, vk.x));
+                    pk_cur[2 * h + 1] = add(p1, mul(dk, vk.y));
+                    *reinterpret_cast<double2 *>(pk_dst + j * plane + ya[h] * g.nx + xa) =
+                        make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
+                    acc_w0[h] = add(acc_w0[h], add(mul(vk.x, vk.x), mul(vk.y, vk.y)));
+                    acc_p0[h] = add(acc_p0[h], add(mul(pk_cur[2 * h], pk_cur[2 * h]),
+                                                   mul(pk_cur[2 * h + 1], pk_cur[2 * h + 1])));
                 }
-                if (load_p) {
-                    release(&pempty[up % Lt::SP]);
-                    ++up;
-                }
+                warp_arrive(&B.pempty[pr.slot]);
+                pr.next();
             }
-            // ---- C: w_{k+1}, p_{k+1} of plane j-1's interior (+ node k+1 norms)
+            // ---- C: w_{k+1}, p_{k+1} of plane j-1 (+ node k+1 norms)
             const int jc = j - 1;
-            if (two && jc >= it.mb && jc < it.me && act) {
-                const double *Vm = vslot(jc - 1), *Vc = vslot(jc), *Vp = vslot(jc + 1);
-                const int o = (r + 1) * TB_EX + 2 * q + 2;
-                double wn[2], pn[2];
-#pragma unroll
-                for (int jj = 0; jj < 2; ++jj) {
-                    const double c = Vc[o + jj];
-                    double lap = lap7(c, Vc[o + jj - 1], Vc[o + jj + 1], Vc[o + jj - TB_EX], Vc[o + jj + TB_EX],
-                                      Vm[o + jj], Vp[o + jj], g.wx, g.wy, g.wz);
-                    if constexpr (COEFF != ES_COEFF_NONE) lap = mul(tb_coeff<COEFF>(g, xa + jj, ya, jc), lap);
+            if (jc >= it.mb && jc < it.me) {
+                if (two) {
+                    const double *Vm = vslot(s2), *Vc = vslot(s1), *Vp = Vj;
+                    const double *Gc = nullptr;
                     if constexpr (GD) {
-                        const double *Gc = reinterpret_cast<const double *>(
-                            smem + Lt::G_OFF + ((ug - 1) % Lt::SG) * Lt::G_STAGE);  // G(j-1)
-                        lap = sub(lap, mul(Gc[(r + 1) * TB_GX + 2 * q + jj + 2], c));
+                        mbar_wait(&B.gfull[gr.slot], gr.phase);  // complete already; orders the TMA bytes for C
+                        Gc = reinterpret_cast<const double *>(smem + Lt::G_OFF + gr.slot * Lt::G_STAGE);
                     }
-                    wn[jj] = add(mul(alpha, lap), mul(beta_k1, c));
-                    pn[jj] = add(pk_prev[jj], mul(dk1, wn[jj]));
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (!act[h]) continue;
+                        const int r = cw + 4 * h;
+                        const int o = (r + 1) * TB_EX + 2 * q + 2;
+                        double wn[2], pn[2];
+#pragma unroll
+                        for (int jj = 0; jj < 2; ++jj) {
+                            const double cc = Vc[o + jj];
+                            double lap = lap7(cc, Vc[o + jj - 1], Vc[o + jj + 1], Vc[o + jj - TB_EX], Vc[o + jj + TB_EX],
+                                              Vm[o + jj], Vp[o + jj], g.wx, g.wy, g.wz);
+                            if constexpr (COEFF != ES_COEFF_NONE) lap = mul(tb_coeff<COEFF>(g, xa + jj, ya[h], jc), lap);
+                            if constexpr (GD) lap = sub(lap, mul(Gc[(r + 1) * TB_GX + 2 * q + jj + 2], cc));
+                            wn[jj] = add(mul(alpha, lap), mul(beta_k1, cc));
+                            pn[jj] = add(pk_prev[2 * h + jj], mul(dk1, wn[jj]));
+                        }
+                        const int64_t off = jc * plane + ya[h] * g.nx + xa;
+                        *reinterpret_cast<double2 *>(w1_dst + off) = make_double2(wn[0], wn[1]);
+                        *reinterpret_cast<double2 *>(pk1_dst + off) = make_double2(pn[0], pn[1]);
+                        acc_w1[h] = add(acc_w1[h], add(mul(wn[0], wn[0]), mul(wn[1], wn[1])));
+                        acc_p1[h] = add(acc_p1[h], add(mul(pn[0], pn[0]), mul(pn[1], pn[1])));
+                    }
                 }
-                const int64_t off = jc * plane + ya * g.nx + xa;
-                *reinterpret_cast<double2 *>(w1_dst + off) = make_double2(wn[0], wn[1]);
-                *reinterpret_cast<double2 *>(pk1_dst + off) = make_double2(pn[0], pn[1]);
-                acc_w1 = add(acc_w1, add(mul(wn[0], wn[0]), mul(wn[1], wn[1])));
-                acc_p1 = add(acc_p1, add(mul(pn[0], pn[0]), mul(pn[1], pn[1])));
             }
             if constexpr (GD) {
-                if (jc >= it.mb - 1) release(&gempty[(ug - 1) % Lt::SG]);  // G(j-1)
-                ++ug;
+                if (jc >= it.mb - 1) {  // G(j-1): C's share of the release
+                    warp_arrive(&B.gempty[gr.slot]);
+                    gr.next();
+                }
             }
-            pk_prev[0] = pk_cur[0];
-            pk_prev[1] = pk_cur[1];
+            if (j - 2 >= it.mb - 1) warp_arrive(&B.vempty[s2]);  // V(j-2)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pk_prev[e] = pk_cur[e];
+            s2 = s1;
+            s1 = s0;
+            vr.next();
         }
-        const uint32_t L4 = (uint32_t)(it.me - it.mb + 4);
-        release(&wempty[(u0 + L4 - 2) % Lt::SW]);  // W(me), W(me+1)
-        release(&wempty[(u0 + L4 - 1) % Lt::SW]);
-        uw = u0 + L4;
-        if constexpr (GD) release(&gempty[(ug - 1) % Lt::SG]);  // G(me)
-        // (chunk, tile, warp) partials of both nodes, one-node kernel layout
-        acc_w0 = warp_sum(acc_w0);
-        acc_p0 = warp_sum(acc_p0);
-        acc_w1 = warp_sum(acc_w1);
-        acc_p1 = warp_sum(acc_p1);
-        if (lane == 0) {
-            const int64_t e = ((int64_t)it.chunk * its.ntiles + it.tile) * TMA_CONSUMER_WARPS + warp;
-            double *d0p = P->part + e * 2;
-            d0p[0] = acc_w0;
-            d0p[1] = acc_p0;
-            double *d1p = P->part + ((int64_t)P->nslices * P->ntiles + e) * 2;
-            d1p[0] = acc_w1;
-            d1p[1] = acc_p1;
+        warp_arrive(&B.vempty[s2]);  // V(me-1), V(me)
+        warp_arrive(&B.vempty[s1]);
+        if constexpr (GD) {  // G(me)
+            warp_arrive(&B.gempty[gr.slot]);
+            gr.next();
+        }
+        // (chunk, tile, row-warp) partials of both nodes, one-node kernel layout
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double w0 = warp_sum(acc_w0[h]), p0 = warp_sum(acc_p0[h]);
+            const double w1 = warp_sum(acc_w1[h]), p1 = warp_sum(acc_p1[h]);
+            if (q == 0) {
+                const int64_t e = ((int64_t)it.chunk * its.ntiles + it.tile) * TMA_CONSUMER_WARPS + cw + 4 * h;
+                double *d0p = P->part + e * 2;
+                d0p[0] = w0;
+                d0p[1] = p0;
+                double *d1p = P->part + ((int64_t)P->nslices * P->ntiles + e) * 2;
+                d1p[0] = w1;
+                d1p[1] = p1;
+            }
         }
     }
 }
@@ -343,34 +474,42 @@ ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
     const Items its = items_of<true>(g, P->chunk_len);
     const TmaMaps &M = *static_cast<const TmaMaps *>(P->maps);
     const int pass = (k - 1) / 2;
-    const TbMaps mp{&M.m[pass == 0 ? MAP_T_V : (pass & 1) ? MAP_T_0 : MAP_T_1], &M.m[MAP_T_G], &M.m[MAP_P_0]};
-    const bool load_p = k > 1;
+    // W: w_{k-1} (v on the first pass); P: p_{k-1}, or v on the first pass (p_0 = dd_0 v)
+    const TbMaps mp{&M.m[pass == 0 ? MAP_T_V : (pass & 1) ? MAP_T_0 : MAP_T_1], &M.m[MAP_T_G],
+                    &M.m[pass == 0 ? MAP_T_PV : MAP_P_0]};
     if (threadIdx.x == 0) {
-        uint64_t *bars = reinterpret_cast<uint64_t *>(smem + Lt::BAR_OFF);
+        const TbBars B = tb_bars<GD>(smem);
         for (int s = 0; s < Lt::SW; ++s) {
-            mbar_init(&bars[s], 1);
-            mbar_init(&bars[Lt::SW + s], TMA_CONSUMER_WARPS);
+            mbar_init(&B.wfull[s], 1);
+            mbar_init(&B.wempty[s], 4);  // A group
         }
         for (int s = 0; s < Lt::SG; ++s) {
-            mbar_init(&bars[2 * Lt::SW + s], 1);
-            mbar_init(&bars[2 * Lt::SW + Lt::SG + s], TMA_CONSUMER_WARPS);
+            mbar_init(&B.gfull[s], 1);
+            mbar_init(&B.gempty[s], 8);  // A and C groups
         }
         for (int s = 0; s < Lt::SP; ++s) {
-            mbar_init(&bars[2 * (Lt::SW + Lt::SG) + s], 1);
-            mbar_init(&bars[2 * (Lt::SW + Lt::SG) + Lt::SP + s], TMA_CONSUMER_WARPS);
+            mbar_init(&B.pfull[s], 1);
+            mbar_init(&B.pempty[s], 4);  // C group
+        }
+        for (int s = 0; s < TB_SV; ++s) {
+            mbar_init(&B.vfull[s], 4);
+            mbar_init(&B.vempty[s], 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x / 32 == TMA_CONSUMER_WARPS) {
+    const int warp = threadIdx.x / 32;
+    if (warp == TMA_CONSUMER_WARPS) {
         if ((threadIdx.x & 31) == 0) {
             tma_acquire(mp.w);
             if (GD) tma_acquire(mp.g);
-            if (load_p) tma_acquire(mp.p);
-            tb_produce<GD>(g, its, mp, smem, load_p, P->work);
+            tma_acquire(mp.p);
+            tb_produce<GD>(g, its, mp, smem, true, P->work);
         }
+    } else if (warp < 4) {
+        tb_group_a<COEFF, GD>(g, P, k, its, smem);
     } else {
-        tb_consume<COEFF, GD>(g, P, k, two, its, smem, load_p);
+        tb_group_c<COEFF, GD>(g, P, k, two, its, smem);
     }
 }
 

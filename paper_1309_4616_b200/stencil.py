@@ -228,6 +228,16 @@ class StencilOperator:
         del keep
         return res
 
+    def two_node_passes(self) -> bool:
+        """Whether series on this operator run two Leja nodes per HBM pass
+        (csrc/stencil_tb.cuh; the C side decides, this mirrors its rule for
+        the bench's launch counts and roofline)."""
+        import os
+
+        g = self.grid
+        return (os.environ.get("ES_TB", "1") != "0" and g.nz > 1 and g.nx % 2 == 0
+                and self.bc.kind in ("homogeneous", "neumann") and os.environ.get("ES_KERNEL", "") != "v1")
+
     def __repr__(self):
         g = self.grid
         return (f"StencilOperator({g.nx}x{g.ny}x{g.nz}, bc={self.bc.label()!r}, "

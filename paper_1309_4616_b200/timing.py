@@ -29,6 +29,11 @@ class SeriesTimer:
     def add_ms(self, ms: float, matvecs: int) -> None:
         self.device_ms.append((float(ms), int(matvecs)))
 
+    def passes(self) -> int:
+        """HBM passes of the recorded series when each pass fuses two nodes."""
+        ms = [m for _, _, m in self.records] + [m for _, m in self.device_ms]
+        return sum((m + 1) // 2 for m in ms)
+
     def totals(self):
         """(seconds spent in series, matvecs) over all recorded series."""
         torch.cuda.synchronize()
