@@ -423,11 +423,13 @@ class Stepper:
         A TMA series = publish maps + init + (node + slice reduce) per node + finalize."""
         m = stats.matvecs
         ex = getattr(self.problem.operator, "exchange", "none")
+        two = getattr(self.problem.operator, "two_node_passes", lambda: False)()
         if self.dist and ex == "p2p":
-            series = 2 * m + 4  # + the round-0 halo kernel; no NCCL per node
+            # + the round-0 halo kernel; no NCCL per node; (node + slice) per pass
+            series = (2 * ((m + 1) // 2) if two else 2 * m) + 4
         elif self.dist and ex == "nccl":
             series = 3 * m + 3  # node + slice reduce + decide per node (NCCL kernels not counted)
-        elif getattr(self.problem.operator, "two_node_passes", lambda: False)():
+        elif two:
             series = 2 * ((m + 1) // 2) + 3  # two nodes per pass: (node + reduce) per pass
         else:
             series = 2 * m + 3
@@ -571,8 +573,7 @@ def run_b200(args, cfg):
     # or the two-node pass (series time / passes) where the series uses it
     node_s = series_s / max(series_mv, 1)
     peak, peak_src = measured_peak()
-    two = (not is_csr(cfg) and not use_dist
-           and getattr(step.problem.operator, "two_node_passes", lambda: False)())
+    two = not is_csr(cfg) and getattr(step.problem.operator, "two_node_passes", lambda: False)()
     if two:
         passes = max(tm.passes(), 1)
         launch_s = series_s / passes

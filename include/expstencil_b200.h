@@ -205,7 +205,19 @@ int es_leja_dist_end(const void *workspace, void *stream);
  * and never reset (pass base = nranks x rounds completed so far, where a
  * series of K nodes completes K + 1 rounds).  A peer that does not arrive
  * within timeout_ns ends the series with ES_ERR_CUDA at es_leja_fetch.
- * Completion / result: es_leja_fetch. */
+ * Completion / result: es_leja_fetch.
+ *
+ * halo_planes = 2 selects two Leja nodes per pass (the single-GPU default,
+ * stencil_tb.cuh) where the operator allows it (Dirichlet / Neumann, no
+ * sampled coefficient array, lz >= 2): halo buffers then hold TWO planes
+ * each (halo_lo: planes -2, -1; halo_hi: lz, lz + 1), one round per pass
+ * (pass p reads halo parity p & 1, round 0 fills parity 0; a series of K
+ * nodes completes ceil(K / 2) + 1 rounds), slice tables hold
+ * 2 x 2 x total_slices x 2 doubles, and with a g' diagonal gdiag_lo /
+ * gdiag_hi are the neighbours' boundary planes of g' (filled by the caller
+ * before the call; NULL without a neighbour).  halo_planes = 2 on an
+ * operator that does not allow it (or with ES_TB=0) is ES_ERR_ARG: ranks must
+ * agree on the round count.  0 or 1: one node per pass, one-plane halos. */
 typedef struct es_p2p_desc {
     int32_t nranks, rank;
     int64_t slice_offset, total_slices;
@@ -216,6 +228,8 @@ typedef struct es_p2p_desc {
     unsigned long long *arrive_local; /* this rank's counter */
     unsigned long long base;
     int64_t timeout_ns;               /* <= 0: 10 s */
+    int32_t halo_planes;              /* 0 / 1: one node per pass; 2: two (see above) */
+    const double *gdiag_lo, *gdiag_hi; /* neighbours' g' boundary planes (halo_planes = 2) */
 } es_p2p_desc;
 
 int es_leja_stencil_nslices(const es_stencil_desc *d, int32_t *nslices_out);

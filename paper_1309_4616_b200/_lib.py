@@ -55,6 +55,7 @@ class P2PDesc(ctypes.Structure):
         ("peer_lo", ctypes.c_void_p * 2), ("peer_hi", ctypes.c_void_p * 2),
         ("rank_slices", ctypes.c_void_p), ("rank_arrive", ctypes.c_void_p), ("arrive_local", ctypes.c_void_p),
         ("base", ctypes.c_uint64), ("timeout_ns", ctypes.c_int64),
+        ("halo_planes", ctypes.c_int32), ("gdiag_lo", ctypes.c_void_p), ("gdiag_hi", ctypes.c_void_p),
     ]
 
 

@@ -306,6 +306,61 @@ ES_DEV void slice_p2p_decide(const SeriesParams &P, int k) {
     }
 }
 
+// Peer-memory two-node pass (stencil_tb.cuh on a slab): both nodes' slices
+// into every rank's table (layout [parity][node][total_slices][2]), ONE
+// round barrier per pass, then the identical tests for node k and -- unless
+// that ended the series -- node k + 1 on every rank.
+ES_DEV void slice_p2p_decide2(const SeriesParams &P, int k) {
+    __shared__ int s_last, s_ok;
+    const int c = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const bool two = k + 1 <= P.ndd - 1;
+    const int pass = (k - 1) / 2, par = pass & 1;
+    const int64_t half = (int64_t)P.nslices * P.ntiles * 2;
+    double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+    cta_slice_sum(P, c, a0, b0);
+    __syncthreads();
+    if (two) cta_slice_sum(P, c, a1, b1, P.part + half);
+    if (t == 0) {
+        for (int q = 0; q < P.nranks; ++q) {
+            double *tab = P.rank_slices[q] + (int64_t)par * 2 * P.total_slices * 2;
+            *reinterpret_cast<double2 *>(tab + (P.slice_off + c) * 2) = make_double2(a0, b0);
+            *reinterpret_cast<double2 *>(tab + (P.total_slices + P.slice_off + c) * 2) = make_double2(a1, b1);
+        }
+        __threadfence_system();
+        s_last = atomicAdd(P.global_cnt, 1u) == gridDim.x - 1u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (t == 0) {
+        *P.global_cnt = 0u;
+        s_ok = p2p_round(P, pass + 1);
+    }
+    __syncthreads();
+    if (!s_ok) {
+        if (t == 0) p2p_fail(P, k, true);
+        return;
+    }
+    if (warp == 0) {
+        const double *tab = P.rank_slices[P.rank] + (int64_t)par * 2 * P.total_slices * 2;
+        for (int node = 0; node < (two ? 2 : 1); ++node) {
+            const double *sl = tab + (int64_t)node * P.total_slices * 2;
+            double sw = 0.0, sp = 0.0;
+            for (int64_t s = lane; s < P.total_slices; s += 32) {
+                sw = add(sw, __ldcg(sl + 2 * s));
+                sp = add(sp, __ldcg(sl + 2 * s + 1));
+            }
+            sw = warp_sum(sw);
+            sp = warp_sum(sp);
+            int stop = 0;
+            if (lane == 0) {
+                decide(P, k + node, sw, sp);
+                stop = P.state->done;
+            }
+            if (__shfl_sync(0xffffffffu, stop, 0)) break;
+        }
+    }
+}
+
 // Reduction of a two-node pass (stencil_tb.cuh): both nodes' slices in
 // the one-node order, then the stopping test for node k and -- unless that
 // ended the series -- for node k + 1.

@@ -203,6 +203,54 @@ __global__ void __launch_bounds__(256) k_p2p_init(const SeriesParams *__restrict
     if (!p2p_round(P, 0)) p2p_fail(P, 0, false);
 }
 
+// Peer-memory two-node pass: push the first / last TWO planes of w_{k+1} into
+// the neighbours' halo buffers of the next pass's parity, then the two-node
+// slice reduction, round barrier and decisions.
+__global__ void __launch_bounds__(256) k_slice_p2p2(const SeriesParams *__restrict__ Pp) {
+    const SeriesParams &P = *Pp;
+    if (P.state->done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && P.cond)
+            cudaGraphSetConditional((cudaGraphConditionalHandle)P.cond, 0);
+        return;
+    }
+    const int k = P.state->k + 1;
+    const int pass = (k - 1) / 2, par = (pass + 1) & 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && P.work) *P.work = 0u;
+    const double2 *w = reinterpret_cast<const double2 *>(P.wbuf[pass & 1]);  // w_{k+1}
+    double2 *lo = reinterpret_cast<double2 *>(P.peer_lo[par]), *hi = reinterpret_cast<double2 *>(P.peer_hi[par]);
+    const int64_t two_planes = P.g.nx * P.g.ny, lz = P.g.lz;  // two planes = nx ny double2
+    if (lo || hi) {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < two_planes;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            if (lo) lo[i] = __ldcg(w + i);                              // planes 0, 1 -> its L, L+1
+            if (hi) hi[i] = __ldcg(w + (lz - 2) * (two_planes / 2) + i);  // planes L-2, L-1 -> its -2, -1
+        }
+        __threadfence_system();
+        __syncthreads();
+    }
+    slice_p2p_decide2(P, k);
+}
+
+// Round 0 of a peer-memory two-node series: v's two boundary planes on each
+// side into the neighbours' halo buffers of parity 0 (read by pass 0).
+__global__ void __launch_bounds__(256) k_p2p_init2(const SeriesParams *__restrict__ Pp, int64_t plane, int64_t lz) {
+    __shared__ int s_last;
+    const SeriesParams &P = *Pp;
+    const double2 *v = reinterpret_cast<const double2 *>(P.v);
+    double2 *lo = reinterpret_cast<double2 *>(P.peer_lo[0]), *hi = reinterpret_cast<double2 *>(P.peer_hi[0]);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane; i += (int64_t)gridDim.x * blockDim.x) {
+        if (lo) lo[i] = v[i];
+        if (hi) hi[i] = v[(lz - 2) * (plane / 2) + i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(P.global_cnt, 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    *P.global_cnt = 0u;
+    if (!p2p_round(P, 0)) p2p_fail(P, 0, false);
+}
+
 // Two Leja nodes per pass (stencil_tb.cuh) and its reduction / decisions.
 template <int COEFF, bool GD>
 __global__ void __launch_bounds__(TMA_THREADS, 2) k_node_tb(const SeriesParams *__restrict__ Pp) {
@@ -690,7 +738,8 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
                           const double *xi, int ndd, double alpha, double shift, double tol, const double *gdiag,
                           const double *halo_lo, const double *halo_hi, bool dist, void *ws, size_t ws_bytes,
                           SeriesSetup &S, cudaStream_t stream, const double *halo_lo_1 = nullptr,
-                          const double *halo_hi_1 = nullptr, bool allow_tb = true) {
+                          const double *halo_hi_1 = nullptr, int allow_tb = 1, const double *g_lo = nullptr,
+                          const double *g_hi = nullptr) {
     S.n = d->nx * d->ny * d->lz;
     char *w = static_cast<char *>(ws);
     S.pl = plan_stencil(d, {v, p_out, gdiag, halo_lo, halo_hi, (const void *)(w + 0)}, true);
@@ -703,8 +752,11 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     // Longer z chunks than the one-node kernel's: an item re-reads three w
     // planes beyond its chunk (8 -> 32: 767 -> 685 us).  ES_TB=0 forces one
     // node per pass.
-    S.tb = pl.tma && allow_tb && !pl.dim2 && !halo_lo && !halo_hi && !dist &&
-           (d->mode == ES_MODE_ZERO || d->mode == ES_MODE_NEUMANN) && env_int("ES_TB", 1);
+    // allow_tb: 0 never, 1 one domain only, 2 also slabs with two-plane peer halos
+    const bool halos = halo_lo || halo_hi;
+    S.tb = pl.tma && allow_tb > 0 && !pl.dim2 && !dist && (d->mode == ES_MODE_ZERO || d->mode == ES_MODE_NEUMANN) &&
+           env_int("ES_TB", 1) &&
+           (!halos || (allow_tb == 2 && d->coeff_kind != ES_COEFF_ARRAY && d->lz >= 2));
     if (S.tb) {
         pl.chunk = std::max(1, env_int("ES_TBCHUNK", 32));
         pl.grid.z = (unsigned)((d->lz + pl.chunk - 1) / pl.chunk);
@@ -777,6 +829,16 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
             if (!rc) rc = encode_map(&maps.m[MAP_T_1], hp.wbuf[1], d, false, MK_W2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_G], gdiag, d, false, MK_W);
             if (!rc) rc = encode_map(&maps.m[MAP_T_PV], v, d, false, MK_P);
+            if (halos) {  // two-plane w halos by parity, g' boundary planes of the neighbours
+                es_stencil_desc d2 = *d;
+                d2.lz = 2;
+                if (!rc) rc = encode_map(&maps.m[MAP_T_HLO0], halo_lo, &d2, false, MK_W2);
+                if (!rc) rc = encode_map(&maps.m[MAP_T_HLO1], halo_lo_1, &d2, false, MK_W2);
+                if (!rc) rc = encode_map(&maps.m[MAP_T_HHI0], halo_hi, &d2, false, MK_W2);
+                if (!rc) rc = encode_map(&maps.m[MAP_T_HHI1], halo_hi_1, &d2, false, MK_W2);
+                if (!rc) rc = encode_map(&maps.m[MAP_T_GLO], g_lo, d, false, MK_HALO);
+                if (!rc) rc = encode_map(&maps.m[MAP_T_GHI], g_hi, d, false, MK_HALO);
+            }
         }
         if (rc) return rc;
         TmaMaps *dmaps = reinterpret_cast<TmaMaps *>(w + L.maps);
@@ -941,11 +1003,18 @@ int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double 
     if ((x->halo_lo[0] == nullptr) != (x->halo_lo[1] == nullptr) || (x->halo_hi[0] == nullptr) != (x->halo_hi[1] == nullptr) ||
         (x->peer_lo[0] == nullptr) != (x->halo_lo[0] == nullptr) || (x->peer_hi[0] == nullptr) != (x->halo_hi[0] == nullptr))
         return set_error(ES_ERR_ARG, "halo / peer buffers must come in parity pairs, one per existing neighbour");
+    const bool want_tb = x->halo_planes == 2;
+    if (want_tb && gdiag && ((x->halo_lo[0] && !x->gdiag_lo) || (x->halo_hi[0] && !x->gdiag_hi)))
+        return set_error(ES_ERR_ARG, "two-node peer series with g' need the neighbours' g' planes");
     SeriesSetup S;
     int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, x->halo_lo[0], x->halo_hi[0], false, ws,
-                            ws_bytes, S, stream, x->halo_lo[1], x->halo_hi[1], false);
+                            ws_bytes, S, stream, x->halo_lo[1], x->halo_hi[1], want_tb ? 2 : 0, x->gdiag_lo,
+                            x->gdiag_hi);
     if (rc) return rc;
     if (!S.pl.tma || S.pl.dim2) return set_error(ES_ERR_ARG, "peer-memory series need the 3D TMA path");
+    if (want_tb != S.tb)
+        return set_error(ES_ERR_ARG, "halo_planes = 2 needs a two-node slab (Dirichlet / Neumann, no coefficient "
+                                     "array, lz >= 2, ES_TB not 0)");
     if (x->slice_offset < 0 || x->slice_offset + S.pl.nslices > x->total_slices)
         return set_error(ES_ERR_ARG, "slice offset / total do not cover this slab's %d slices", S.pl.nslices);
     SeriesParams &hp = S.hp;
@@ -963,23 +1032,27 @@ int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double 
     hp.arrive_local = x->arrive_local;
     hp.base = x->base;
     hp.timeout_ns = x->timeout_ns > 0 ? x->timeout_ns : 10000000000ll;
+    NodeFn sf = S.tb ? k_slice_p2p2 : k_slice_p2p;
     GraphKernel gk[2] = {{(const void *)S.nf, S.lp.grid, S.lp.block, S.lp.smem},
-                         {(const void *)k_slice_p2p, dim3((unsigned)S.pl.nslices), dim3(256), 0}};
+                         {(const void *)sf, dim3((unsigned)S.pl.nslices), dim3(256), 0}};
     unsigned long long handle = 0;
     cudaGraphExec_t ge = series_graph(gk, 2, S.dparams, &handle);
     if (ge) hp.cond = handle;
     k_series_init<<<1, 256, 0, stream>>>(hp, S.dparams);
     const int64_t plane = d->nx * d->ny;
-    k_p2p_init<<<(unsigned)std::min<int64_t>(std::max<int64_t>(1, (plane / 2 + 255) / 256), 148), 256, 0, stream>>>(
-        S.dparams, plane, d->lz);
+    const unsigned ig = (unsigned)std::min<int64_t>(std::max<int64_t>(1, (plane / 2 + 255) / 256), 148);
+    if (S.tb)
+        k_p2p_init2<<<ig, 256, 0, stream>>>(S.dparams, plane, d->lz);
+    else
+        k_p2p_init<<<ig, 256, 0, stream>>>(S.dparams, plane, d->lz);
     rc = check_launch("peer-memory series init");
     if (rc) return rc;
     if (ge) {
         if (cudaGraphLaunch(ge, stream) != cudaSuccess) return check_launch("peer-memory series graph");
     } else {
-        for (int k = 1; k < ndd; ++k) {
+        for (int k = 1; k < ndd; k += S.tb ? 2 : 1) {
             S.nf<<<S.lp.grid, S.lp.block, S.lp.smem, stream>>>(S.dparams);
-            k_slice_p2p<<<(unsigned)S.pl.nslices, 256, 0, stream>>>(S.dparams);
+            sf<<<(unsigned)S.pl.nslices, 256, 0, stream>>>(S.dparams);
         }
     }
     k_series_finalize<<<148 * 8, 256, 0, stream>>>(S.dparams, S.n);

@@ -68,6 +68,8 @@ struct TbLayout {
 
 struct TbMaps {
     const CUtensorMap *w, *g, *p;
+    // peer-memory slabs: the neighbours' two w planes (this pass's parity) and g' planes, or null
+    const CUtensorMap *hlo = nullptr, *hhi = nullptr, *glo = nullptr, *ghi = nullptr;
 };
 
 template <bool GD>
@@ -91,8 +93,13 @@ ES_DEV void tb_produce(const Geom &g, const Items &its, const TbMaps &mp, char *
                 if (uw >= (uint32_t)Lt::SW) mbar_wait(&wempty[s], ((uw / Lt::SW) - 1) & 1);
                 itemq[s] = i;
                 mbar_expect_tx(&wfull[s], TB_WX * TB_WY * 8);
-                tma_load(smem + Lt::W_OFF + s * Lt::W_STAGE, mp.w, &wfull[s], it.x0 - 4, it.y0 - 2,
-                         march_src<true>(g, t, its.L));
+                char *dst = smem + Lt::W_OFF + s * Lt::W_STAGE;
+                if (t < 0 && mp.hlo)  // planes -2, -1 from the lower neighbour
+                    tma_load(dst, mp.hlo, &wfull[s], it.x0 - 4, it.y0 - 2, t + 2);
+                else if (t >= its.L && mp.hhi)  // planes L, L+1 from the upper neighbour
+                    tma_load(dst, mp.hhi, &wfull[s], it.x0 - 4, it.y0 - 2, t - its.L);
+                else
+                    tma_load(dst, mp.w, &wfull[s], it.x0 - 4, it.y0 - 2, march_src<true>(g, t, its.L));
                 ++uw;
             }
             const int tg = t - 1;  // G(t-1), P(t-1): what consumer iteration t-1 needs besides W(t)
@@ -101,7 +108,13 @@ ES_DEV void tb_produce(const Geom &g, const Items &its, const TbMaps &mp, char *
                     const uint32_t s = ug % Lt::SG;
                     if (ug >= (uint32_t)Lt::SG) mbar_wait(&gempty[s], ((ug / Lt::SG) - 1) & 1);
                     mbar_expect_tx(&gfull[s], TB_GX * TB_GY * 8);
-                    tma_load(smem + Lt::G_OFF + s * Lt::G_STAGE, mp.g, &gfull[s], it.x0 - 2, it.y0 - 1, tg);
+                    char *dst = smem + Lt::G_OFF + s * Lt::G_STAGE;
+                    if (tg < 0 && mp.glo)
+                        tma_load(dst, mp.glo, &gfull[s], it.x0 - 2, it.y0 - 1);
+                    else if (tg >= its.L && mp.ghi)
+                        tma_load(dst, mp.ghi, &gfull[s], it.x0 - 2, it.y0 - 1);
+                    else
+                        tma_load(dst, mp.g, &gfull[s], it.x0 - 2, it.y0 - 1, tg);
                     ++ug;
                 }
             }
@@ -234,6 +247,7 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const Items 
     double *vwin = reinterpret_cast<double *>(smem + Lt::V_OFF);
     const int a = threadIdx.x;  // 0..127
     const bool neu = g.mode == ES_MODE_NEUMANN;
+    const bool has_lo = g.halo_lo != nullptr, has_hi = g.halo_hi != nullptr;  // peer slabs below / above
     const double alpha = P->alpha, beta_k = sub(-P->shift, P->xi[k - 1]);
     int pey[3], pex[3];
 #pragma unroll
@@ -287,7 +301,7 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const Items 
             take_v();
             double *Vj = vslot(vr.slot);
             if (j == it.mb - 1 && a == 0) vitem[vr.slot] = i;
-            const bool zin = j >= 0 && j < its.L;
+            const bool zin = (j >= 0 || has_lo) && (j < its.L || has_hi);
             bool arrive_prev = false;
             if (zin) {
 #pragma unroll
@@ -303,7 +317,7 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const Items 
                                                                  beta_k));
                     *reinterpret_cast<double2 *>(Vj + ey * TB_EX + ex) = wk;
                 }
-                if (neu && j == 0) {  // the mirrored plane below the domain = w_k of plane 0
+                if (neu && j == 0 && !has_lo) {  // the mirrored plane below the domain = w_k of plane 0
                     a_group_sync();
                     double *Vb = vslot(v_prev);
                     for (int e = a; e < TB_EX * TB_EY; e += 128) Vb[e] = Vj[e];
@@ -322,7 +336,7 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const Items 
                 gr.next();
             }
             if (arrive_prev) warp_arrive(&B.vfull[v_prev]);
-            if (!(neu && j < 0)) warp_arrive(&B.vfull[vr.slot]);  // Neumann plane -1 arrives with plane 0
+            if (!(neu && j < 0 && !has_lo)) warp_arrive(&B.vfull[vr.slot]);  // Neumann plane -1 arrives with plane 0
             v_prev = vr.slot;
             vr.next();
             rm = rc;
@@ -475,8 +489,12 @@ ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
     const TmaMaps &M = *static_cast<const TmaMaps *>(P->maps);
     const int pass = (k - 1) / 2;
     // W: w_{k-1} (v on the first pass); P: p_{k-1}, or v on the first pass (p_0 = dd_0 v)
-    const TbMaps mp{&M.m[pass == 0 ? MAP_T_V : (pass & 1) ? MAP_T_0 : MAP_T_1], &M.m[MAP_T_G],
-                    &M.m[pass == 0 ? MAP_T_PV : MAP_P_0]};
+    TbMaps mp{&M.m[pass == 0 ? MAP_T_V : (pass & 1) ? MAP_T_0 : MAP_T_1], &M.m[MAP_T_G],
+              &M.m[pass == 0 ? MAP_T_PV : MAP_P_0]};
+    if (g.halo_lo) mp.hlo = &M.m[(pass & 1) ? MAP_T_HLO1 : MAP_T_HLO0];  // pass p reads halo parity p & 1
+    if (g.halo_hi) mp.hhi = &M.m[(pass & 1) ? MAP_T_HHI1 : MAP_T_HHI0];
+    if (GD && g.halo_lo) mp.glo = &M.m[MAP_T_GLO];
+    if (GD && g.halo_hi) mp.ghi = &M.m[MAP_T_GHI];
     if (threadIdx.x == 0) {
         const TbBars B = tb_bars<GD>(smem);
         for (int s = 0; s < Lt::SW; ++s) {
@@ -504,6 +522,8 @@ ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
             tma_acquire(mp.w);
             if (GD) tma_acquire(mp.g);
             tma_acquire(mp.p);
+            for (const CUtensorMap *h : {mp.hlo, mp.hhi, mp.glo, mp.ghi})
+                if (h) tma_acquire(h);
             tb_produce<GD>(g, its, mp, smem, true, P->work);
         }
     } else if (warp < 4) {

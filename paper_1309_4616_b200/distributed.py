@@ -351,7 +351,9 @@ class _PeerMemory:
         rc = self.lib.es_leja_fetch(ptr(ws), ctypes.byref(res), stream_handle())
         if rc != _lib.ES_ERR_NOT_CONVERGED:
             _lib.check(rc, "es_leja_fetch")
-        self.rounds += int(res.matvecs) + 1  # round 0 + one per node, identical on every rank
+        # round 0 + one per node (one per two-node pass), identical on every rank
+        k = int(res.matvecs)
+        self.rounds += ((k + 1) // 2 if getattr(self, "two", False) else k) + 1
         return res
 
     def close(self):
@@ -372,14 +374,20 @@ class PeerSlab(_PeerMemory):
         self.comm = c = comm
         dev = torch.device("cuda", torch.cuda.current_device())
         plane = c.plane
-        # [lo parity 0, lo parity 1, hi parity 0, hi parity 1]
-        self.halo = torch.zeros(4 * plane, dtype=torch.float64, device=dev)
+        # two Leja nodes per pass on the slab (the single-GPU default) where the
+        # C side allows it: two-plane halos, one round per pass
+        self.two = (op.two_node_passes() and op.coeff_kind() != _lib.ES_COEFF_ARRAY and c.lz >= 2
+                    and all(hi - lo >= 2 for lo, hi in c.partition.ranges()))
+        hp = 2 if self.two else 1
+        # [lo parity 0, lo parity 1, hi parity 0, hi parity 1], hp planes each
+        self.halo = torch.zeros(4 * hp * plane, dtype=torch.float64, device=dev)
+        self.ghalo = torch.zeros(2 * plane, dtype=torch.float64, device=dev) if self.two else None
         d, keep = op.desc(z0=c.z_lo, lz=c.lz)
         ns = ctypes.c_int32()
         _lib.check(self.lib.es_leja_stencil_nslices(ctypes.byref(d), ctypes.byref(ns)), "es_leja_stencil_nslices")
         counts = [None] * c.world
         dist.all_gather_object(counts, int(ns.value), group=c.group)
-        self.slices = torch.zeros(2 * sum(counts) * 2, dtype=torch.float64, device=dev)
+        self.slices = torch.zeros(hp * 2 * sum(counts) * 2, dtype=torch.float64, device=dev)
         self.arrive = torch.zeros(1, dtype=torch.int64, device=dev)
         ptrs = self._exchange(c, (self.halo, self.slices, self.arrive))  # per rank: (halo, slices, arrive)
         self.rank_slices = torch.tensor([p[1] for p in ptrs], dtype=torch.int64, device=dev)
@@ -391,11 +399,12 @@ class PeerSlab(_PeerMemory):
         base = self.halo.data_ptr()
         for par in range(2):
             if c.rank > 0:  # receive from / send to the lower neighbour
-                x.halo_lo[par] = base + 8 * par * plane
-                x.peer_lo[par] = ptrs[c.rank - 1][0] + 8 * (2 + par) * plane  # its halo_hi
+                x.halo_lo[par] = base + 8 * par * hp * plane
+                x.peer_lo[par] = ptrs[c.rank - 1][0] + 8 * (2 + par) * hp * plane  # its halo_hi
             if c.rank < c.world - 1:
-                x.halo_hi[par] = base + 8 * (2 + par) * plane
-                x.peer_hi[par] = ptrs[c.rank + 1][0] + 8 * par * plane  # its halo_lo
+                x.halo_hi[par] = base + 8 * (2 + par) * hp * plane
+                x.peer_hi[par] = ptrs[c.rank + 1][0] + 8 * par * hp * plane  # its halo_lo
+        x.halo_planes = hp
         x.rank_slices, x.rank_arrive = self.rank_slices.data_ptr(), self.rank_arrive.data_ptr()
         x.arrive_local = self.arrive.data_ptr()
         x.timeout_ns = int(timeout_s * 1e9)
@@ -405,6 +414,14 @@ class PeerSlab(_PeerMemory):
     def enqueue(self, d, v, p_out, dd, xi, alpha, shift, tol, gdiag, ws):
         """Enqueue the whole series (one graph) on the current stream."""
         self.desc.base = self.comm.world * self.rounds
+        c = self.comm
+        self.desc.gdiag_lo = self.desc.gdiag_hi = None
+        if self.two and gdiag is not None:  # the neighbours' g' boundary planes, once per series
+            lo = self.ghalo[: c.plane] if c.rank > 0 else None
+            hi = self.ghalo[c.plane:] if c.rank < c.world - 1 else None
+            c.exchange(gdiag, lo, hi)
+            self.desc.gdiag_lo = lo.data_ptr() if lo is not None else None
+            self.desc.gdiag_hi = hi.data_ptr() if hi is not None else None
         rc = self.lib.es_leja_p2p(ctypes.byref(d), ctypes.byref(self.desc), ptr(v), ptr(p_out), ptr(dd), ptr(xi),
                                   dd.numel(), float(alpha), float(shift), float(tol), ptr(gdiag), ptr(ws), ws.numel(),
                                   stream_handle())
@@ -550,6 +567,12 @@ class DistributedStencil:
             tm.add(ev0, timing.event(), res.matvecs)
         del keep
         return res
+
+    def two_node_passes(self) -> bool:
+        """Whether this rank's series run two Leja nodes per HBM pass."""
+        if self.whole:
+            return self.base_operator.two_node_passes()
+        return self.peer is not None and self.peer.two
 
     def halo_exchange(self, x: torch.Tensor):
         """Fill the halo planes from the neighbours' copies of x (for fused

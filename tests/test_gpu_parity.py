@@ -598,9 +598,10 @@ def test_complex_series_large_vs_oracle():
 # ---- peer-memory (NVLink P2P) slab series, emulated ranks on one device -----
 
 
-def _p2p_ranks(op, bounds, timeout_ns=5_000_000_000):
+def _p2p_ranks(op, bounds, timeout_ns=5_000_000_000, two=False):
     """Per-rank buffers and es_p2p_desc of an in-process emulation: every
-    "peer" address is another emulated rank's local buffer."""
+    "peer" address is another emulated rank's local buffer.  two: two Leja
+    nodes per pass (two-plane halos, halo_planes = 2)."""
     import ctypes
 
     from paper_1309_4616_b200 import _lib
@@ -616,11 +617,13 @@ def _p2p_ranks(op, bounds, timeout_ns=5_000_000_000):
         _lib.check(lib.es_leja_stencil_nslices(ctypes.byref(d), ctypes.byref(ns)))
         counts.append(ns.value)
     total = sum(counts)
+    hp = 2 if two else 1
     ranks = []
     for r, (lo, hi) in enumerate(bounds):
-        ranks.append(dict(lo=lo, hi=hi, halo=torch.zeros(4 * plane, dtype=torch.float64, device="cuda"),
-                          slices=torch.zeros(4 * total, dtype=torch.float64, device="cuda"),
-                          arrive=torch.zeros(1, dtype=torch.int64, device="cuda"), off=sum(counts[:r])))
+        ranks.append(dict(lo=lo, hi=hi, halo=torch.zeros(4 * hp * plane, dtype=torch.float64, device="cuda"),
+                          slices=torch.zeros(hp * 4 * total, dtype=torch.float64, device="cuda"),
+                          ghalo=torch.zeros(2 * plane, dtype=torch.float64, device="cuda"),
+                          arrive=torch.zeros(1, dtype=torch.int64, device="cuda"), off=sum(counts[:r]), two=two))
     rank_slices = torch.tensor([q["slices"].data_ptr() for q in ranks], dtype=torch.int64, device="cuda")
     rank_arrive = torch.tensor([q["arrive"].data_ptr() for q in ranks], dtype=torch.int64, device="cuda")
     for r, q in enumerate(ranks):
@@ -628,11 +631,15 @@ def _p2p_ranks(op, bounds, timeout_ns=5_000_000_000):
         x.nranks, x.rank, x.slice_offset, x.total_slices = m, r, q["off"], total
         for par in range(2):
             if r > 0:
-                x.halo_lo[par] = q["halo"].data_ptr() + 8 * par * plane
-                x.peer_lo[par] = ranks[r - 1]["halo"].data_ptr() + 8 * (2 + par) * plane
+                x.halo_lo[par] = q["halo"].data_ptr() + 8 * par * hp * plane
+                x.peer_lo[par] = ranks[r - 1]["halo"].data_ptr() + 8 * (2 + par) * hp * plane
             if r < m - 1:
-                x.halo_hi[par] = q["halo"].data_ptr() + 8 * (2 + par) * plane
-                x.peer_hi[par] = ranks[r + 1]["halo"].data_ptr() + 8 * par * plane
+                x.halo_hi[par] = q["halo"].data_ptr() + 8 * (2 + par) * hp * plane
+                x.peer_hi[par] = ranks[r + 1]["halo"].data_ptr() + 8 * par * hp * plane
+        x.halo_planes = hp
+        if two:  # g' boundary planes of the neighbours (filled per run by _p2p_run)
+            x.gdiag_lo = q["ghalo"].data_ptr() if r > 0 else None
+            x.gdiag_hi = q["ghalo"].data_ptr() + 8 * plane if r < m - 1 else None
         x.rank_slices, x.rank_arrive, x.arrive_local = rank_slices.data_ptr(), rank_arrive.data_ptr(), \
             q["arrive"].data_ptr()
         x.timeout_ns = timeout_ns
@@ -700,9 +707,15 @@ def _p2p_run(op, ranks, it, v, tol, rounds, only=None, gdiag=None):
     vd = torch.from_numpy(v).cuda()
     gd = None if gdiag is None else torch.from_numpy(gdiag).cuda()
     launched = [q for r, q in enumerate(ranks) if only is None or r in only]
+    nz = op.grid.nz
     for q in launched:  # all host-side preparation before any rank starts spinning
         q["v"] = vd[q["lo"] * plane: q["hi"] * plane].clone()
         q["g"] = None if gd is None else gd[q["lo"] * plane: q["hi"] * plane].clone()
+        if gd is not None and q["two"]:
+            if q["lo"] > 0:
+                q["ghalo"][:plane] = gd[(q["lo"] - 1) * plane: q["lo"] * plane]
+            if q["hi"] < nz:
+                q["ghalo"][plane:] = gd[q["hi"] * plane: (q["hi"] + 1) * plane]
         q["p"] = torch.empty_like(q["v"])
         q["desc"].base = len(ranks) * rounds
     torch.cuda.synchronize()
@@ -722,14 +735,15 @@ def _p2p_run(op, ranks, it, v, tol, rounds, only=None, gdiag=None):
     return out
 
 
+@pytest.mark.parametrize("two", [False, True])
 @pytest.mark.parametrize("graph", [True, False])
-def test_p2p_slab_series_emulated_ranks_bitwise(graph, monkeypatch):
+def test_p2p_slab_series_emulated_ranks_bitwise(graph, two, monkeypatch):
     if not graph:
         monkeypatch.setenv("ES_NO_GRAPH", "1")
     g = es.Grid3D(64, 40, 48)
     op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
     bounds = [(0, 16), (16, 40), (40, 48)]  # chunk-aligned: decisions bitwise those of one domain
-    ranks, keep = _p2p_ranks(op, bounds)
+    ranks, keep = _p2p_ranks(op, bounds, two=two)
     rounds = 0
     for target, scale, tol in (("exp", -4e-4, 0.0), ("phi1", -3e-4, 1e-8), ("exp", -4e-4, 1e-8)):
         it = es.make_interpolant(es.gershgorin_interval(op), target, scale, 40, 1e-8)
@@ -739,14 +753,15 @@ def test_p2p_slab_series_emulated_ranks_bitwise(graph, monkeypatch):
         assert [o[0] for o in outs] == [0, 0, 0]
         assert [o[1] for o in outs] == [mv] * 3
         assert np.concatenate([o[2] for o in outs]).tobytes() == ref.tobytes()
-        rounds += mv + 1  # consecutive series continue the counters
+        rounds += ((mv + 1) // 2 if two else mv) + 1  # consecutive series continue the counters
 
 
-def test_p2p_slab_series_rosenbrock_diag_and_neumann():
+@pytest.mark.parametrize("two", [False, True])
+def test_p2p_slab_series_rosenbrock_diag_and_neumann(two):
     g = es.Grid3D(32, 24, 40)
     op = es.StencilOperator(g, es.BoundaryCondition.neumann())
     bounds = [(0, 8), (8, 16), (16, 32), (32, 40)]
-    ranks, keep = _p2p_ranks(op, bounds)
+    ranks, keep = _p2p_ranks(op, bounds, two=two)
     it = es.make_interpolant(es.gershgorin_interval(op).widened(50.0), "phi1", -5e-4, 50, 1e-8)
     v = np.random.default_rng(5).standard_normal(g.n)
     gd = np.random.default_rng(6).random(g.n) * 30.0
@@ -761,7 +776,7 @@ def test_p2p_missing_peer_times_out_instead_of_hanging():
 
     g = es.Grid3D(32, 16, 16)
     op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
-    ranks, keep = _p2p_ranks(op, [(0, 8), (8, 16)], timeout_ns=200_000_000)
+    ranks, keep = _p2p_ranks(op, [(0, 8), (8, 16)], timeout_ns=200_000_000, two=True)
     it = es.make_interpolant(es.gershgorin_interval(op), "exp", -1e-3, 20, 1e-8)
     v = np.random.default_rng(1).standard_normal(g.n)
     (rc, mv, _), = _p2p_run(op, ranks, it, v, 0.0, 0, only=[0])
