@@ -39,6 +39,9 @@ constexpr int TB_GX = 68, TB_GY = 10;  // g': x0-2 .. x0+65, y0-1 .. y0+8
 #ifndef TB_SG
 #define TB_SG 5
 #endif
+#ifndef TB_SP
+#define TB_SP 4
+#endif
 #ifndef TB_SW_GD
 #define TB_SW_GD 6
 #endif
@@ -50,7 +53,7 @@ template <bool GD>
 struct TbLayout {
     // ring depths: two CTAs per SM (<= 113 KiB each); G slots are held until
     // group C is done with the plane, so the G ring is the deeper one
-    static constexpr int SW = GD ? TB_SW_GD : TB_SW_NG, SG = GD ? TB_SG : 0, SP = 4;
+    static constexpr int SW = GD ? TB_SW_GD : TB_SW_NG, SG = GD ? TB_SG : 0, SP = TB_SP;
     static constexpr int W_STAGE = (TB_WX * TB_WY * 8 + 127) & ~127;
     static constexpr int G_STAGE = (TB_GX * TB_GY * 8 + 127) & ~127;
     static constexpr int P_STAGE = 64 * 8 * 8;
