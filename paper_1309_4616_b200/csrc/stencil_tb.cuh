@@ -428,15 +428,28 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                         if (!act[h]) continue;
                         const int r = cw + 4 * h;
                         const int o = (r + 1) * TB_EX + 2 * q + 2;
+                        // pair loads (16-byte aligned: o is even), as in tb_fast_pair
+                        const double2 cc = *reinterpret_cast<const double2 *>(Vc + o);
+                        const double2 ym = *reinterpret_cast<const double2 *>(Vc + o - TB_EX);
+                        const double2 yp = *reinterpret_cast<const double2 *>(Vc + o + TB_EX);
+                        const double2 zm = *reinterpret_cast<const double2 *>(Vm + o);
+                        const double2 zp = *reinterpret_cast<const double2 *>(Vp + o);
+                        double lap[2] = {lap7(cc.x, Vc[o - 1], cc.y, ym.x, yp.x, zm.x, zp.x, g.wx, g.wy, g.wz),
+                                         lap7(cc.y, cc.x, Vc[o + 2], ym.y, yp.y, zm.y, zp.y, g.wx, g.wy, g.wz)};
+                        const double cv[2] = {cc.x, cc.y};
+                        double gv[2] = {0.0, 0.0};
+                        if constexpr (GD) {
+                            const double2 g2 = *reinterpret_cast<const double2 *>(Gc + (r + 1) * TB_GX + 2 * q + 2);
+                            gv[0] = g2.x;
+                            gv[1] = g2.y;
+                        }
                         double wn[2], pn[2];
 #pragma unroll
                         for (int jj = 0; jj < 2; ++jj) {
-                            const double cc = Vc[o + jj];
-                            double lap = lap7(cc, Vc[o + jj - 1], Vc[o + jj + 1], Vc[o + jj - TB_EX], Vc[o + jj + TB_EX],
-                                              Vm[o + jj], Vp[o + jj], g.wx, g.wy, g.wz);
-                            if constexpr (COEFF != ES_COEFF_NONE) lap = mul(tb_coeff<COEFF>(g, xa + jj, ya[h], jc), lap);
-                            if constexpr (GD) lap = sub(lap, mul(Gc[(r + 1) * TB_GX + 2 * q + jj + 2], cc));
-                            wn[jj] = add(mul(alpha, lap), mul(beta_k1, cc));
+                            if constexpr (COEFF != ES_COEFF_NONE)
+                                lap[jj] = mul(tb_coeff<COEFF>(g, xa + jj, ya[h], jc), lap[jj]);
+                            if constexpr (GD) lap[jj] = sub(lap[jj], mul(gv[jj], cv[jj]));
+                            wn[jj] = add(mul(alpha, lap[jj]), mul(beta_k1, cv[jj]));
                             pn[jj] = add(pk_prev[2 * h + jj], mul(dk1, wn[jj]));
                         }
                         const int64_t off = jc * plane + ya[h] * g.nx + xa;
