@@ -1057,3 +1057,24 @@ def test_two_node_pass_bitwise(graph, monkeypatch):
         monkeypatch.delenv("ES_TB")
         assert mv2 == mv, (dims, bc)
         assert torch.equal(got, ref), (dims, bc)
+
+
+@pytest.mark.parametrize("dims,bc,nodes", [((6, 4, 2), "homogeneous", 7), ((10, 9, 3), "neumann", 8),
+                                           ((130, 17, 33), "homogeneous", 9), ((64, 8, 64), "neumann", 2),
+                                           ((66, 10, 35), "homogeneous", 3), ((2, 2, 5), "neumann", 6)])
+def test_two_node_pass_edges_vs_oracle(dims, bc, nodes, monkeypatch):
+    """Two-node passes on tiny / ragged grids (tiles cut by the domain in x, y
+    and z, one- and two-plane slabs, odd and even node counts, g' diagonal)
+    against the oracle, bitwise, at fixed degree."""
+    g = es.Grid3D(*dims)
+    op = es.StencilOperator(g, BCS[bc])
+    lo, hi = es.gershgorin_bounds(op)
+    it = es.make_interpolant(es.SpectralInterval(lo, hi), "phi1", -2e-4, nodes, 1e-8)
+    rng = np.random.default_rng(sum(dims))
+    v = rng.standard_normal(g.n)
+    gd = rng.random(g.n) * 5.0
+    p, mv = es.newton_apply(es.RosenbrockOperator(op, torch.from_numpy(gd).cuda()), it, v, 0.0)
+    spec = orc.StencilSpec(*dims, mode=ORC_MODE[bc])
+    ref, _ = orc.newton_stencil(spec, orc.Interp(lo, hi, "phi1", -2e-4, it.xi, it.dd), v, 0.0, gdiag=gd)
+    assert mv == nodes
+    assert np.asarray(p).tobytes() == ref.tobytes()
