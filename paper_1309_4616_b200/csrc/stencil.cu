@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(256) k_p2p_init2(const SeriesParams *__restric
 
 // Two Leja nodes per pass (stencil_tb.cuh) and its reduction / decisions.
 template <int COEFF, bool GD>
-__global__ void __launch_bounds__(TMA_THREADS, 2) k_node_tb(const SeriesParams *__restrict__ Pp) {
+__global__ void __launch_bounds__(TB_THREADS, TB_MINB) k_node_tb(const SeriesParams *__restrict__ Pp) {
     extern __shared__ __align__(128) char tsmem[];
     const SeriesParams &P = *Pp;
     if (P.state->done) return;
@@ -477,7 +477,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3, MK_W2 = 4 };
+// MK_W2 / MK_G2 / MK_P2 / MK_GH2: the two-node pass's tiles (stencil_tb.cuh)
+enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3, MK_W2 = 4, MK_G2 = 5, MK_P2 = 6, MK_GH2 = 7 };
 
 // TMA descriptor of a slab-shaped fp64 vector (x fastest); OOB reads are
 // zero-filled, which is the homogeneous Dirichlet ghost rule.
@@ -489,13 +490,13 @@ static int encode_map(CUtensorMap *m, const double *base, const es_stencil_desc 
     cuuint64_t dims[3], strides[2];
     cuuint32_t box[3], estr[3] = {1, 1, 1};
     cuuint32_t rank;
-    if (kind == MK_HALO) {  // one (ny, nx) plane, same box as the 3D W tiles
+    if (kind == MK_HALO || kind == MK_GH2) {  // one (ny, nx) plane, same box as the 3D W (g') tiles
         rank = 2;
         dims[0] = (cuuint64_t)d->nx;
         dims[1] = (cuuint64_t)d->ny;
         strides[0] = (cuuint64_t)d->nx * 8;
         box[0] = 68;
-        box[1] = 10;
+        box[1] = kind == MK_GH2 ? TB_GY : 10;
     } else if (dim2) {
         rank = 2;
         dims[0] = (cuuint64_t)d->nx;
@@ -510,8 +511,8 @@ static int encode_map(CUtensorMap *m, const double *base, const es_stencil_desc 
         dims[2] = (cuuint64_t)d->lz;
         strides[0] = (cuuint64_t)d->nx * 8;
         strides[1] = (cuuint64_t)d->nx * d->ny * 8;
-        box[0] = kind == MK_P ? 64 : kind == MK_W2 ? TB_WX : 68;  // MK_W2: two-point halo (two-node pass)
-        box[1] = kind == MK_P ? 8 : kind == MK_W2 ? TB_WY : 10;
+        box[0] = (kind == MK_P || kind == MK_P2) ? 64 : kind == MK_W2 ? TB_WX : 68;  // MK_W2: two-point halo
+        box[1] = kind == MK_P ? 8 : kind == MK_P2 ? TB_TY : kind == MK_W2 ? TB_WY : kind == MK_G2 ? TB_GY : 10;
         box[2] = 1;
     }
     const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double *>(base), dims, strides, box,
@@ -528,11 +529,12 @@ static int encode_w(CUtensorMap *wa, CUtensorMap *wb, const double *base, const 
 }
 
 // persistent grid: every resident CTA slot, at most one per item
-static void finish_tma_plan(StencilPlan &pl, const void *fn, size_t smem) {
+static void finish_tma_plan(StencilPlan &pl, const void *fn, size_t smem, int threads = TMA_THREADS) {
     pl.smem = smem;
+    pl.block = dim3((unsigned)threads, 1, 1);
     set_smem_attr(fn, smem);
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, TMA_THREADS, smem) != cudaSuccess || nb < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess || nb < 1) {
         cudaGetLastError();
         nb = 1;
     }
@@ -772,7 +774,7 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
         if (S.tb) {
             S.nf = gdiag ? pick_node_tb<true>(d->coeff_kind) : pick_node_tb<false>(d->coeff_kind);
             finish_tma_plan(S.lp, (const void *)S.nf,
-                            gdiag ? (size_t)TbLayout<true>::BYTES : (size_t)TbLayout<false>::BYTES);
+                            gdiag ? (size_t)TbLayout<true>::BYTES : (size_t)TbLayout<false>::BYTES, TB_THREADS);
         } else {
             S.nf = pick_node_tma(pl.dim2, d->coeff_kind, gdiag != nullptr);
             finish_tma_plan(S.lp, (const void *)S.nf, node_smem(pl.dim2, gdiag != nullptr, pl.chunk));
@@ -827,8 +829,9 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
             if (!rc) rc = encode_map(&maps.m[MAP_T_V], v, d, false, MK_W2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_0], hp.wbuf[0], d, false, MK_W2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_1], hp.wbuf[1], d, false, MK_W2);
-            if (!rc) rc = encode_map(&maps.m[MAP_T_G], gdiag, d, false, MK_W);
-            if (!rc) rc = encode_map(&maps.m[MAP_T_PV], v, d, false, MK_P);
+            if (!rc) rc = encode_map(&maps.m[MAP_T_G], gdiag, d, false, MK_G2);
+            if (!rc) rc = encode_map(&maps.m[MAP_T_PV], v, d, false, MK_P2);
+            if (!rc) rc = encode_map(&maps.m[MAP_T_P0], hp.pbuf[0], d, false, MK_P2);
             if (halos) {  // two-plane w halos by parity, g' boundary planes of the neighbours
                 es_stencil_desc d2 = *d;
                 d2.lz = 2;
@@ -836,8 +839,8 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
                 if (!rc) rc = encode_map(&maps.m[MAP_T_HLO1], halo_lo_1, &d2, false, MK_W2);
                 if (!rc) rc = encode_map(&maps.m[MAP_T_HHI0], halo_hi, &d2, false, MK_W2);
                 if (!rc) rc = encode_map(&maps.m[MAP_T_HHI1], halo_hi_1, &d2, false, MK_W2);
-                if (!rc) rc = encode_map(&maps.m[MAP_T_GLO], g_lo, d, false, MK_HALO);
-                if (!rc) rc = encode_map(&maps.m[MAP_T_GHI], g_hi, d, false, MK_HALO);
+                if (!rc) rc = encode_map(&maps.m[MAP_T_GLO], g_lo, d, false, MK_GH2);
+                if (!rc) rc = encode_map(&maps.m[MAP_T_GHI], g_hi, d, false, MK_GH2);
             }
         }
         if (rc) return rc;

@@ -29,10 +29,31 @@
 
 namespace es {
 
-constexpr int TB_WX = 72, TB_WY = 12;  // w_{k-1}: x0-4 .. x0+67, y0-2 .. y0+9
-constexpr int TB_EX = 68, TB_EY = 10;  // w_k window: x0-2 .. x0+65 (even start: pair loads), y0-1 .. y0+8
-constexpr int TB_PAIRS = TB_EX / 2 * TB_EY;  // 340 point pairs per window plane
-constexpr int TB_GX = 68, TB_GY = 10;  // g': x0-2 .. x0+65, y0-1 .. y0+8
+// tile: 64 x TB_TY points; warp group A (TB_AW warps), C (TB_CW warps, two
+// rows per thread), one producer warp.  64 x 8 with 4 + 4 warps runs two
+// CTAs per SM; 64 x 16 with 7 + 8 runs one CTA of 16 warps (128 registers).
+#ifndef TB_TY
+#define TB_TY 16
+#endif
+#if TB_TY == 8
+#define TB_AW_DEF 4
+#define TB_CW_DEF 4
+#define TB_MINB 2
+#else
+#define TB_AW_DEF 7
+#define TB_CW_DEF 8
+#define TB_MINB 1
+#endif
+constexpr int TB_AW = TB_AW_DEF, TB_CW = TB_CW_DEF;
+static_assert(TB_TY == 2 * TB_CW, "group C threads own two rows each");
+constexpr int TB_NA = 32 * TB_AW, TB_NC = 32 * TB_CW;
+constexpr int TB_THREADS = 32 * (TB_AW + TB_CW + 1);
+constexpr int TB_WX = 72, TB_WY = TB_TY + 4;  // w_{k-1}: x0-4 .. x0+67, y0-2 .. y0+TY+1
+constexpr int TB_EX = 68, TB_EY = TB_TY + 2;  // w_k window: x0-2 .. x0+65 (even start: pair loads), y0-1 .. y0+TY
+constexpr int TB_PAIRS = TB_EX / 2 * TB_EY;  // point pairs per window plane
+constexpr int TB_APT = (TB_PAIRS + TB_NA - 1) / TB_NA;  // window pairs per group-A thread
+static_assert(TB_APT == 3, "group A loop is written for three pairs per thread");
+constexpr int TB_GX = 68, TB_GY = TB_TY + 2;  // g': x0-2 .. x0+65, y0-1 .. y0+TY
 #ifndef TB_SV
 #define TB_SV 5  // w_k window planes in flight between the warp groups (>= 4: j-2 .. j+1)
 #endif
@@ -43,7 +64,11 @@ constexpr int TB_GX = 68, TB_GY = 10;  // g': x0-2 .. x0+65, y0-1 .. y0+8
 #define TB_SP 4
 #endif
 #ifndef TB_SW_GD
+#if TB_TY == 8
 #define TB_SW_GD 6
+#else
+#define TB_SW_GD 7
+#endif
 #endif
 #ifndef TB_SW_NG
 #define TB_SW_NG 9
@@ -51,12 +76,12 @@ constexpr int TB_GX = 68, TB_GY = 10;  // g': x0-2 .. x0+65, y0-1 .. y0+8
 
 template <bool GD>
 struct TbLayout {
-    // ring depths: two CTAs per SM (<= 113 KiB each); G slots are held until
-    // group C is done with the plane, so the G ring is the deeper one
+    // ring depths: two CTAs per SM (<= 113 KiB each) at 64 x 8; one CTA per
+    // SM (<= 226 KiB) at 64 x 16
     static constexpr int SW = GD ? TB_SW_GD : TB_SW_NG, SG = GD ? TB_SG : 0, SP = TB_SP;
     static constexpr int W_STAGE = (TB_WX * TB_WY * 8 + 127) & ~127;
     static constexpr int G_STAGE = (TB_GX * TB_GY * 8 + 127) & ~127;
-    static constexpr int P_STAGE = 64 * 8 * 8;
+    static constexpr int P_STAGE = 64 * TB_TY * 8;
     static constexpr int V_SLOT = TB_EX * TB_EY * 8;
     static constexpr int W_OFF = 0;
     static constexpr int G_OFF = W_OFF + SW * W_STAGE;
@@ -69,6 +94,39 @@ struct TbLayout {
     static constexpr int BYTES = VITEM_OFF + 16;
 };
 
+// Work items of the two-node pass: (z chunk, 64 x TB_TY tile), chunk-major.
+// Norm partials keep the one-node kernel's (chunk, 64 x 8 tile, row) layout.
+struct TbItems {
+    int tiles_x, ntiles8, ntiles, nchunks, chunk_len, L;
+};
+
+ES_DEV TbItems tb_items_of(const Geom &g, int chunk_len) {
+    TbItems it;
+    it.tiles_x = (int)((g.nx + 63) / 64);
+    it.ntiles8 = it.tiles_x * (int)((g.ny + 7) / 8);
+    it.ntiles = it.tiles_x * (int)((g.ny + TB_TY - 1) / TB_TY);
+    it.L = (int)g.lz;
+    it.chunk_len = chunk_len;
+    it.nchunks = (it.L + chunk_len - 1) / chunk_len;
+    return it;
+}
+
+struct TbItem {
+    int chunk, x0, y0, mb, me, tile8;  // tile8: one-node index of the 64 x 8 tile at row y0
+};
+
+ES_DEV TbItem tb_item_at(const TbItems &its, int i) {
+    TbItem r;
+    r.chunk = i / its.ntiles;
+    const int t = i % its.ntiles, tx = t % its.tiles_x, ty = t / its.tiles_x;
+    r.x0 = tx * 64;
+    r.y0 = ty * TB_TY;
+    r.mb = r.chunk * its.chunk_len;
+    r.me = min(its.L, r.mb + its.chunk_len);
+    r.tile8 = (r.y0 / 8) * its.tiles_x + tx;
+    return r;
+}
+
 struct TbMaps {
     const CUtensorMap *w, *g, *p;
     // peer-memory slabs: the neighbours' two w planes (this pass's parity) and g' planes, or null
@@ -76,7 +134,7 @@ struct TbMaps {
 };
 
 template <bool GD>
-ES_DEV void tb_produce(const Geom &g, const Items &its, const TbMaps &mp, char *smem, bool load_p,
+ES_DEV void tb_produce(const Geom &g, const TbItems &its, const TbMaps &mp, char *smem, bool load_p,
                        unsigned *work) {
     using Lt = TbLayout<GD>;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + Lt::BAR_OFF);
@@ -87,7 +145,7 @@ ES_DEV void tb_produce(const Geom &g, const Items &its, const TbMaps &mp, char *
     const int total = its.ntiles * its.nchunks;
     int i = work ? (int)atomicAdd(work, 1u) : (int)blockIdx.x;
     while (i < total) {
-        const Item it = item_at<true>(its, i);
+        const TbItem it = tb_item_at(its, i);
         int inext = -1;
         for (int t = it.mb - 2; t <= it.me + 1; ++t) {
             if (t == max(it.mb - 2, it.me - 3)) inext = work ? (int)atomicAdd(work, 1u) : i + (int)gridDim.x;
@@ -203,7 +261,7 @@ ES_DEV void warp_arrive(uint64_t *b) {
     if ((threadIdx.x & 31) == 0) mbar_arrive(b);
 }
 
-ES_DEV void a_group_sync() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+ES_DEV void a_group_sync() { asm volatile("bar.sync 2, %0;" ::"n"(TB_NA) : "memory"); }
 
 // slot / phase of a ring position
 template <int S>
@@ -242,20 +300,20 @@ ES_DEV double2 tb_fast_pair(const Geom &g, const double *Wm, const double *Wc, c
 }
 
 template <int COEFF, bool GD>
-ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const Items &its, char *smem) {
+ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const TbItems &its, char *smem) {
     using Lt = TbLayout<GD>;
     const TbBars B = tb_bars<GD>(smem);
     const volatile int *itemq = reinterpret_cast<const volatile int *>(smem + Lt::ITEMQ_OFF);
     volatile int *vitem = reinterpret_cast<volatile int *>(smem + Lt::VITEM_OFF);
     double *vwin = reinterpret_cast<double *>(smem + Lt::V_OFF);
-    const int a = threadIdx.x;  // 0..127
+    const int a = threadIdx.x;  // 0 .. TB_NA-1
     const bool neu = g.mode == ES_MODE_NEUMANN;
     const bool has_lo = g.halo_lo != nullptr, has_hi = g.halo_hi != nullptr;  // peer slabs below / above
     const double alpha = P->alpha, beta_k = sub(-P->shift, P->xi[k - 1]);
     int pey[3], pex[3];
 #pragma unroll
     for (int h = 0; h < 3; ++h) {
-        const int pr = a + 128 * h;
+        const int pr = a + TB_NA * h;
         pey[h] = pr < TB_PAIRS ? pr / (TB_EX / 2) : -1;
         pex[h] = 2 * (pr % (TB_EX / 2));
     }
@@ -278,7 +336,7 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const Items 
             warp_arrive(&B.vfull[vr.slot]);
             break;
         }
-        const Item it = item_at<true>(its, i);
+        const TbItem it = tb_item_at(its, i);
         bool fast[3];
 #pragma unroll
         for (int h = 0; h < 3; ++h) {
@@ -323,15 +381,15 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const Items 
                 if (neu && j == 0 && !has_lo) {  // the mirrored plane below the domain = w_k of plane 0
                     a_group_sync();
                     double *Vb = vslot(v_prev);
-                    for (int e = a; e < TB_EX * TB_EY; e += 128) Vb[e] = Vj[e];
+                    for (int e = a; e < TB_EX * TB_EY; e += TB_NA) Vb[e] = Vj[e];
                     arrive_prev = true;
                 }
             } else if (j >= 0) {  // plane L: zeros (Dirichlet) or the mirrored plane L-1 (Neumann)
                 if (neu) a_group_sync();
                 const double *Vs = vslot(v_prev);
-                for (int e = a; e < TB_EX * TB_EY; e += 128) Vj[e] = neu ? Vs[e] : 0.0;
+                for (int e = a; e < TB_EX * TB_EY; e += TB_NA) Vj[e] = neu ? Vs[e] : 0.0;
             } else if (!neu) {  // plane -1, Dirichlet
-                for (int e = a; e < TB_EX * TB_EY; e += 128) Vj[e] = 0.0;
+                for (int e = a; e < TB_EX * TB_EY; e += TB_NA) Vj[e] = 0.0;
             }
             warp_arrive(&B.wempty[rm.slot]);  // W(j-1): last read by A of plane j
             if constexpr (GD) {
@@ -353,12 +411,12 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const Items 
 }
 
 template <int COEFF, bool GD>
-ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, const Items &its, char *smem) {
+ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, const TbItems &its, char *smem) {
     using Lt = TbLayout<GD>;
     const TbBars B = tb_bars<GD>(smem);
     const volatile int *vitem = reinterpret_cast<const volatile int *>(smem + Lt::VITEM_OFF);
     const double *vwin = reinterpret_cast<const double *>(smem + Lt::V_OFF);
-    const int c = threadIdx.x - 128, cw = c >> 5, q = c & 31;  // rows cw and cw + 4, pair x0 + 2q
+    const int c = threadIdx.x - TB_NA, cw = c >> 5, q = c & 31;  // rows cw and cw + TB_CW, pair x0 + 2q
     const int64_t plane = g.nx * g.ny;
     const int pass = (k - 1) / 2;
     double *w1_dst = P->wbuf[pass & 1];
@@ -374,13 +432,13 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
         mbar_wait(&B.vfull[vr.slot], vr.phase);
         const int i = vitem[vr.slot];
         if (i < 0) break;
-        const Item it = item_at<true>(its, i);
+        const TbItem it = tb_item_at(its, i);
         const int64_t xa = it.x0 + 2 * q;
         bool act[2];
         int64_t ya[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            ya[h] = it.y0 + cw + 4 * h;
+            ya[h] = it.y0 + cw + TB_CW * h;
             act[h] = xa < g.nx && ya[h] < g.ny;
         }
         double acc_w0[2] = {0.0, 0.0}, acc_p0[2] = {0.0, 0.0}, acc_w1[2] = {0.0, 0.0}, acc_p1[2] = {0.0, 0.0};
@@ -398,7 +456,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     if (!act[h]) continue;
-                    const int r = cw + 4 * h;
+                    const int r = cw + TB_CW * h;
                     const double2 vk = *reinterpret_cast<const double2 *>(Vj + (r + 1) * TB_EX + 2 * q + 2);
                     const double2 po = *reinterpret_cast<const double2 *>(Pc + r * 64 + 2 * q);
                     const double p0 = k == 1 ? mul(pscale, po.x) : po.x, p1 = k == 1 ? mul(pscale, po.y) : po.y;
@@ -426,7 +484,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         if (!act[h]) continue;
-                        const int r = cw + 4 * h;
+                        const int r = cw + TB_CW * h;
                         const int o = (r + 1) * TB_EX + 2 * q + 2;
                         // pair loads (16-byte aligned: o is even), as in tb_fast_pair
                         const double2 cc = *reinterpret_cast<const double2 *>(Vc + o);
@@ -484,8 +542,10 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
         for (int h = 0; h < 2; ++h) {
             const double w0 = warp_sum(acc_w0[h]), p0 = warp_sum(acc_p0[h]);
             const double w1 = warp_sum(acc_w1[h]), p1 = warp_sum(acc_p1[h]);
-            if (q == 0) {
-                const int64_t e = ((int64_t)it.chunk * its.ntiles + it.tile) * TMA_CONSUMER_WARPS + cw + 4 * h;
+            const int r = cw + TB_CW * h;
+            if (q == 0 && it.y0 + (r & ~7) < g.ny) {  // the 64 x 8 tile of row r exists
+                const int64_t e =
+                    ((int64_t)it.chunk * its.ntiles8 + it.tile8 + (r >> 3) * its.tiles_x) * TMA_CONSUMER_WARPS + (r & 7);
                 double *d0p = P->part + e * 2;
                 d0p[0] = w0;
                 d0p[1] = p0;
@@ -501,12 +561,12 @@ template <int COEFF, bool GD>
 ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
     using Lt = TbLayout<GD>;
     const Geom &g = P->g;
-    const Items its = items_of<true>(g, P->chunk_len);
+    const TbItems its = tb_items_of(g, P->chunk_len);
     const TmaMaps &M = *static_cast<const TmaMaps *>(P->maps);
     const int pass = (k - 1) / 2;
     // W: w_{k-1} (v on the first pass); P: p_{k-1}, or v on the first pass (p_0 = dd_0 v)
     TbMaps mp{&M.m[pass == 0 ? MAP_T_V : (pass & 1) ? MAP_T_0 : MAP_T_1], &M.m[MAP_T_G],
-              &M.m[pass == 0 ? MAP_T_PV : MAP_P_0]};
+              &M.m[pass == 0 ? MAP_T_PV : MAP_T_P0]};
     if (g.halo_lo) mp.hlo = &M.m[(pass & 1) ? MAP_T_HLO1 : MAP_T_HLO0];  // pass p reads halo parity p & 1
     if (g.halo_hi) mp.hhi = &M.m[(pass & 1) ? MAP_T_HHI1 : MAP_T_HHI0];
     if (GD && g.halo_lo) mp.glo = &M.m[MAP_T_GLO];
@@ -515,25 +575,25 @@ ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
         const TbBars B = tb_bars<GD>(smem);
         for (int s = 0; s < Lt::SW; ++s) {
             mbar_init(&B.wfull[s], 1);
-            mbar_init(&B.wempty[s], 4);  // A group
+            mbar_init(&B.wempty[s], TB_AW);  // A group
         }
         for (int s = 0; s < Lt::SG; ++s) {
             mbar_init(&B.gfull[s], 1);
-            mbar_init(&B.gempty[s], 8);  // A and C groups
+            mbar_init(&B.gempty[s], TB_AW + TB_CW);  // A and C groups
         }
         for (int s = 0; s < Lt::SP; ++s) {
             mbar_init(&B.pfull[s], 1);
-            mbar_init(&B.pempty[s], 4);  // C group
+            mbar_init(&B.pempty[s], TB_CW);  // C group
         }
         for (int s = 0; s < TB_SV; ++s) {
-            mbar_init(&B.vfull[s], 4);
-            mbar_init(&B.vempty[s], 4);
+            mbar_init(&B.vfull[s], TB_AW);
+            mbar_init(&B.vempty[s], TB_CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const int warp = threadIdx.x / 32;
-    if (warp == TMA_CONSUMER_WARPS) {
+    if (warp == TB_AW + TB_CW) {
         if ((threadIdx.x & 31) == 0) {
             tma_acquire(mp.w);
             if (GD) tma_acquire(mp.g);
@@ -542,7 +602,7 @@ ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
                 if (h) tma_acquire(h);
             tb_produce<GD>(g, its, mp, smem, true, P->work);
         }
-    } else if (warp < 4) {
+    } else if (warp < TB_AW) {
         tb_group_a<COEFF, GD>(g, P, k, its, smem);
     } else {
         tb_group_c<COEFF, GD>(g, P, k, two, its, smem);
