@@ -91,7 +91,7 @@ struct TbLayout {
     static constexpr int NBAR = 2 * (SW + SG + SP + TB_SV);
     static constexpr int ITEMQ_OFF = BAR_OFF + NBAR * 8;
     static constexpr int VITEM_OFF = ITEMQ_OFF + ((SW * 4 + 15) & ~15);
-    static constexpr int BYTES = VITEM_OFF + 16;
+    static constexpr int BYTES = VITEM_OFF + ((TB_SV * 4 + 15) & ~15);  // one item slot per V slot
 };
 
 // Work items of the two-node pass: (z chunk, 64 x TB_TY tile), chunk-major.
