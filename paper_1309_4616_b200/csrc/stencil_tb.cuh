@@ -471,51 +471,49 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                 warp_arrive(&B.pempty[pr.slot]);
                 pr.next();
             }
-            // ---- C: w_{k+1}, p_{k+1} of plane j-1 (+ node k+1 norms)
+            // ---- C: w_{k+1}, p_{k+1} of plane j-1 (+ node k+1 norms); both rows side by side
             const int jc = j - 1;
-            if (jc >= it.mb && jc < it.me) {
-                if (two) {
-                    const double *Vm = vslot(s2), *Vc = vslot(s1), *Vp = Vj;
-                    const double *Gc = nullptr;
+            if (two && jc >= it.mb && jc < it.me) {
+                const double *Vm = vslot(s2), *Vc = vslot(s1), *Vp = Vj;
+                const double *Gc = nullptr;
+                if constexpr (GD) {
+                    mbar_wait(&B.gfull[gr.slot], gr.phase);  // complete already; orders the TMA bytes for C
+                    Gc = reinterpret_cast<const double *>(smem + Lt::G_OFF + gr.slot * Lt::G_STAGE);
+                }
+                double wn[4], pn[4];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int r = cw + TB_CW * h;
+                    const int o = (r + 1) * TB_EX + 2 * q + 2;
+                    const double2 cc = *reinterpret_cast<const double2 *>(Vc + o);
+                    const double2 ym = *reinterpret_cast<const double2 *>(Vc + o - TB_EX);
+                    const double2 yp = *reinterpret_cast<const double2 *>(Vc + o + TB_EX);
+                    const double2 zm = *reinterpret_cast<const double2 *>(Vm + o);
+                    const double2 zp = *reinterpret_cast<const double2 *>(Vp + o);
+                    double l0 = lap7(cc.x, Vc[o - 1], cc.y, ym.x, yp.x, zm.x, zp.x, g.wx, g.wy, g.wz);
+                    double l1 = lap7(cc.y, cc.x, Vc[o + 2], ym.y, yp.y, zm.y, zp.y, g.wx, g.wy, g.wz);
+                    if constexpr (COEFF != ES_COEFF_NONE) {
+                        l0 = mul(tb_coeff<COEFF>(g, xa, ya[h], jc), l0);
+                        l1 = mul(tb_coeff<COEFF>(g, xa + 1, ya[h], jc), l1);
+                    }
                     if constexpr (GD) {
-                        mbar_wait(&B.gfull[gr.slot], gr.phase);  // complete already; orders the TMA bytes for C
-                        Gc = reinterpret_cast<const double *>(smem + Lt::G_OFF + gr.slot * Lt::G_STAGE);
+                        const double2 gv = *reinterpret_cast<const double2 *>(Gc + (r + 1) * TB_GX + 2 * q + 2);
+                        l0 = sub(l0, mul(gv.x, cc.x));
+                        l1 = sub(l1, mul(gv.y, cc.y));
                     }
+                    wn[2 * h] = add(mul(alpha, l0), mul(beta_k1, cc.x));
+                    wn[2 * h + 1] = add(mul(alpha, l1), mul(beta_k1, cc.y));
+                    pn[2 * h] = add(pk_prev[2 * h], mul(dk1, wn[2 * h]));
+                    pn[2 * h + 1] = add(pk_prev[2 * h + 1], mul(dk1, wn[2 * h + 1]));
+                }
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (!act[h]) continue;
-                        const int r = cw + TB_CW * h;
-                        const int o = (r + 1) * TB_EX + 2 * q + 2;
-                        // pair loads (16-byte aligned: o is even), as in tb_fast_pair
-                        const double2 cc = *reinterpret_cast<const double2 *>(Vc + o);
-                        const double2 ym = *reinterpret_cast<const double2 *>(Vc + o - TB_EX);
-                        const double2 yp = *reinterpret_cast<const double2 *>(Vc + o + TB_EX);
-                        const double2 zm = *reinterpret_cast<const double2 *>(Vm + o);
-                        const double2 zp = *reinterpret_cast<const double2 *>(Vp + o);
-                        double lap[2] = {lap7(cc.x, Vc[o - 1], cc.y, ym.x, yp.x, zm.x, zp.x, g.wx, g.wy, g.wz),
-                                         lap7(cc.y, cc.x, Vc[o + 2], ym.y, yp.y, zm.y, zp.y, g.wx, g.wy, g.wz)};
-                        const double cv[2] = {cc.x, cc.y};
-                        double gv[2] = {0.0, 0.0};
-                        if constexpr (GD) {
-                            const double2 g2 = *reinterpret_cast<const double2 *>(Gc + (r + 1) * TB_GX + 2 * q + 2);
-                            gv[0] = g2.x;
-                            gv[1] = g2.y;
-                        }
-                        double wn[2], pn[2];
-#pragma unroll
-                        for (int jj = 0; jj < 2; ++jj) {
-                            if constexpr (COEFF != ES_COEFF_NONE)
-                                lap[jj] = mul(tb_coeff<COEFF>(g, xa + jj, ya[h], jc), lap[jj]);
-                            if constexpr (GD) lap[jj] = sub(lap[jj], mul(gv[jj], cv[jj]));
-                            wn[jj] = add(mul(alpha, lap[jj]), mul(beta_k1, cv[jj]));
-                            pn[jj] = add(pk_prev[2 * h + jj], mul(dk1, wn[jj]));
-                        }
-                        const int64_t off = jc * plane + ya[h] * g.nx + xa;
-                        *reinterpret_cast<double2 *>(w1_dst + off) = make_double2(wn[0], wn[1]);
-                        *reinterpret_cast<double2 *>(pk1_dst + off) = make_double2(pn[0], pn[1]);
-                        acc_w1[h] = add(acc_w1[h], add(mul(wn[0], wn[0]), mul(wn[1], wn[1])));
-                        acc_p1[h] = add(acc_p1[h], add(mul(pn[0], pn[0]), mul(pn[1], pn[1])));
-                    }
+                for (int h = 0; h < 2; ++h) {
+                    if (!act[h]) continue;
+                    const int64_t off = jc * plane + ya[h] * g.nx + xa;
+                    *reinterpret_cast<double2 *>(w1_dst + off) = make_double2(wn[2 * h], wn[2 * h + 1]);
+                    *reinterpret_cast<double2 *>(pk1_dst + off) = make_double2(pn[2 * h], pn[2 * h + 1]);
+                    acc_w1[h] = add(acc_w1[h], add(mul(wn[2 * h], wn[2 * h]), mul(wn[2 * h + 1], wn[2 * h + 1])));
+                    acc_p1[h] = add(acc_p1[h], add(mul(pn[2 * h], pn[2 * h]), mul(pn[2 * h + 1], pn[2 * h + 1])));
                 }
             }
             if constexpr (GD) {
