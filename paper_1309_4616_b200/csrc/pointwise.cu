@@ -22,7 +22,7 @@ __global__ void k_combustion(const double *__restrict__ u, double *__restrict__ 
     ES_GRID_STRIDE(i, n) {
         const double x = u[i];
         if (x <= 0.0) atomicMin(bad, (unsigned long long)i);
-        const double r = div(1.0, x);
+        const double r = __drcp_rn(x);  // = div(1.0, x), correctly rounded either way
         const double t = mul(20.0, sub(1.0, r));
         out[i] = mul(mul(0.25, sub(2.0, x)), exp(t));
     }
@@ -34,7 +34,7 @@ __global__ void k_combustion_jac(const double *__restrict__ u, double *__restric
     unsigned long long lo = ~0ull, hi = 0ull;
     ES_GRID_STRIDE(i, n) {
         const double x = u[i];
-        const double r = div(1.0, x);
+        const double r = __drcp_rn(x);  // = div(1.0, x), correctly rounded either way
         const double e = exp(mul(20.0, sub(1.0, r)));
         const double q = mul(mul(5.0, sub(2.0, x)), mul(r, r));
         const double gp = mul(e, sub(q, 0.25));

@@ -383,7 +383,7 @@ ES_DEV void tma_consume(const Geom &g, const Pass &ps, const Items &its, char *s
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         const double x = cc[j];
-                        const double rr = div(1.0, x);
+                        const double rr = __drcp_rn(x);  // = div(1.0, x), correctly rounded either way
                         const double e = exp(mul(20.0, sub(1.0, rr)));
                         const double gval = mul(mul(0.25, sub(2.0, x)), e);
                         const double q = mul(mul(5.0, sub(2.0, x)), mul(rr, rr));
