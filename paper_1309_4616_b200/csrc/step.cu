@@ -42,7 +42,7 @@ int fork_resources(Fork *&f) {
         cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&f->join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&f->t0) != cudaSuccess || cudaEventCreate(&f->t1) != cudaSuccess ||
-        cudaMalloc(&f->bad, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&f->bad, 2 * sizeof(unsigned long long)) != cudaSuccess ||  // k_fill_u64 writes two words
         cudaMallocHost(&f->bad_host, sizeof(unsigned long long)) != cudaSuccess)
         return check_launch("step resources");
     f->device = dev;
