@@ -771,6 +771,27 @@ def test_p2p_slab_series_rosenbrock_diag_and_neumann(two):
     assert np.concatenate([o[2] for o in outs]).tobytes() == np.asarray(ref).tobytes()
 
 
+@pytest.mark.parametrize("bc", ["homogeneous", "neumann"])
+def test_p2p_two_node_thin_slabs(bc):
+    """Two-node peer slabs of 2 and 3 planes (the two-plane halos are a whole
+    neighbour slab), ragged x/y tiles, with a g' diagonal: bitwise = one domain."""
+    g = es.Grid3D(70, 21, 9)
+    op = es.StencilOperator(g, BCS[bc])
+    bounds = [(0, 2), (2, 5), (5, 7), (7, 9)]
+    ranks, keep = _p2p_ranks(op, bounds, two=True)
+    it = es.make_interpolant(es.gershgorin_interval(op).widened(20.0), "phi1", -5e-4, 31, 1e-8)
+    v = np.random.default_rng(8).standard_normal(g.n)
+    gd = np.random.default_rng(9).random(g.n) * 10.0
+    for tol, gdiag in ((0.0, gd), (1e-9, None)):
+        ref, mv = es.newton_apply(op if gdiag is None else es.RosenbrockOperator(op, torch.from_numpy(gdiag).cuda()),
+                                  it, v, tol)
+        rounds = 0 if tol == 0.0 else (31 + 1) // 2 + 1
+        outs = _p2p_run(op, ranks, it, v, tol, rounds, gdiag=gdiag)
+        assert [o[0] for o in outs] == [0] * 4
+        assert [o[1] for o in outs] == [mv] * 4
+        assert np.concatenate([o[2] for o in outs]).tobytes() == np.asarray(ref).tobytes()
+
+
 def test_p2p_missing_peer_times_out_instead_of_hanging():
     from paper_1309_4616_b200 import _lib
 
