@@ -606,6 +606,8 @@ def _p2p_ranks(op, bounds, timeout_ns=5_000_000_000, two=False):
 
     from paper_1309_4616_b200 import _lib
 
+    if two and os.environ.get("ES_TB", "1") == "0":
+        pytest.skip("two-node passes disabled (ES_TB=0)")
     lib = _lib.load()
     g = op.grid
     plane = g.nx * g.ny
