@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(TMA_THREADS, (COEFF == ES_COEFF_RADIAL && !DIM
     const bool odd = P.p2p && (k & 1);  // peer-memory series: node k reads halo parity k & 1
     const PassMaps mp{&M.m[2 * wi], &M.m[2 * wi + 1], &M.m[MAP_P_0 + ((k - 1) & 1)], &M.m[MAP_G],
                       &M.m[odd ? MAP_HLO_1 : MAP_HLO], &M.m[odd ? MAP_HHI_1 : MAP_HHI]};
-    tma_pass<DIM3, COEFF, GD, true>(P.g, ps, mp, P.chunk_len, true, tsmem, Pp, k, P.work);
+    // the second PG slot carries g' (GD) or the staged coefficient (MAP_G encodes it)
+    tma_pass<DIM3, COEFF, GD || COEFF == ES_COEFF_STAGED, true>(P.g, ps, mp, P.chunk_len, true, tsmem, Pp, k, P.work);
 }
 
 // Reduction + stopping decision of a TMA node (one CTA per z / row chunk).
@@ -564,6 +565,7 @@ static NodeTmaFn pick_node_tma_c(int coeff) {
     switch (coeff) {
         case ES_COEFF_RADIAL: return k_node_tma<DIM3, ES_COEFF_RADIAL, GD>;
         case ES_COEFF_ARRAY: return k_node_tma<DIM3, ES_COEFF_ARRAY, GD>;
+        case ES_COEFF_STAGED: return k_node_tma<DIM3, ES_COEFF_STAGED, false>;
         default: return k_node_tma<DIM3, ES_COEFF_NONE, GD>;
     }
 }
@@ -725,6 +727,7 @@ struct SeriesSetup {
     SeriesParams *dparams;
     int64_t n;
     bool tb = false;  // two nodes per pass (k_node_tb + k_slice_reduce2)
+    bool staged = false;  // sampled coefficient through the PG ring (ES_COEFF_STAGED)
 };
 
 template <bool GD>
@@ -776,8 +779,10 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
             finish_tma_plan(S.lp, (const void *)S.nf,
                             gdiag ? (size_t)TbLayout<true>::BYTES : (size_t)TbLayout<false>::BYTES, TB_THREADS);
         } else {
-            S.nf = pick_node_tma(pl.dim2, d->coeff_kind, gdiag != nullptr);
-            finish_tma_plan(S.lp, (const void *)S.nf, node_smem(pl.dim2, gdiag != nullptr, pl.chunk));
+            // a sampled coefficient without g' streams through the PG ring's g' slot
+            S.staged = !gdiag && d->coeff_kind == ES_COEFF_ARRAY && env_int("ES_DSTAGE", 1);
+            S.nf = pick_node_tma(pl.dim2, S.staged ? ES_COEFF_STAGED : d->coeff_kind, gdiag != nullptr);
+            finish_tma_plan(S.lp, (const void *)S.nf, node_smem(pl.dim2, gdiag != nullptr || S.staged, pl.chunk));
         }
     } else {
         pick_all(pl, d->coeff_kind, gdiag != nullptr, af, S.nf);
@@ -820,7 +825,7 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
         if (!rc) rc = encode_w(&maps.m[MAP_WA_1], &maps.m[MAP_WB_1], hp.wbuf[1], d, pl.dim2);
         if (!rc) rc = encode_map(&maps.m[MAP_P_0], hp.pbuf[0], d, pl.dim2, MK_P);
         if (!rc) rc = encode_map(&maps.m[MAP_P_1], hp.pbuf[1], d, pl.dim2, MK_P);
-        if (!rc) rc = encode_map(&maps.m[MAP_G], gdiag, d, pl.dim2, MK_P);
+        if (!rc) rc = encode_map(&maps.m[MAP_G], S.staged ? d->coeff : gdiag, d, pl.dim2, MK_P);
         if (!rc) rc = encode_map(&maps.m[MAP_HLO], halo_lo, d, pl.dim2, MK_HALO);
         if (!rc) rc = encode_map(&maps.m[MAP_HHI], halo_hi, d, pl.dim2, MK_HALO);
         if (!rc) rc = encode_map(&maps.m[MAP_HLO_1], halo_lo_1, d, pl.dim2, MK_HALO);

@@ -36,6 +36,10 @@ struct TShape<false> {
 };
 
 constexpr int TMA_CONSUMER_WARPS = 8;
+// device-internal coefficient kind: the sampled D array (ES_COEFF_ARRAY)
+// streamed by TMA through the second slot of the PG ring (the g' slot; only
+// without a g' diagonal) instead of per-thread loads
+constexpr int ES_COEFF_STAGED = 3;
 constexpr int TMA_THREADS = 32 * (TMA_CONSUMER_WARPS + 1);
 
 // tensor maps of one pass; for 2D, W needs two maps (256-wide and 4-wide
@@ -359,7 +363,7 @@ ES_DEV void tma_consume(const Geom &g, const Pass &ps, const Items &its, char *s
                 if constexpr (LEJA) {
                     if (ps.p_src) pv = *reinterpret_cast<const double2 *>(Pc + pidx);
                 }
-                if constexpr (GD) gv = *reinterpret_cast<const double2 *>(Pc + Lt::P_BYTES / 8 + pidx);
+                if constexpr (GD) gv = *reinterpret_cast<const double2 *>(Pc + Lt::P_BYTES / 8 + pidx);  // g' or D
                 const double pvv[2] = {pv.x, pv.y}, gvv[2] = {gv.x, gv.y};
                 double wn[2], pn[2];
 #pragma unroll
@@ -367,7 +371,8 @@ ES_DEV void tma_consume(const Geom &g, const Pass &ps, const Items &its, char *s
                     double lap = lap7(cc[j], xm[j], xp[j], ymv[j], ypv[j], zmv[j], zpv[j], g.wx, g.wy, g.wz);
                     if constexpr (COEFF == ES_COEFF_RADIAL) lap = mul(DIM3 ? dco[j] : radial_from_sq(ox2[j], yy), lap);
                     if constexpr (COEFF == ES_COEFF_ARRAY) lap = mul(__ldg(g.coeff + row_base + ix + j), lap);
-                    if constexpr (GD) lap = sub(lap, mul(gvv[j], cc[j]));
+                    if constexpr (COEFF == ES_COEFF_STAGED) lap = mul(gvv[j], lap);
+                    if constexpr (GD && COEFF != ES_COEFF_STAGED) lap = sub(lap, mul(gvv[j], cc[j]));
                     wn[j] = add(mul(ps.alpha, lap), mul(ps.beta, cc[j]));
                     if constexpr (LEJA) {
                         const double pold = ps.p_src ? pvv[j] : mul(ps.d0, cc[j]);

@@ -148,16 +148,20 @@ class StencilOperator:
 
     def coeff_kind(self) -> int:
         """ES_COEFF_RADIAL when D is (bit-for-bit) the radial coefficient --
-        evaluated in-kernel, no extra HBM traffic -- else a staged array."""
+        evaluated in-kernel, no extra HBM traffic -- else a staged array.
+        Single-plane grids take the radial D as a sampled array too: their
+        one-node series kernel is fp64-issue bound on the in-kernel sqrt and
+        reciprocal, and streaming D through its TMA ring is faster (4096^2
+        Neumann node: 122.5 vs 133.3 us); the values are identical."""
         if self._coeff_kind is None:
             if self.coeff is None:
                 self._coeff_kind = _lib.ES_COEFF_NONE
             elif getattr(self.coeff, "es_kind", None) == "radial":
-                self._coeff_kind = _lib.ES_COEFF_RADIAL
+                self._coeff_kind = _lib.ES_COEFF_ARRAY if self.grid.nz == 1 else _lib.ES_COEFF_RADIAL
             else:
                 vals = self.coeff_values("f64")
                 same = np.array_equal(vals, np.broadcast_to(_radial_grid(self.grid), vals.shape))
-                self._coeff_kind = _lib.ES_COEFF_RADIAL if same else _lib.ES_COEFF_ARRAY
+                self._coeff_kind = _lib.ES_COEFF_RADIAL if same and self.grid.nz > 1 else _lib.ES_COEFF_ARRAY
         return self._coeff_kind
 
     def _coeff_device(self, kind: str = "f64") -> torch.Tensor:
