@@ -105,8 +105,10 @@ int es_combustion_pointwise(const double *u, double *out, int64_t n, int64_t *fi
 
 /* Fused Newton-Leja series on a stencil slab: p_out = sum_k dd_k w_k with
  * w_k = (alpha A + beta_k I) w_{k-1}, beta_k = -shift - xi[k-1], w_0 = v,
- * ONE pass over HBM per node and the stopping test on the device
- * (matfunc.py:271-318).  gdiag (nullable) turns A into the build-defined
+ * one pass over HBM per node -- per TWO nodes on 3D Dirichlet / Neumann
+ * grids (ES_TB, default on) -- and the stopping test on the device
+ * (matfunc.py:271-318); results and matvec counts do not depend on the
+ * pass structure.  gdiag (nullable) turns A into the build-defined
  * Rosenbrock operator A - diag(gdiag).  dd, xi are device arrays of ndd
  * values.  Blocks until the series finished (one host read-back);
  * returns ES_ERR_NOT_CONVERGED when tol > 0 and the nodes ran out. */
