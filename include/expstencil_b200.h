@@ -149,6 +149,23 @@ int es_csr_fused_rows_z(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr,
                         const double *x, double *y, double alpha_re, double alpha_im,
                         double beta_re, double beta_im, int32_t use_beta, void *stream);
 
+/* Every dtype combination of the kernel module's csr_fused_rows
+ * (_core.pyx:281-315): col_bytes 4 (int32) or 8 (int64 -- the reference
+ * widens columns past 2^31-1, sparse.py:37-39); (vals_kind, x_kind) one of
+ * (F64, F64), (F32, F32), (F64, C128), (C128, C128); anything else returns
+ * ES_ERR_TYPE (the core's TypeError).  Sums in storage order in the data's
+ * precision; alpha / beta complex for C128 x (imaginary parts ignored for
+ * real x, rounded to float for F32).  int32 f64 / complex route to the same
+ * kernels as es_csr_fused_rows / es_csr_fused_rows_z. */
+#define ES_ERR_TYPE 6
+#define ES_KIND_F32 0
+#define ES_KIND_F64 1
+#define ES_KIND_C128 2
+int es_csr_fused_rows_ex(int64_t row_lo, int64_t row_hi, const int64_t *row_ptr, const void *col_idx,
+                         int32_t col_bytes, const void *vals, int32_t vals_kind, const void *x, void *y,
+                         int32_t x_kind, double alpha_re, double alpha_im, double beta_re, double beta_im,
+                         int32_t use_beta, void *stream);
+
 /* Complex Newton-Leja series: p = sum_k dd_k w_k with complex dd (ndd
  * interleaved values), w_k = (alpha A + beta_k) w_{k-1}, complex alpha (the
  * reference's op_alpha: 1/gamma, or -1j/gamma on an imaginary-axis interval),

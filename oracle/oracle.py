@@ -445,15 +445,19 @@ def combustion_jac(u: np.ndarray) -> np.ndarray:
 
 
 def expeuler_step(spec: StencilSpec, u: np.ndarray, h: float, tol: float, max_degree=150,
-                  interval=None, nonlinear=True):
-    """integrator._StepWorkspace.step (integrator.py:177-189) without rescue."""
+                  interval=None, nonlinear=True, source=None):
+    """integrator._StepWorkspace.step (integrator.py:177-189) without rescue.
+    ``source`` is the affine-split boundary vector b: the forcing is g(u) - b,
+    or -b for a linear problem (SemilinearProblem.forcing, integrator.py:104-123)."""
     a, b = interval if interval is not None else spec.gershgorin()
     ie = interpolant(a, b, "exp", -h, max_degree)
     ip = interpolant(a, b, "phi1", -h, max_degree)
     y, m1 = newton_stencil(spec, ie, u, tol)
-    if not nonlinear:
+    g = combustion(u) if nonlinear else None
+    if source is not None:
+        g = -source if g is None else g - source
+    if g is None:
         return y, (m1, 0)
-    g = combustion(u)
     z, m2 = newton_stencil(spec, ip, g, tol)
     out = np.empty_like(u)
     lib().orc_axpy_step(_ptr(y), _ptr(np.ascontiguousarray(z)), float(h), _ptr(out), u.size)
@@ -485,3 +489,24 @@ def rosenbrock_step(spec: StencilSpec, u: np.ndarray, h: float, tol: float, max_
     out = np.empty_like(u)
     lib().orc_axpy_step(_ptr(u), _ptr(np.ascontiguousarray(z)), float(h), _ptr(out), u.size)
     return out, m
+
+
+def integrate(spec: StencilSpec, u0: np.ndarray, h: float, t_end: float, tol: float, max_degree=150,
+              nonlinear=True, source=None):
+    """integrator.integrate (integrator.py:209-239) without rescue: exponential
+    Euler to t_end, the last step shortened to land on t_end exactly.
+    Returns (u, observer records [(step, t, matvecs, max|u|)])."""
+    u = np.array(u0, dtype=np.float64, copy=True)
+    n_steps = max(1, math.ceil(t_end / h - 1e-12))
+    iv = spec.gershgorin()
+    t, obs = 0.0, []
+    for k in range(n_steps):
+        last = k == n_steps - 1
+        h_k = t_end - (n_steps - 1) * h if last else h
+        if not (last and abs(h_k - h) > 1e-15 * h):
+            h_k = h
+        u, (m1, m2) = expeuler_step(spec, u, h_k, tol, max_degree, interval=iv, nonlinear=nonlinear,
+                                    source=source)
+        t = t_end if last else t + h
+        obs.append((k + 1, t, m1 + m2, float(np.max(np.abs(u)))))
+    return u, obs

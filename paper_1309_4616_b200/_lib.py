@@ -16,7 +16,8 @@ from .errors import ConvergenceError, DomainError, ExpStencilError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libexpstencil_b200.so")
 
-ES_OK, ES_ERR_ARG, ES_ERR_NOT_CONVERGED, ES_ERR_DOMAIN, ES_ERR_CUDA, ES_ERR_RANGE = 0, 1, 2, 3, 4, 5
+ES_OK, ES_ERR_ARG, ES_ERR_NOT_CONVERGED, ES_ERR_DOMAIN, ES_ERR_CUDA, ES_ERR_RANGE, ES_ERR_TYPE = 0, 1, 2, 3, 4, 5, 6
+ES_KIND_F32, ES_KIND_F64, ES_KIND_C128 = 0, 1, 2
 ES_NONLIN_NONE, ES_NONLIN_COMBUSTION = 0, 1
 ES_MODE_ZERO, ES_MODE_PERIODIC, ES_MODE_FACES, ES_MODE_NEUMANN = 0, 1, 2, 3
 ES_COEFF_NONE, ES_COEFF_RADIAL, ES_COEFF_ARRAY = 0, 1, 2
@@ -33,7 +34,7 @@ EXPORTS = (
     "es_leja_csr_dist_node", "es_leja_csr_dist_end", "es_csr_fused_rows_z", "es_leja_csr_z_workspace_bytes",
     "es_leja_csr_z", "es_leja_csr_z_async", "es_leja_stencil_nslices", "es_leja_p2p", "es_ipc_handle",
     "es_ipc_open", "es_ipc_close", "es_leja_csr_nslices", "es_leja_csr_p2p", "es_stencil_fused_slab_f32",
-    "es_combustion_pointwise_f32", "es_expeuler_step", "es_exprb_step", "es_exprb_finish",
+    "es_combustion_pointwise_f32", "es_expeuler_step", "es_exprb_step", "es_exprb_finish", "es_csr_fused_rows_ex",
 )
 
 
@@ -122,6 +123,7 @@ def _declare(lib):
                                    ctypes.c_int),
         "es_leja_csr_dist_source": ([vp, i32, P(vp)], ctypes.c_int),
         "es_csr_fused_rows_z": ([i64, i64, vp, vp, vp, i32, vp, vp, d, d, d, d, i32, vp], ctypes.c_int),
+        "es_csr_fused_rows_ex": ([i64, i64, vp, vp, i32, vp, i32, vp, vp, i32, d, d, d, d, i32, vp], ctypes.c_int),
         "es_leja_csr_z_workspace_bytes": ([i64], sz),
         "es_leja_stencil_nslices": ([P(StencilDesc), P(i32)], ctypes.c_int),
         "es_leja_p2p": ([P(StencilDesc), P(P2PDesc), vp, vp, vp, vp, i32, d, d, d, vp, vp, sz, vp], ctypes.c_int),
@@ -187,6 +189,8 @@ def check(rc: int, what: str = "") -> None:
         msg = f"{what}: {msg}"
     if rc == ES_ERR_ARG:
         raise ValueError(msg)
+    if rc == ES_ERR_TYPE:
+        raise TypeError(msg)
     if rc == ES_ERR_DOMAIN:
         raise DomainError(msg)
     if rc == ES_ERR_NOT_CONVERGED:

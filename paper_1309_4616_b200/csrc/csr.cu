@@ -487,9 +487,7 @@ int run_csr_series(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
 //              which on this build is (fma(a.r, b.r, -(a.i b.i)),
 //              fma(a.r, b.i, a.i b.r)) (pinned by the oracle tests).
 
-ES_DEV double2 cmul_c(double ar, double ai, double br, double bi) {
-    return make_double2(sub(mul(ar, br), mul(ai, bi)), add(mul(ar, bi), mul(ai, br)));
-}
+// cmul_c lives in es_common.cuh (shared with csr_generic.cu).
 ES_DEV double2 cmul_np(double ar, double ai, double br, double bi) {
     return make_double2(__fma_rn(ar, br, -mul(ai, bi)), __fma_rn(ar, bi, mul(ai, br)));
 }

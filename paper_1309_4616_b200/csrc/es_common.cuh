@@ -35,6 +35,12 @@ ES_DEV double lap7(double c, double xm, double xp, double ym, double yp, double 
     return add(add(sx, sy), sz);
 }
 
+// The compiled core's C99 `double complex` product under -ffp-contract=off
+// (_core.pyx:263-278; real operands promoted to (v, 0)).
+ES_DEV double2 cmul_c(double ar, double ai, double br, double bi) {
+    return make_double2(sub(mul(ar, br), mul(ai, bi)), add(mul(ar, bi), mul(ai, br)));
+}
+
 // D(x, y) = 1/sqrt((1 + x*x) + y*y) with x = (ix+1)/(nx+1) (grid.py:80-83,
 // bench.py:40-41): correctly rounded div/sqrt reproduce numpy's sampling.
 ES_DEV double axis_coord(int64_t i, int64_t n) { return div((double)(i + 1), (double)(n + 1)); }

@@ -424,7 +424,82 @@ def f32_cases():
     save("f32", **out)
 
 
+def c1_trajectory_case():
+    """BASELINE config 1 at full size: 256x256 homogeneous Dirichlet,
+    combustion, exponential Euler h=1e-4, tol=1e-4, 10 steps through
+    integrate() with its observer (integrator.py:209-239).  u0 = 1 + 0.1 U[0,1)
+    from default_rng(1234), the bench's seeding."""
+    g = Grid3D(256, 256, 1)
+    op = StencilOperator(g, BoundaryCondition.homogeneous())
+    u0 = 1.0 + 0.1 * np.random.default_rng(1234).random(g.n)
+    h, tol, nsteps = 1e-4, 1e-4, 10
+    obs = []
+    prob = SemilinearProblem(operator=op, nonlinearity=lambda u: combustion_g(u), u0=u0)
+    u = integrate(prob, StepperConfig(h=h, t_end=h * nsteps, tol=tol),
+                  observer=lambda k, t, mv, mx: obs.append((k, t, mv, mx)))
+    save("c1_trajectory", u0=u0, u=u, obs=np.array(obs), params=np.array([h, tol, nsteps]),
+         dims=np.array([256, 256, 1]))
+
+
+def split_cases():
+    """Dirichlet-function boundaries through the affine split
+    (stencil.py:281-312): apply_affine_split, homogeneous_part applies,
+    boundary_source_field, and exponential-Euler trajectories on the split
+    problem (forcing g - b, integrator.py:104-123)."""
+    from expstencil.grid import Field as RField
+    from expstencil.stencil import apply_affine_split, boundary_source_field, homogeneous_part
+
+    rng = np.random.default_rng(106)
+    out = {}
+    cases = [((9, 7, 5), "poly", False), ((9, 7, 5), "trig", True), ((33, 17, 1), "trig", False),
+             ((24, 20, 16), "poly", True), ((40, 36, 1), "trig", True)]
+    for i, (dims, bc, coeff) in enumerate(cases):
+        g = Grid3D(*dims)
+        op = StencilOperator(g, bc_of(bc), coeff=coeff_d if coeff else None)
+        x = rng.standard_normal(g.n)
+        hom, b = apply_affine_split(op, RField(g, x))
+        bs = boundary_source_field(op)
+        hp = homogeneous_part(op)
+        y = hp.fused_apply_flat(0.75, -0.5, x)
+        full = apply(op, RField(g, x)).values
+        out[f"s{i}_dims"], out[f"s{i}_bc"], out[f"s{i}_coeff"] = np.array(dims), np.array(bc), np.array(coeff)
+        out[f"s{i}_x"] = x
+        out[f"s{i}_hom"], out[f"s{i}_b"], out[f"s{i}_bsrc"] = hom.values, b.values, bs.values
+        out[f"s{i}_hp_y"], out[f"s{i}_full"] = y, full
+        for j, f in enumerate(boundary_faces(op, np.float64)):
+            out[f"s{i}_face{j}"] = f
+    out["ncases"] = np.array(len(cases))
+    # trajectories on the split problem: du/dt + A_hom u = g(u) - b
+    traj = [((32, 32, 1), "trig", False, True, 2e-4, 1e-6, 3), ((20, 18, 16), "poly", True, True, 2e-4, 1e-6, 2),
+            ((48, 40, 1), "poly", False, False, 1e-3, 1e-8, 2)]
+    for i, (dims, bc, coeff, nonlin, h, tol, nsteps) in enumerate(traj):
+        g = Grid3D(*dims)
+        op = StencilOperator(g, bc_of(bc), coeff=coeff_d if coeff else None)
+        b = boundary_source_field(op).values
+        u0 = 1.0 + 0.1 * rng.random(g.n)
+        obs = []
+        prob = SemilinearProblem(operator=homogeneous_part(op),
+                                 nonlinearity=(lambda u: combustion_g(u)) if nonlin else None, u0=u0,
+                                 boundary_source=b)
+        u = integrate(prob, StepperConfig(h=h, t_end=h * nsteps, tol=tol),
+                      observer=lambda k, t, mv, mx: obs.append((k, t, mv, mx)))
+        out[f"t{i}_dims"], out[f"t{i}_bc"], out[f"t{i}_coeff"] = np.array(dims), np.array(bc), np.array(coeff)
+        out[f"t{i}_nonlin"] = np.array(nonlin)
+        out[f"t{i}_params"] = np.array([h, tol, nsteps])
+        out[f"t{i}_u0"], out[f"t{i}_b"], out[f"t{i}_u"], out[f"t{i}_obs"] = u0, b, u, np.array(obs)
+        for j, f in enumerate(boundary_faces(op, np.float64)):
+            out[f"t{i}_face{j}"] = f
+    out["ntraj"] = np.array(len(traj))
+    save("split", **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate selected fixtures only: make_golden.py split c1_trajectory
+        for name in sys.argv[1:]:
+            globals()[name + ("_case" if name == "c1_trajectory" else "_cases")]()
+        sys.exit(0)
+    c1_trajectory_case()
+    split_cases()
     stencil_cases()
     slab_cases()
     leja_cases()

@@ -160,3 +160,54 @@ def test_neumann_matches_dense_oracle(oracle):
     ev = np.linalg.eigvals(mat)
     assert lo <= ev.real.min() + 1e-9 and ev.real.max() <= hi + 1e-9
     assert lo == 0.0
+
+
+def test_c1_full_size_trajectory(golden, oracle):
+    # BASELINE config 1 at full size (256^2, 10 steps, reference integrate())
+    d = golden("c1_trajectory")
+    h, tol, nsteps = d["params"]
+    nx, ny, nz = (int(v) for v in d["dims"])
+    u, obs = oracle.integrate(orc.StencilSpec(nx, ny, nz), d["u0"], h, h * nsteps, tol)
+    ref_obs = d["obs"]
+    assert [o[2] for o in obs] == [int(m) for m in ref_obs[:, 2]]
+    np.testing.assert_allclose([o[3] for o in obs], ref_obs[:, 3], rtol=1e-12, atol=0)
+    ref = d["u"]
+    assert np.max(np.abs(u - ref)) <= 1e-10 * np.max(np.abs(ref))
+
+
+def _split_spec(d, p, faces=True):
+    nx, ny, nz = (int(v) for v in d[f"{p}_dims"])
+    ck = orc.COEFF_RADIAL if bool(d[f"{p}_coeff"]) else orc.COEFF_NONE
+    if not faces:
+        return orc.StencilSpec(nx, ny, nz, coeff_kind=ck)
+    return orc.StencilSpec(nx, ny, nz, mode=orc.MODE_FACES, coeff_kind=ck,
+                           faces=tuple(d[f"{p}_face{j}"] for j in range(6)))
+
+
+def test_affine_split_pieces(golden, oracle):
+    # apply_affine_split / homogeneous_part / boundary_source_field
+    # (stencil.py:281-312): A u = A_hom u + b, bitwise
+    d = golden("split")
+    for i in range(int(d["ncases"])):
+        p = f"s{i}"
+        x = d[f"{p}_x"]
+        full = _split_spec(d, p)
+        hom = _split_spec(d, p, faces=False)
+        b = oracle.stencil_fused(full, 1.0, 0.0, np.zeros_like(x))
+        assert b.tobytes() == d[f"{p}_b"].tobytes() == d[f"{p}_bsrc"].tobytes(), p
+        assert oracle.stencil_fused(hom, 1.0, 0.0, x).tobytes() == d[f"{p}_hom"].tobytes(), p
+        assert oracle.stencil_fused(hom, 0.75, -0.5, x).tobytes() == d[f"{p}_hp_y"].tobytes(), p
+        assert oracle.stencil_fused(full, 1.0, 0.0, x).tobytes() == d[f"{p}_full"].tobytes(), p
+
+
+def test_split_problem_trajectories(golden, oracle):
+    # du/dt + A_hom u = g(u) - b (SemilinearProblem.forcing, integrator.py:104-123)
+    d = golden("split")
+    for i in range(int(d["ntraj"])):
+        p = f"t{i}"
+        h, tol, nsteps = d[f"{p}_params"]
+        u, obs = oracle.integrate(_split_spec(d, p, faces=False), d[f"{p}_u0"], h, h * nsteps, tol,
+                                  nonlinear=bool(d[f"{p}_nonlin"]), source=d[f"{p}_b"])
+        assert [o[2] for o in obs] == [int(m) for m in d[f"{p}_obs"][:, 2]], p
+        ref = d[f"{p}_u"]
+        assert np.max(np.abs(u - ref)) <= 1e-12 * np.max(np.abs(ref)), p
