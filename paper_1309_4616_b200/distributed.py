@@ -154,7 +154,14 @@ class SeriesOutcome:
 def drive_series(backend, comm, ndd: int, batch: int = 4, ledger: Optional[TransferLedger] = None):
     """Host loop of a multi-GPU series (slab or row block): exchange -> node
     -> gather -> decide per node, batches of `batch` nodes between
-    asynchronous state polls."""
+    asynchronous state polls.
+
+    Polling lags the device by up to two batches, so a few nodes may be
+    enqueued after the series has stopped (they early-exit on the device but
+    their exchanges still move data).  The ledger keeps the reference's
+    contract -- one entry per operator apply of the series (decomp.py:86-103)
+    -- and books the speculative exchanges separately
+    (``ledger.speculative_scalars``)."""
     counts = backend.slice_counts(comm)
     k, pending = 0, []
     while k < ndd - 1:
@@ -163,15 +170,19 @@ def drive_series(backend, comm, ndd: int, batch: int = 4, ledger: Optional[Trans
                 break
             k += 1
             backend.exchange(k)
-            if ledger is not None:
-                ledger.record(comm.ledger_scalars(), 8)
             local = backend.node()
             backend.decide(comm.gather(local, counts))
         pending.append(backend.poll_state())
         if len(pending) >= 2 and backend.state_done(pending.pop(0)):
             break
     backend.end()
-    return backend.fetch()
+    res = backend.fetch()
+    if ledger is not None:
+        applied = min(k, backend.matvecs_of(res))
+        for _ in range(applied):
+            ledger.record(comm.ledger_scalars(), 8)
+        ledger.speculative_scalars = getattr(ledger, "speculative_scalars", 0) + (k - applied) * comm.ledger_scalars()
+    return res
 
 
 class _CudaSeriesBackend:
@@ -234,6 +245,10 @@ class _CudaSeriesBackend:
 
     def end(self):
         _lib.check(getattr(self.lib, self.END)(ptr(self.ws), stream_handle()), self.END)
+
+    @staticmethod
+    def matvecs_of(res) -> int:
+        return int(res.matvecs)
 
     def fetch(self):
         res = _lib.SeriesResult()

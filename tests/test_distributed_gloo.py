@@ -91,6 +91,10 @@ class OracleSlabBackend:
     def fetch(self):
         return self.k, self.converged, self.p
 
+    @staticmethod
+    def matvecs_of(res):
+        return res[0]
+
 
 def _decide(self, slices_all):
     if self.done:
@@ -141,6 +145,7 @@ class OracleRowBackend:
     state_done = staticmethod(OracleSlabBackend.state_done)
     end = OracleSlabBackend.end
     fetch = OracleSlabBackend.fetch
+    matvecs_of = staticmethod(OracleSlabBackend.matvecs_of)
 
     def exchange(self, k):
         self.comm.exchange(self.source(k), self.xg)
@@ -261,7 +266,7 @@ def _worker(rank, world, port, dims, tol, batch, queue):
         dist.all_gather_object(hparts, hashes.numpy())
         if rank == 0:
             queue.put((ok_halo, k, conv, [q for _, q in sorted(parts, key=lambda t: t[0])], ledger.last_scalars(),
-                       ledger.apply_count, np.concatenate(hparts)))
+                       (ledger.apply_count, getattr(ledger, "speculative_scalars", 0)), np.concatenate(hparts)))
         else:
             queue.put(("ok", ok_halo))
     finally:
@@ -293,6 +298,8 @@ def test_slab_series_matches_single_domain(world, dims, tol, batch):
     assert k == mv and conv
     assert np.concatenate(parts).tobytes() == ref.tobytes()  # bitwise, whatever the rank count
     assert last == 2 * (world - 1) * nx * ny  # reference ledger formula (decomp.py:7-8)
-    assert napplies >= k
+    napplies, speculative = napplies
+    assert napplies == k  # one ledger entry per operator apply of the series
+    assert speculative % (2 * (world - 1) * nx * ny) == 0  # wasted exchanges booked apart
     # the synthetic state does not depend on the partition
     assert np.array_equal(hashes, global_hash_state(nx, ny, nz, 0, nz, "cpu").numpy())
