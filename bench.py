@@ -492,6 +492,8 @@ def run_b200(args, cfg):
     from paper_1309_4616_b200 import timing
 
     rank, world, local = dist_env()
+    if torch.cuda.device_count() <= local:
+        raise RuntimeError(f"rank {rank}: LOCAL_RANK {local} but only {torch.cuda.device_count()} CUDA device(s)")
     torch.cuda.set_device(local)
     use_dist = world > 1 or args.force_dist
     # single-plane grids (C1, C2) cannot be slab-partitioned (decomp.py:76-77):
@@ -644,9 +646,15 @@ def run_b200(args, cfg):
         cpu = {"value": u_cpu / dt / 1e9, "unit": UNIT, "cores": threads, "kind": kind, "sample": desc,
                "seconds": dt, "host_cpu_count": os.cpu_count()}
 
+    gpus_active = 1
+    if world > 1:  # distinct physical devices the ranks ran on
+        uuids = [None] * world
+        dist.all_gather_object(uuids, str(torch.cuda.get_device_properties(local).uuid))
+        gpus_active = len(set(uuids))
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "gpus_active": gpus_active,
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if world > 1 and not replicas else "weak", "vs_baseline": None, "dtype": "f64",
             "data": ("synthetic: seeded symmetric CSR (default_rng(1234)), v ~ N(0,1) default_rng(1234)"
@@ -666,13 +674,41 @@ def run_b200(args, cfg):
         dist.destroy_process_group()
 
 
+def self_launch(args) -> int:
+    """`bench.py --gpus N` run without a launcher: start N ranks (one process
+    per GPU) under torch.distributed.run on 127.0.0.1 and pass their exit
+    code through; rank 0 prints the JSON line."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible",
+              file=sys.stderr, flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
-    else:
-        run_b200(args, cfg)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    world = dist_env()[1]
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or drop the launcher", file=sys.stderr, flush=True)
+        sys.exit(2)
+    run_b200(args, cfg)
 
 
 if __name__ == "__main__":

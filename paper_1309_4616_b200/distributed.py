@@ -67,7 +67,18 @@ class SlabComm:
 
     def exchange(self, src: torch.Tensor, halo_lo: Optional[torch.Tensor], halo_hi: Optional[torch.Tensor]) -> None:
         """Send this slab's first / last plane down / up; receive the
-        neighbours' into the halo buffers (one batched NCCL group)."""
+        neighbours' into the halo buffers (one batched NCCL group; staged
+        through host memory on a gloo group, which cannot send device
+        tensors)."""
+        if src.is_cuda and dist.get_backend(self.group) != "nccl":
+            hl = None if halo_lo is None else torch.empty(halo_lo.shape, dtype=halo_lo.dtype)
+            hh = None if halo_hi is None else torch.empty(halo_hi.shape, dtype=halo_hi.dtype)
+            self.exchange(src.cpu(), hl, hh)
+            if hl is not None:
+                halo_lo.copy_(hl)
+            if hh is not None:
+                halo_hi.copy_(hh)
+            return
         ops = []
         if self.rank > 0:
             ops.append(dist.P2POp(dist.isend, src[: self.plane], self._peer(self.rank - 1), self.group))
@@ -89,6 +100,11 @@ class SlabComm:
         return torch.cat([p[: 2 * c] for p, c in zip(parts, counts)])
 
     def allreduce(self, t: torch.Tensor, op) -> torch.Tensor:
+        if t.is_cuda and dist.get_backend(self.group) != "nccl":  # gloo: through host memory
+            h = t.cpu()
+            dist.all_reduce(h, op=op, group=self.group)
+            t.copy_(h)
+            return t
         dist.all_reduce(t, op=op, group=self.group)
         return t
 
@@ -137,6 +153,8 @@ class RowComm:
 
     def gather(self, local: torch.Tensor, counts: list[int]) -> torch.Tensor:
         return SlabComm.gather(self, local, counts)
+
+    allreduce = SlabComm.allreduce
 
     def ledger_scalars(self) -> int:
         # every worker receives the other blocks (decomp.py:323)
@@ -304,10 +322,16 @@ class CudaRowBackend(_CudaSeriesBackend):
 
 def _peer_or_none(make, exchange: str, group):
     """The peer-memory resources when requested / possible on EVERY rank
-    (collective; 'auto' falls back to the NCCL-driven series together)."""
-    if exchange == "nccl" or dist.get_backend(group) != "nccl":
-        if exchange == "p2p":
-            raise RuntimeError("exchange='p2p' needs the NCCL backend (one CUDA device per rank)")
+    (collective; 'auto' falls back to the NCCL-driven series together).
+
+    The data path of the peer-memory series is the kernels' own peer loads /
+    stores; torch.distributed only carries the set-up (IPC handles, slice
+    counts, barriers).  So an explicit exchange='p2p' also runs over a gloo
+    group -- the way several processes sharing ONE device exercise the
+    cross-process path (CUDA IPC, system-scope arrival counters) where NCCL
+    refuses duplicate devices."""
+    backend = dist.get_backend(group)
+    if exchange == "nccl" or (backend != "nccl" and exchange != "p2p"):
         return None
     if exchange == "auto" and dist.get_world_size(group) == 1:
         return None  # nothing to exchange: the caller runs the single-device series
@@ -316,7 +340,7 @@ def _peer_or_none(make, exchange: str, group):
         peer = make()
     except Exception as e:  # IPC mapping impossible on this node
         err = e
-    ok = torch.tensor([0 if peer is None else 1], device="cuda")
+    ok = torch.tensor([0 if peer is None else 1], device=_reduce_device(group))
     dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)  # every rank takes the same path
     if int(ok.item()) == 0:
         if peer is not None:
@@ -361,6 +385,8 @@ class _PeerMemory:
         self._opened.append(p.value)
         return int(p.value)
 
+    poisoned = False
+
     def fetch(self, ws):
         res = _lib.SeriesResult()
         rc = self.lib.es_leja_fetch(ptr(ws), ctypes.byref(res), stream_handle())
@@ -370,6 +396,40 @@ class _PeerMemory:
         k = int(res.matvecs)
         self.rounds += ((k + 1) // 2 if getattr(self, "two", False) else k) + 1
         return res
+
+    def run(self, enqueue, ws):
+        """Enqueue one series and fetch its result.  The arrival counters
+        only stay in step across ranks while every series completes on every
+        rank: after a failure here (a peer timed out, or a rank raised before
+        launching) the peers' arrivals may be ahead of ``base``, and a
+        following series could read halos / slices that were never written.
+        So a failure poisons these resources until ``reset()`` has run
+        collectively on every rank."""
+        if self.poisoned:
+            raise RuntimeError("peer-memory series state is out of step after a failed series; "
+                               "call reset() on every rank (collective) before the next series")
+        try:
+            enqueue()
+            return self.fetch(ws)
+        except Exception:
+            self.poisoned = True
+            raise
+
+    def _zero(self):
+        for t in self._resettable():
+            t.zero_()
+
+    def reset(self):
+        """Collective resynchronisation after a failed series: every rank
+        drains its device work, then the arrival counters, slice tables and
+        exchange buffers are zeroed and the round count restarts at 0."""
+        torch.cuda.synchronize()
+        dist.barrier(group=self.comm.group)
+        self._zero()
+        self.rounds = 0
+        torch.cuda.synchronize()
+        dist.barrier(group=self.comm.group)
+        self.poisoned = False
 
     def close(self):
         for p in getattr(self, "_opened", []):
@@ -426,6 +486,9 @@ class PeerSlab(_PeerMemory):
         self.desc = x
         dist.barrier(group=c.group)
 
+    def _resettable(self):
+        return [t for t in (self.halo, self.ghalo, self.slices, self.arrive) if t is not None]
+
     def enqueue(self, d, v, p_out, dd, xi, alpha, shift, tol, gdiag, ws):
         """Enqueue the whole series (one graph) on the current stream."""
         self.desc.base = self.comm.world * self.rounds
@@ -477,6 +540,9 @@ class PeerRows(_PeerMemory):
         self.desc = x
         dist.barrier(group=c.group)
 
+    def _resettable(self):
+        return [self.xg2, self.slices, self.arrive]
+
     def enqueue(self, op, v, p_out, dd, xi, alpha, shift, tol, ws):
         self.desc.base = self.comm.world * self.rounds
         rp, col, vals = op.device_arrays()
@@ -492,7 +558,7 @@ class DistributedStencil:
     local slab, flat x fastest)."""
 
     def __init__(self, op: StencilOperator, group=None, ledger: Optional[TransferLedger] = None, batch: int = 4,
-                 exchange: str = "auto"):
+                 exchange: str = "auto", peer_timeout_s: float = 30.0):
         """exchange: 'p2p' -- the peer-memory series (es_leja_p2p: halo
         planes and slice sums written over NVLink by the kernels, one graph
         per series); 'nccl' -- the host-driven series (NCCL send/recv and
@@ -508,7 +574,8 @@ class DistributedStencil:
         # a single-plane grid has one slab (make_partition refuses m > nz,
         # decomp.py:76-77): world 1 runs the plain device series
         self.whole = g.nz == 1
-        self.peer = None if self.whole else _peer_or_none(lambda: PeerSlab(op, self.comm), exchange, group)
+        self.peer = None if self.whole else _peer_or_none(lambda: PeerSlab(op, self.comm, peer_timeout_s), exchange,
+                                                          group)
         # one rank and no exchange requested: the single-device series
         self.whole = self.whole or (self.peer is None and exchange == "auto" and self.comm.world == 1)
         self.exchange = "none" if self.whole else "p2p" if self.peer is not None else "nccl"
@@ -564,9 +631,14 @@ class DistributedStencil:
             tm = timing.active()
             ev0 = timing.event() if tm else None
             ws = self._workspace()
-            self.peer.enqueue(d, v, p_out, dd, xi, alpha, shift, tol, gdiag, ws)
-            ev1 = timing.event() if tm else None
-            res = self.peer.fetch(ws)
+            ev1 = []
+
+            def go():
+                self.peer.enqueue(d, v, p_out, dd, xi, alpha, shift, tol, gdiag, ws)
+                ev1.append(timing.event() if tm else None)
+
+            res = self.peer.run(go, ws)
+            ev1 = ev1[0]
             for _ in range(int(res.matvecs)):
                 self.ledger.record(self.comm.ledger_scalars(), 8)
             if tm:
@@ -582,6 +654,11 @@ class DistributedStencil:
             tm.add(ev0, timing.event(), res.matvecs)
         del keep
         return res
+
+    def reset_peer(self) -> None:
+        """Collective: resynchronise the peer-memory series after a failure."""
+        if self.peer is not None:
+            self.peer.reset()
 
     def two_node_passes(self) -> bool:
         """Whether this rank's series run two Leja nodes per HBM pass."""
@@ -602,7 +679,7 @@ class DistributedCsr:
     protocol, vectors are the local rows (``n`` = local row count)."""
 
     def __init__(self, a, group=None, ledger: Optional[TransferLedger] = None, batch: int = 4,
-                 exchange: str = "auto"):
+                 exchange: str = "auto", peer_timeout_s: float = 30.0):
         """exchange: 'p2p' (es_leja_csr_p2p: every node stores its rows into
         every rank's gathered vector over NVLink), 'nccl' (host-driven
         all-gather per node), 'auto' (p2p when CUDA IPC works on all ranks)."""
@@ -626,13 +703,18 @@ class DistributedCsr:
         self._dev = None
         self._ws = None
         self._xg = None
-        self.peer = _peer_or_none(lambda: PeerRows(self), exchange, group)
+        self.peer = _peer_or_none(lambda: PeerRows(self, peer_timeout_s), exchange, group)
         self.whole = self.peer is None and exchange == "auto" and c.world == 1
         self.exchange = "none" if self.whole else "p2p" if self.peer is not None else "nccl"
 
     @property
     def n(self) -> int:
         return self.comm.n_local
+
+    def reset_peer(self) -> None:
+        """Collective: resynchronise the peer-memory series after a failure."""
+        if self.peer is not None:
+            self.peer.reset()
 
     @property
     def xg(self) -> torch.Tensor:
@@ -679,9 +761,14 @@ class DistributedCsr:
             tm = timing.active()
             ev0 = timing.event() if tm else None
             ws = self._workspace()
-            self.peer.enqueue(self, v, p_out, dd, xi, alpha, shift, tol, ws)
-            ev1 = timing.event() if tm else None
-            res = self.peer.fetch(ws)
+            ev1 = []
+
+            def go():
+                self.peer.enqueue(self, v, p_out, dd, xi, alpha, shift, tol, ws)
+                ev1.append(timing.event() if tm else None)
+
+            res = self.peer.run(go, ws)
+            ev1 = ev1[0]
             for _ in range(int(res.matvecs)):
                 self.ledger.record(self.comm.ledger_scalars(), 8)
             if tm:
@@ -695,6 +782,43 @@ class DistributedCsr:
         if tm:
             tm.add(ev0, timing.event(), res.matvecs)
         return res
+
+
+def _reduce_device(group) -> str:
+    return "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+
+
+def allreduce_scalar(comm, value, op, dtype=torch.float64):
+    """One scalar reduced over the operator's ranks (NCCL: on the device)."""
+    t = torch.tensor([value], dtype=dtype, device=_reduce_device(comm.group))
+    dist.all_reduce(t, op=op, group=comm.group)
+    return t.item()
+
+
+def global_offset(op) -> int:
+    """Global flat index of this rank's first local point / row."""
+    c = op.comm
+    return c.r_lo if isinstance(op, DistributedCsr) else c.z_lo * c.plane
+
+
+def rank_consistent_pointwise(op, fn):
+    """Run a pointwise evaluation that may raise DomainError on this rank's
+    part, and make the outcome the same on every rank: if any rank hit the
+    domain, all ranks raise DomainError with the smallest GLOBAL index (the
+    index a single-device run reports).  Without this, one rank raises while
+    its peers enter the next series and wait for it forever."""
+    from .errors import DomainError
+
+    try:
+        out, bad = fn(), -1
+    except DomainError as e:
+        out, bad = None, int(e.index if e.index is not None else 0)
+    big = 2**62
+    gbad = int(allreduce_scalar(op.comm, big if bad < 0 else global_offset(op) + bad, dist.ReduceOp.MIN,
+                                dtype=torch.int64))
+    if gbad < big:
+        raise DomainError(f"combustion nonlinearity undefined at global index {gbad}", index=gbad)
+    return out
 
 
 def global_hash_state(nx: int, ny: int, nz: int, z_lo: int, z_hi: int, device) -> torch.Tensor:

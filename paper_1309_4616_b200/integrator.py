@@ -135,6 +135,17 @@ class SemilinearProblem:
     def initial_values(self):
         return _values(self.u0)
 
+    def _call_g(self, g, u, t):
+        if self._g_takes_time is None:
+            try:
+                gu = g(u, t)
+                self._g_takes_time = True
+            except TypeError:
+                gu = g(u)
+                self._g_takes_time = False
+            return gu
+        return g(u, t) if self._g_takes_time else g(u)
+
     def forcing(self, u: torch.Tensor, t: float) -> Optional[torch.Tensor]:
         """g(u[, t]) - b on the device, or None for a purely linear problem."""
         g = self.nonlinearity
@@ -144,15 +155,12 @@ class SemilinearProblem:
             neg = empty(self._b_dev.numel())
             _lib.check(_lib.load().es_scale(ptr(self._b_dev), -1.0, ptr(neg), neg.numel(), stream_handle()))
             return neg
-        if self._g_takes_time is None:
-            try:
-                gu = g(u, t)
-                self._g_takes_time = True
-            except TypeError:
-                gu = g(u)
-                self._g_takes_time = False
+        if hasattr(self.operator, "comm"):  # one slab / row block per rank: agree on DomainError
+            from .distributed import rank_consistent_pointwise
+
+            gu = rank_consistent_pointwise(self.operator, lambda: self._call_g(g, u, t))
         else:
-            gu = g(u, t) if self._g_takes_time else g(u)
+            gu = self._call_g(g, u, t)
         gu = to_device(gu)
         if self.boundary_source is not None:
             gu = _axpy(gu, self._b_dev, -1.0)
@@ -329,7 +337,12 @@ def integrate(problem: SemilinearProblem, cfg: StepperConfig, observer: Optional
             raise type(err)(f"step {k + 1} (t={t:.6g}): {err}") from err
         t = cfg.t_end if last else t + cfg.h
         if observer is not None:
-            observer(k + 1, t, stats.matvecs, max_abs(u))
+            mx = max_abs(u)
+            if hasattr(problem.operator, "comm"):  # the global max-norm, like a single-device run
+                from .distributed import allreduce_scalar
+
+                mx = allreduce_scalar(problem.operator.comm, mx, torch.distributed.ReduceOp.MAX)
+            observer(k + 1, t, stats.matvecs, mx)
     return _wrap(problem.u0, u)
 
 

@@ -303,3 +303,52 @@ def test_slab_series_matches_single_domain(world, dims, tol, batch):
     assert speculative % (2 * (world - 1) * nx * ny) == 0  # wasted exchanges booked apart
     # the synthetic state does not depend on the partition
     assert np.array_equal(hashes, global_hash_state(nx, ny, nz, 0, nz, "cpu").numpy())
+
+
+def _domain_worker(rank, world, port, queue):
+    from types import SimpleNamespace
+
+    from paper_1309_4616_b200.distributed import allreduce_scalar, rank_consistent_pointwise
+    from paper_1309_4616_b200.errors import DomainError
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = SlabComm(4, 3, 6)  # z-slabs of 4x3 planes
+        op = SimpleNamespace(comm=comm)
+
+        def g_local():  # only the last rank sees u <= 0, at local index 5
+            if rank == world - 1:
+                raise DomainError("local", index=5)
+            return "fine"
+
+        try:
+            rank_consistent_pointwise(op, g_local)
+            got = None
+        except DomainError as e:
+            got = e.index
+        ok = rank_consistent_pointwise(op, lambda: "fine") == "fine"
+        mx = allreduce_scalar(comm, float(rank + 1), dist.ReduceOp.MAX)
+        queue.put((rank, got, ok, mx, comm.z_lo))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_domain_error_and_norm_are_rank_consistent():
+    # every rank raises DomainError with the GLOBAL index (one rank
+    # raising alone would leave its peers waiting in the next series)
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_domain_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    last_z_lo = results[-1][4]
+    for rank, got, ok, mx, _ in results:
+        assert got == last_z_lo * 12 + 5
+        assert ok and mx == float(world)
