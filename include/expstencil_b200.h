@@ -66,6 +66,8 @@ typedef struct es_series_result {
     int32_t converged; /* 1: stopped by the twice-in-a-row test, or tol == 0 */
     double last_term;  /* |dd_k| ||w_k||_2 of the last node */
     double last_pnorm; /* ||p_k||_2 of the last node */
+    int32_t passes;    /* sweeps over the operand: == matvecs, except where two nodes share one pass */
+    int32_t reserved;
 } es_series_result;
 
 int es_abi_version(void);

@@ -14,7 +14,8 @@ import threading
 from .errors import ConvergenceError, DomainError, ExpStencilError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libexpstencil_b200.so")
+# ES_LIB: an alternative build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("ES_LIB") or os.path.join(_HERE, "_lib", "libexpstencil_b200.so")
 
 ES_OK, ES_ERR_ARG, ES_ERR_NOT_CONVERGED, ES_ERR_DOMAIN, ES_ERR_CUDA, ES_ERR_RANGE, ES_ERR_TYPE = 0, 1, 2, 3, 4, 5, 6
 ES_KIND_F32, ES_KIND_F64, ES_KIND_C128 = 0, 1, 2
@@ -75,6 +76,7 @@ class SeriesResult(ctypes.Structure):
     _fields_ = [
         ("matvecs", ctypes.c_int32), ("converged", ctypes.c_int32),
         ("last_term", ctypes.c_double), ("last_pnorm", ctypes.c_double),
+        ("passes", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 

@@ -54,6 +54,8 @@ int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaS
     res->converged = st.converged;
     res->last_term = st.last_term;
     res->last_pnorm = st.last_pnorm;
+    res->passes = st.pass > 0 ? st.pass : st.k;  // one-node series never count passes
+    res->reserved = 0;
     if (!st.done) return set_error(ES_ERR_CUDA, "series did not finish (k=%d)", st.k);
     if (st.converged < 0)
         return set_error(ES_ERR_CUDA, "peer-memory series: a peer did not arrive within the timeout (node %d)", st.k);
@@ -87,7 +89,7 @@ static int check_desc(const es_stencil_desc *d, bool pointers = true) {
 
 using namespace es;
 
-extern "C" int es_abi_version(void) { return 1; }
+extern "C" int es_abi_version(void) { return 2; }
 
 extern "C" const char *es_last_error(void) { return t_err; }
 

@@ -251,6 +251,7 @@ __global__ void k_csr_init(const SeriesParams p, SeriesParams *dst) {
         SeriesState &st = *p.state;
         st.k = 0;
         st.consecutive = 0;
+        st.pass = 0;
         st.done = 0;
         st.converged = 0;
         st.last_term = __longlong_as_double(0x7ff0000000000000ll);

@@ -64,6 +64,8 @@ struct SeriesState {
     int converged;    // 1 unless the degree budget ran out with tol > 0
     double last_term;
     double last_pnorm;
+    int pass;  // two-node series (stencil_tb.cuh): HBM passes completed (selects the w buffers / halo parity)
+    int pad_;
 };
 
 }  // namespace es

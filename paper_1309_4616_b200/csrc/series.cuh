@@ -213,6 +213,16 @@ ES_DEV void decide_gathered(const SeriesParams &P, int k, const double *slices, 
     if (lane == 0) decide(P, k, sw, sp);
 }
 
+// Does the pass starting at node k also compute node k + 1?  Not past the
+// last divided difference, and (tail1) not when node k - 1 met the term test
+// for the first time: the series then usually stops at k, so the pass runs
+// k alone (and stores w_k in case it does not).  Every kernel of the pass
+// reads the state before the pass's decisions change it.
+ES_DEV bool tb_two(const SeriesParams &P, int k) {
+    if (k + 1 > P.ndd - 1) return false;
+    return !(P.tail1 && P.tol > 0.0 && P.state->consecutive == 1);
+}
+
 // Node k's pass description from the device state (k = last completed + 1).
 ES_DEV Pass node_pass(const SeriesParams &P, int k) {
     Pass ps;
@@ -313,8 +323,8 @@ ES_DEV void slice_p2p_decide(const SeriesParams &P, int k) {
 ES_DEV void slice_p2p_decide2(const SeriesParams &P, int k) {
     __shared__ int s_last, s_ok;
     const int c = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const bool two = k + 1 <= P.ndd - 1;
-    const int pass = (k - 1) / 2, par = pass & 1;
+    const bool two = tb_two(P, k);
+    const int pass = P.state->pass, par = pass & 1;
     const int64_t half = (int64_t)P.nslices * P.ntiles * 2;
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
     cta_slice_sum(P, c, a0, b0);
@@ -358,6 +368,7 @@ ES_DEV void slice_p2p_decide2(const SeriesParams &P, int k) {
             }
             if (__shfl_sync(0xffffffffu, stop, 0)) break;
         }
+        if (lane == 0) P.state->pass = pass + 1;
     }
 }
 
@@ -367,7 +378,7 @@ ES_DEV void slice_p2p_decide2(const SeriesParams &P, int k) {
 ES_DEV void slice_reduce_decide2(const SeriesParams &P, int k) {
     __shared__ int s_last;
     const int c = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const bool two = k + 1 <= P.ndd - 1;
+    const bool two = tb_two(P, k);
     const int64_t half = (int64_t)P.nslices * P.ntiles * 2;
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
     cta_slice_sum(P, c, a0, b0);
@@ -401,7 +412,10 @@ ES_DEV void slice_reduce_decide2(const SeriesParams &P, int k) {
             }
             if (__shfl_sync(0xffffffffu, stop, 0)) break;
         }
-        if (lane == 0) *P.global_cnt = 0u;
+        if (lane == 0) {
+            *P.global_cnt = 0u;
+            P.state->pass += 1;
+        }
     }
 }
 

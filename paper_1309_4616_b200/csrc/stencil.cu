@@ -215,9 +215,9 @@ __global__ void __launch_bounds__(256) k_slice_p2p2(const SeriesParams *__restri
         return;
     }
     const int k = P.state->k + 1;
-    const int pass = (k - 1) / 2, par = (pass + 1) & 1;
+    const int pass = P.state->pass, par = (pass + 1) & 1;
     if (blockIdx.x == 0 && threadIdx.x == 0 && P.work) *P.work = 0u;
-    const double2 *w = reinterpret_cast<const double2 *>(P.wbuf[pass & 1]);  // w_{k+1}
+    const double2 *w = reinterpret_cast<const double2 *>(P.wbuf[pass & 1]);  // w_{k+1} (w_k: one-node pass)
     double2 *lo = reinterpret_cast<double2 *>(P.peer_lo[par]), *hi = reinterpret_cast<double2 *>(P.peer_hi[par]);
     const int64_t two_planes = P.g.nx * P.g.ny, lz = P.g.lz;  // two planes = nx ny double2
     if (lo || hi) {
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(TB_THREADS, TB_MINB) k_node_tb(const SeriesPar
     const SeriesParams &P = *Pp;
     if (P.state->done) return;
     const int k = P.state->k + 1;
-    tb_pass<COEFF, GD>(Pp, k, k + 1 <= P.ndd - 1, tsmem);
+    tb_pass<COEFF, GD>(Pp, k, tb_two(P, k), tsmem);
 }
 
 __global__ void __launch_bounds__(256) k_slice_reduce2(const SeriesParams *__restrict__ Pp) {
@@ -283,6 +283,7 @@ __global__ void k_series_init(const SeriesParams p, SeriesParams *dst) {
         SeriesState &st = *p.state;
         st.k = 0;
         st.consecutive = 0;
+        st.pass = 0;
         st.done = 0;
         st.converged = 0;
         st.last_term = __longlong_as_double(0x7ff0000000000000ll);  // +inf
@@ -307,6 +308,7 @@ __global__ void k_series_finalize(const SeriesParams *__restrict__ Pp, int64_t n
 __global__ void k_state_trivial(SeriesState *st) {
     st->k = 0;
     st->consecutive = 0;
+    st->pass = 0;
     st->done = 1;
     st->converged = 1;
     st->last_term = 0.0;
@@ -819,6 +821,7 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     hp.cond = 0;
     hp.maps = nullptr;
     hp.dist = dist ? 1 : 0;
+    hp.tail1 = env_int("ES_TB_TAIL", 1) ? 1 : 0;
     S.dparams = reinterpret_cast<SeriesParams *>(w + L.params);
     if (pl.tma) {
         TmaMaps maps;
@@ -840,6 +843,7 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
             if (!rc) rc = encode_map(&maps.m[MAP_T_G], gdiag, d, false, MK_G2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_PV], v, d, false, MK_P2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_P0], hp.pbuf[0], d, false, MK_P2);
+            if (!rc) rc = encode_map(&maps.m[MAP_T_P1], hp.pbuf[1], d, false, MK_P2);
             if (halos) {  // two-plane w halos by parity, g' boundary planes of the neighbours
                 es_stencil_desc d2 = *d;
                 d2.lz = 2;
@@ -891,7 +895,8 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     if (ge) {
         if (cudaGraphLaunch(ge, stream) != cudaSuccess) return check_launch("series graph");
     } else {
-        for (int k = 1; k < ndd; k += S.tb ? 2 : 1) {
+        // one launch pair per node at most (a two-node series may run one-node passes)
+        for (int k = 1; k < ndd; ++k) {
             S.nf<<<S.lp.grid, S.lp.block, S.lp.smem, stream>>>(S.dparams);
             if (S.pl.tma) rf<<<(unsigned)S.pl.nslices, 256, 0, stream>>>(S.dparams);
         }
@@ -1061,7 +1066,8 @@ int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double 
     if (ge) {
         if (cudaGraphLaunch(ge, stream) != cudaSuccess) return check_launch("peer-memory series graph");
     } else {
-        for (int k = 1; k < ndd; k += S.tb ? 2 : 1) {
+        // one launch pair per node at most (a two-node series may run one-node passes)
+        for (int k = 1; k < ndd; ++k) {
             S.nf<<<S.lp.grid, S.lp.block, S.lp.smem, stream>>>(S.dparams);
             sf<<<(unsigned)S.pl.nslices, 256, 0, stream>>>(S.dparams);
         }

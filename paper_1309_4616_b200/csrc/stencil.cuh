@@ -77,6 +77,11 @@ struct SeriesParams {
     double *xgp[2];                     // this rank's gathered vector by parity (node k gathers from xgp[k & 1])
     double *const *rank_xg;             // [nranks] -> every rank's gathered-vector buffer (parity 1 at + npad)
     int64_t row_off, npad;
+    // two-node series: after a pass whose second node met the term test once
+    // (consecutive == 1), run the next node alone (a one-node tb pass) -- the
+    // series usually stops there, and a two-node pass would compute a node
+    // nobody reads.  Decisions are unchanged (bitwise).
+    int tail1;
 };
 
 // One pass: what a node (or a plain fused apply) reads and writes.

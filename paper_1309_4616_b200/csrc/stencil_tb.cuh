@@ -276,6 +276,9 @@ struct Ring {
 };
 
 // w_k at a window pair whose stencils need no ghost handling
+// (Dirichlet: also at window points outside the domain, which the caller
+// masks to the zero ghost -- a sampled coefficient is then read at the
+// clamped point, the value is discarded)
 template <int COEFF, bool GD>
 ES_DEV double2 tb_fast_pair(const Geom &g, const double *Wm, const double *Wc, const double *Wp, const double *Gj,
                             int ey, int ex, int64_t x, int64_t y, int j, double alpha, double beta) {
@@ -287,7 +290,11 @@ ES_DEV double2 tb_fast_pair(const Geom &g, const double *Wm, const double *Wc, c
     const double2 zp = *reinterpret_cast<const double2 *>(Wp + o);
     double l0 = lap7(c.x, Wc[o - 1], c.y, ym.x, yp.x, zm.x, zp.x, g.wx, g.wy, g.wz);
     double l1 = lap7(c.y, c.x, Wc[o + 2], ym.y, yp.y, zm.y, zp.y, g.wx, g.wy, g.wz);
-    if constexpr (COEFF != ES_COEFF_NONE) {
+    if constexpr (COEFF == ES_COEFF_ARRAY) {
+        const int64_t xc = min(max(x, (int64_t)0), g.nx - 2), yc = min(max(y, (int64_t)0), g.ny - 1);
+        l0 = mul(tb_coeff<COEFF>(g, xc, yc, j), l0);
+        l1 = mul(tb_coeff<COEFF>(g, xc + 1, yc, j), l1);
+    } else if constexpr (COEFF != ES_COEFF_NONE) {
         l0 = mul(tb_coeff<COEFF>(g, x, y, j), l0);
         l1 = mul(tb_coeff<COEFF>(g, x + 1, y, j), l1);
     }
@@ -337,12 +344,15 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const TbItem
             break;
         }
         const TbItem it = tb_item_at(its, i);
-        bool fast[3];
+        bool fast[3], in0[3], in1[3];
 #pragma unroll
         for (int h = 0; h < 3; ++h) {
             const int64_t x = it.x0 - 2 + pex[h], y = it.y0 - 1 + pey[h];
             const int64_t lo = neu ? 1 : 0, xhi = neu ? g.nx - 2 : g.nx - 1, yhi = neu ? g.ny - 2 : g.ny - 1;
             fast[h] = x >= lo && x + 1 <= xhi && y >= lo && y <= yhi;
+            const bool yin = y >= 0 && y < g.ny;
+            in0[h] = yin && x >= 0 && x < g.nx;
+            in1[h] = yin && x + 1 >= 0 && x + 1 < g.nx;
         }
         // W slots of planes j-1, j, j+1 (plane mb-2 is at wr)
         Ring<Lt::SW> rm = wr, rc = wr;
@@ -364,7 +374,27 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const TbItem
             if (j == it.mb - 1 && a == 0) vitem[vr.slot] = i;
             const bool zin = (j >= 0 || has_lo) && (j < its.L || has_hi);
             bool arrive_prev = false;
-            if (zin) {
+            if (zin && !neu) {
+                // Dirichlet: every pair by the ghost-free formula (TMA's zero
+                // fill is the ghost of w_{k-1}), points outside the domain
+                // masked to w_k's zero ghost.  Straight-line code, so the
+                // three pairs' loads and fp64 chains interleave.  A thread
+                // without a third pair computes one at a valid window spot
+                // and does not store it.
+                double2 wk[3];
+#pragma unroll
+                for (int h = 0; h < 3; ++h) {
+                    const int ey = pey[h] < 0 ? 0 : pey[h], ex = pex[h];
+                    const int64_t x = it.x0 - 2 + ex, y = it.y0 - 1 + ey;
+                    wk[h] = tb_fast_pair<COEFF, GD>(g, Wm, Wc, Wp, Gj, ey, ex, x, y, j, alpha, beta_k);
+                }
+#pragma unroll
+                for (int h = 0; h < 3; ++h) {
+                    if (pey[h] < 0) continue;
+                    const double2 w = make_double2(in0[h] ? wk[h].x : 0.0, in1[h] ? wk[h].y : 0.0);
+                    *reinterpret_cast<double2 *>(Vj + pey[h] * TB_EX + pex[h]) = w;
+                }
+            } else if (zin) {
 #pragma unroll
                 for (int h = 0; h < 3; ++h) {
                     const int ey = pey[h], ex = pex[h];
@@ -418,8 +448,8 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
     const double *vwin = reinterpret_cast<const double *>(smem + Lt::V_OFF);
     const int c = threadIdx.x - TB_NA, cw = c >> 5, q = c & 31;  // rows cw and cw + TB_CW, pair x0 + 2q
     const int64_t plane = g.nx * g.ny;
-    const int pass = (k - 1) / 2;
-    double *w1_dst = P->wbuf[pass & 1];
+    const int pass = P->state->pass;
+    double *w1_dst = P->wbuf[pass & 1];  // w_{k+1}, or w_k on a one-node pass
     double *pk_dst = P->pbuf[k & 1], *pk1_dst = P->pbuf[(k + 1) & 1];
     const double alpha = P->alpha, dk = P->dd[k];
     const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
@@ -462,8 +492,9 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                     const double p0 = k == 1 ? mul(pscale, po.x) : po.x, p1 = k == 1 ? mul(pscale, po.y) : po.y;
                     pk_cur[2 * h] = add(p0, mul(dk, vk.x));
                     pk_cur[2 * h + 1] = add(p1, mul(dk, vk.y));
-                    *reinterpret_cast<double2 *>(pk_dst + j * plane + ya[h] * g.nx + xa) =
-                        make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
+                    const int64_t off = j * plane + ya[h] * g.nx + xa;
+                    *reinterpret_cast<double2 *>(pk_dst + off) = make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
+                    if (!two) *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
                     acc_w0[h] = add(acc_w0[h], add(mul(vk.x, vk.x), mul(vk.y, vk.y)));
                     acc_p0[h] = add(acc_p0[h], add(mul(pk_cur[2 * h], pk_cur[2 * h]),
                                                    mul(pk_cur[2 * h + 1], pk_cur[2 * h + 1])));
@@ -558,13 +589,16 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
 template <int COEFF, bool GD>
 ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
     using Lt = TbLayout<GD>;
-    const Geom &g = P->g;
+    // a private copy: the ring waits' memory clobbers would otherwise make
+    // every use of a weight / extent a reload from the parameter block
+    const Geom g = P->g;
     const TbItems its = tb_items_of(g, P->chunk_len);
     const TmaMaps &M = *static_cast<const TmaMaps *>(P->maps);
-    const int pass = (k - 1) / 2;
-    // W: w_{k-1} (v on the first pass); P: p_{k-1}, or v on the first pass (p_0 = dd_0 v)
+    const int pass = P->state->pass;
+    // W: w_{k-1} (v on the first pass; pass p writes wbuf[p & 1]); P: p_{k-1}
+    // (pbuf[(k - 1) & 1]), or v on the first pass (p_0 = dd_0 v)
     TbMaps mp{&M.m[pass == 0 ? MAP_T_V : (pass & 1) ? MAP_T_0 : MAP_T_1], &M.m[MAP_T_G],
-              &M.m[pass == 0 ? MAP_T_PV : MAP_T_P0]};
+              &M.m[k == 1 ? MAP_T_PV : ((k - 1) & 1) ? MAP_T_P1 : MAP_T_P0]};
     if (g.halo_lo) mp.hlo = &M.m[(pass & 1) ? MAP_T_HLO1 : MAP_T_HLO0];  // pass p reads halo parity p & 1
     if (g.halo_hi) mp.hhi = &M.m[(pass & 1) ? MAP_T_HHI1 : MAP_T_HHI0];
     if (GD && g.halo_lo) mp.glo = &M.m[MAP_T_GLO];

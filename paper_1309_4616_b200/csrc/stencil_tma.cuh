@@ -52,7 +52,7 @@ enum {
     // two-node pass (stencil_tb.cuh): w tiles with a two-point halo, g' tiles with a one-point halo
     MAP_T_V, MAP_T_0, MAP_T_1, MAP_T_G, MAP_T_PV,
     // two-node pass on a peer-memory slab: two-plane w halos by parity, g' boundary planes
-    MAP_T_HLO0, MAP_T_HLO1, MAP_T_HHI0, MAP_T_HHI1, MAP_T_GLO, MAP_T_GHI, MAP_T_P0, MAP_COUNT
+    MAP_T_HLO0, MAP_T_HLO1, MAP_T_HHI0, MAP_T_HHI1, MAP_T_GLO, MAP_T_GHI, MAP_T_P0, MAP_T_P1, MAP_COUNT
 };
 
 struct alignas(64) TmaMaps {

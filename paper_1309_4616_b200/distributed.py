@@ -392,9 +392,9 @@ class _PeerMemory:
         rc = self.lib.es_leja_fetch(ptr(ws), ctypes.byref(res), stream_handle())
         if rc != _lib.ES_ERR_NOT_CONVERGED:
             _lib.check(rc, "es_leja_fetch")
-        # round 0 + one per node (one per two-node pass), identical on every rank
-        k = int(res.matvecs)
-        self.rounds += ((k + 1) // 2 if getattr(self, "two", False) else k) + 1
+        # round 0 + one per pass over the slab (a node, or two nodes sharing a
+        # pass), identical on every rank
+        self.rounds += int(res.passes) + 1
         return res
 
     def run(self, enqueue, ws):

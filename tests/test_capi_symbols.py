@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load(require_device=False)
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.es_abi_version() == 1
+    assert lib.es_abi_version() == 2
 
 
 def test_device_query_never_errors():
@@ -37,7 +37,7 @@ def test_device_query_never_errors():
 def test_struct_layouts():
     # es_stencil_desc: 5 x i64 + 3 x f64 + 2 x i32 + 7 pointers
     assert ctypes.sizeof(_lib.StencilDesc) == 5 * 8 + 3 * 8 + 2 * 4 + 7 * 8
-    assert ctypes.sizeof(_lib.SeriesResult) == 4 + 4 + 8 + 8
+    assert ctypes.sizeof(_lib.SeriesResult) == 4 + 4 + 8 + 8 + 4 + 4
 
 
 def test_bad_descriptor_rejected_without_gpu():
