@@ -447,7 +447,8 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
     const volatile int *vitem = reinterpret_cast<const volatile int *>(smem + Lt::VITEM_OFF);
     const double *vwin = reinterpret_cast<const double *>(smem + Lt::V_OFF);
     const int c = threadIdx.x - TB_NA, cw = c >> 5, q = c & 31;  // rows cw and cw + TB_CW, pair x0 + 2q
-    const int64_t plane = g.nx * g.ny;
+    const int64_t nx = g.nx, plane = g.nx * g.ny;
+    const double wx = g.wx, wy = g.wy, wz = g.wz;
     const int pass = P->state->pass;
     double *w1_dst = P->wbuf[pass & 1];  // w_{k+1}, or w_k on a one-node pass
     double *pk_dst = P->pbuf[k & 1], *pk1_dst = P->pbuf[(k + 1) & 1];
@@ -473,11 +474,18 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
         }
         double acc_w0[2] = {0.0, 0.0}, acc_p0[2] = {0.0, 0.0}, acc_w1[2] = {0.0, 0.0}, acc_p1[2] = {0.0, 0.0};
         double pk_prev[4] = {0.0, 0.0, 0.0, 0.0};
-        uint32_t s2 = 0, s1 = 0;  // V slots of planes j-2, j-1
+        // w_k at this thread's pairs of planes j-2, j-1 (centre values kept in
+        // registers across planes: the zm / c of the next plane's stencil)
+        double2 vm1[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}, vc1[2] = {vm1[0], vm1[1]};
+        uint32_t s1 = 0;  // V slot of plane j-1
         for (int j = it.mb - 1; j <= it.me; ++j) {
             if (j > it.mb - 1) mbar_wait(&B.vfull[vr.slot], vr.phase);
             const uint32_t s0 = vr.slot;
             const double *Vj = vslot(s0);
+            double2 vcur[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                vcur[h] = *reinterpret_cast<const double2 *>(Vj + (cw + TB_CW * h + 1) * TB_EX + 2 * q + 2);
             // ---- B: p_k of plane j (+ node k norms)
             double pk_cur[4] = {0.0, 0.0, 0.0, 0.0};
             if (j >= it.mb && j < it.me) {
@@ -485,19 +493,20 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                 const double *Pc = reinterpret_cast<const double *>(smem + Lt::P_OFF + pr.slot * Lt::P_STAGE);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    if (!act[h]) continue;
                     const int r = cw + TB_CW * h;
-                    const double2 vk = *reinterpret_cast<const double2 *>(Vj + (r + 1) * TB_EX + 2 * q + 2);
+                    const double2 vk = vcur[h];
                     const double2 po = *reinterpret_cast<const double2 *>(Pc + r * 64 + 2 * q);
                     const double p0 = k == 1 ? mul(pscale, po.x) : po.x, p1 = k == 1 ? mul(pscale, po.y) : po.y;
                     pk_cur[2 * h] = add(p0, mul(dk, vk.x));
                     pk_cur[2 * h + 1] = add(p1, mul(dk, vk.y));
-                    const int64_t off = j * plane + ya[h] * g.nx + xa;
-                    *reinterpret_cast<double2 *>(pk_dst + off) = make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
-                    if (!two) *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
-                    acc_w0[h] = add(acc_w0[h], add(mul(vk.x, vk.x), mul(vk.y, vk.y)));
-                    acc_p0[h] = add(acc_p0[h], add(mul(pk_cur[2 * h], pk_cur[2 * h]),
-                                                   mul(pk_cur[2 * h + 1], pk_cur[2 * h + 1])));
+                    if (act[h]) {
+                        const int64_t off = j * plane + ya[h] * nx + xa;
+                        *reinterpret_cast<double2 *>(pk_dst + off) = make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
+                        if (!two) *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
+                        acc_w0[h] = add(acc_w0[h], add(mul(vk.x, vk.x), mul(vk.y, vk.y)));
+                        acc_p0[h] = add(acc_p0[h], add(mul(pk_cur[2 * h], pk_cur[2 * h]),
+                                                       mul(pk_cur[2 * h + 1], pk_cur[2 * h + 1])));
+                    }
                 }
                 warp_arrive(&B.pempty[pr.slot]);
                 pr.next();
@@ -505,7 +514,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
             // ---- C: w_{k+1}, p_{k+1} of plane j-1 (+ node k+1 norms); both rows side by side
             const int jc = j - 1;
             if (two && jc >= it.mb && jc < it.me) {
-                const double *Vm = vslot(s2), *Vc = vslot(s1), *Vp = Vj;
+                const double *Vc = vslot(s1);
                 const double *Gc = nullptr;
                 if constexpr (GD) {
                     mbar_wait(&B.gfull[gr.slot], gr.phase);  // complete already; orders the TMA bytes for C
@@ -516,13 +525,11 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                 for (int h = 0; h < 2; ++h) {
                     const int r = cw + TB_CW * h;
                     const int o = (r + 1) * TB_EX + 2 * q + 2;
-                    const double2 cc = *reinterpret_cast<const double2 *>(Vc + o);
+                    const double2 cc = vc1[h], zm = vm1[h], zp = vcur[h];
                     const double2 ym = *reinterpret_cast<const double2 *>(Vc + o - TB_EX);
                     const double2 yp = *reinterpret_cast<const double2 *>(Vc + o + TB_EX);
-                    const double2 zm = *reinterpret_cast<const double2 *>(Vm + o);
-                    const double2 zp = *reinterpret_cast<const double2 *>(Vp + o);
-                    double l0 = lap7(cc.x, Vc[o - 1], cc.y, ym.x, yp.x, zm.x, zp.x, g.wx, g.wy, g.wz);
-                    double l1 = lap7(cc.y, cc.x, Vc[o + 2], ym.y, yp.y, zm.y, zp.y, g.wx, g.wy, g.wz);
+                    double l0 = lap7(cc.x, Vc[o - 1], cc.y, ym.x, yp.x, zm.x, zp.x, wx, wy, wz);
+                    double l1 = lap7(cc.y, cc.x, Vc[o + 2], ym.y, yp.y, zm.y, zp.y, wx, wy, wz);
                     if constexpr (COEFF != ES_COEFF_NONE) {
                         l0 = mul(tb_coeff<COEFF>(g, xa, ya[h], jc), l0);
                         l1 = mul(tb_coeff<COEFF>(g, xa + 1, ya[h], jc), l1);
@@ -540,7 +547,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     if (!act[h]) continue;
-                    const int64_t off = jc * plane + ya[h] * g.nx + xa;
+                    const int64_t off = jc * plane + ya[h] * nx + xa;
                     *reinterpret_cast<double2 *>(w1_dst + off) = make_double2(wn[2 * h], wn[2 * h + 1]);
                     *reinterpret_cast<double2 *>(pk1_dst + off) = make_double2(pn[2 * h], pn[2 * h + 1]);
                     acc_w1[h] = add(acc_w1[h], add(mul(wn[2 * h], wn[2 * h]), mul(wn[2 * h + 1], wn[2 * h + 1])));
@@ -553,15 +560,18 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                     gr.next();
                 }
             }
-            if (j - 2 >= it.mb - 1) warp_arrive(&B.vempty[s2]);  // V(j-2)
+            if (j - 1 >= it.mb - 1) warp_arrive(&B.vempty[s1]);  // V(j-1): its neighbours were last read above
 #pragma unroll
             for (int e = 0; e < 4; ++e) pk_prev[e] = pk_cur[e];
-            s2 = s1;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                vm1[h] = vc1[h];
+                vc1[h] = vcur[h];
+            }
             s1 = s0;
             vr.next();
         }
-        warp_arrive(&B.vempty[s2]);  // V(me-1), V(me)
-        warp_arrive(&B.vempty[s1]);
+        warp_arrive(&B.vempty[s1]);  // V(me)
         if constexpr (GD) {  // G(me)
             warp_arrive(&B.gempty[gr.slot]);
             gr.next();
