@@ -384,6 +384,7 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const TbItem
                 double2 wk[3];
 #pragma unroll
                 for (int h = 0; h < 3; ++h) {
+                    if (h == 2 && a >= (TB_PAIRS - 2 * TB_NA + 31) / 32 * 32) break;  // no third pair in this warp
                     const int ey = pey[h] < 0 ? 0 : pey[h], ex = pex[h];
                     const int64_t x = it.x0 - 2 + ex, y = it.y0 - 1 + ey;
                     wk[h] = tb_fast_pair<COEFF, GD>(g, Wm, Wc, Wp, Gj, ey, ex, x, y, j, alpha, beta_k);
@@ -474,10 +475,14 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
         }
         double acc_w0[2] = {0.0, 0.0}, acc_p0[2] = {0.0, 0.0}, acc_w1[2] = {0.0, 0.0}, acc_p1[2] = {0.0, 0.0};
         double pk_prev[4] = {0.0, 0.0, 0.0, 0.0};
+        // element offsets of this thread's two rows in plane j (advanced by a plane per iteration)
+        int64_t off0 = (int64_t)(it.mb - 1) * plane + ya[0] * nx + xa;
+        const int64_t drow = (int64_t)TB_CW * nx;  // row h = 1 is TB_CW rows below row 0
         // w_k at this thread's pairs of planes j-2, j-1 (centre values kept in
         // registers across planes: the zm / c of the next plane's stencil)
         double2 vm1[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}, vc1[2] = {vm1[0], vm1[1]};
         uint32_t s1 = 0;  // V slot of plane j-1
+#pragma unroll 2
         for (int j = it.mb - 1; j <= it.me; ++j) {
             if (j > it.mb - 1) mbar_wait(&B.vfull[vr.slot], vr.phase);
             const uint32_t s0 = vr.slot;
@@ -496,11 +501,12 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                     const int r = cw + TB_CW * h;
                     const double2 vk = vcur[h];
                     const double2 po = *reinterpret_cast<const double2 *>(Pc + r * 64 + 2 * q);
-                    const double p0 = k == 1 ? mul(pscale, po.x) : po.x, p1 = k == 1 ? mul(pscale, po.y) : po.y;
+                    // pscale is 1.0 after the first pass, and 1.0 * x == x bit for bit
+                    const double p0 = mul(pscale, po.x), p1 = mul(pscale, po.y);
                     pk_cur[2 * h] = add(p0, mul(dk, vk.x));
                     pk_cur[2 * h + 1] = add(p1, mul(dk, vk.y));
                     if (act[h]) {
-                        const int64_t off = j * plane + ya[h] * nx + xa;
+                        const int64_t off = off0 + h * drow;
                         *reinterpret_cast<double2 *>(pk_dst + off) = make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
                         if (!two) *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
                         acc_w0[h] = add(acc_w0[h], add(mul(vk.x, vk.x), mul(vk.y, vk.y)));
@@ -547,7 +553,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     if (!act[h]) continue;
-                    const int64_t off = jc * plane + ya[h] * nx + xa;
+                    const int64_t off = off0 - plane + h * drow;  // plane jc = j - 1
                     *reinterpret_cast<double2 *>(w1_dst + off) = make_double2(wn[2 * h], wn[2 * h + 1]);
                     *reinterpret_cast<double2 *>(pk1_dst + off) = make_double2(pn[2 * h], pn[2 * h + 1]);
                     acc_w1[h] = add(acc_w1[h], add(mul(wn[2 * h], wn[2 * h]), mul(wn[2 * h + 1], wn[2 * h + 1])));
@@ -570,6 +576,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
             }
             s1 = s0;
             vr.next();
+            off0 += plane;
         }
         warp_arrive(&B.vempty[s1]);  // V(me)
         if constexpr (GD) {  // G(me)
