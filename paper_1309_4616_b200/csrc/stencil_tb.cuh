@@ -361,6 +361,7 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const TbItem
         rp.next();
         mbar_wait(&B.wfull[rc.slot], rc.phase);
         uint32_t v_prev = 0;  // slot of V(j-1)
+#pragma unroll 2
         for (int j = it.mb - 1; j <= it.me; ++j) {
             mbar_wait(&B.wfull[rp.slot], rp.phase);
             const double *Wm = wst(rm.slot), *Wc = wst(rc.slot), *Wp = wst(rp.slot);
