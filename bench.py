@@ -580,13 +580,18 @@ def run_b200(args, cfg):
     two = not is_csr(cfg) and getattr(step.problem.operator, "two_node_passes", lambda: False)()
     if two:
         passes = max(tm.passes(), 1)
+        two_p, one_p = tm.pass_mix()
         launch_s = series_s / passes
-        bytes_launch = (cfg["bytes_per_node"] + 8) * n_local  # read w, p (+g'); write w'', p', p''
+        # a two-node pass reads w, p (+g') and writes w'', p', p''; the one-node
+        # tail pass of a series reads w, p (+g') and writes w', p'
+        bytes_all = (two_p * (cfg["bytes_per_node"] + 8) + one_p * cfg["bytes_per_node"]) * n_local
+        bytes_launch = bytes_all / passes
         achieved = bytes_launch / launch_s / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": profiled_traffic(args.config + "_tb"),
                     "kernel": "k_node_tb (two fused Leja nodes per HBM pass)", "bytes_per_launch": bytes_launch,
                     "bytes_per_point": bytes_launch / n_local, "launch_us": launch_s * 1e6, "launches": passes,
+                    "two_node_passes": two_p, "one_node_passes": one_p,
                     "node_us": node_s * 1e6,
                     "one_node_equiv_GBs": bytes_node / node_s / 1e9,
                     "note": "one-node algorithmic bytes (SURVEY 8(d)) per node time; above the HBM peak because "

@@ -642,7 +642,7 @@ class DistributedStencil:
             for _ in range(int(res.matvecs)):
                 self.ledger.record(self.comm.ledger_scalars(), 8)
             if tm:
-                tm.add(ev0, ev1, res.matvecs)
+                tm.add(ev0, ev1, res.matvecs, res.passes)
             del keep
             return res
         be = CudaSlabBackend(self.base_operator, self.comm, self._workspace(), self.halo_lo, self.halo_hi)
@@ -651,7 +651,7 @@ class DistributedStencil:
         be.begin(d, v, p_out, dd, xi, alpha, shift, tol, gdiag)
         res = drive_series(be, self.comm, dd.numel(), self.batch, self.ledger)
         if tm:
-            tm.add(ev0, timing.event(), res.matvecs)
+            tm.add(ev0, timing.event(), res.matvecs, res.passes)
         del keep
         return res
 
@@ -772,7 +772,7 @@ class DistributedCsr:
             for _ in range(int(res.matvecs)):
                 self.ledger.record(self.comm.ledger_scalars(), 8)
             if tm:
-                tm.add(ev0, ev1, res.matvecs)
+                tm.add(ev0, ev1, res.matvecs, res.passes)
             return res
         be = CudaRowBackend(self, self._workspace())
         tm = timing.active()
@@ -780,7 +780,7 @@ class DistributedCsr:
         be.begin(v, p_out, dd, xi, alpha, shift, tol)
         res = drive_series(be, self.comm, dd.numel(), self.batch, self.ledger)
         if tm:
-            tm.add(ev0, timing.event(), res.matvecs)
+            tm.add(ev0, timing.event(), res.matvecs, res.passes)
         return res
 
 

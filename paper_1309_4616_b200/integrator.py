@@ -257,7 +257,7 @@ class _StepWorkspace:
         mv_e, mv_p = int(res.exp_series.matvecs), int(res.phi1_series.matvecs)
         tm = timing.active()
         if tm:
-            tm.add_ms(res.series_ms, mv_e + mv_p)
+            tm.add_ms(res.series_ms, mv_e + mv_p, int(res.exp_series.passes) + int(res.phi1_series.passes))
         st = StepStats(matvecs=mv_e + mv_p, matvecs_exp=mv_e, matvecs_phi1=mv_p, degree_exp=mv_e, degree_phi1=mv_p)
         return out, st
 
@@ -513,7 +513,7 @@ class RosenbrockStepper:
         mv = int(res.phi1_series.matvecs)
         tm = timing.active()
         if tm:
-            tm.add_ms(res.series_ms, mv)
+            tm.add_ms(res.series_ms, mv, int(res.phi1_series.passes))
         return out, RosenbrockStats(matvecs=mv, matvecs_phi1=mv, degree_phi1=mv, interval=(lo, hi))
 
     def step(self, u: torch.Tensor, t: float, h: float):

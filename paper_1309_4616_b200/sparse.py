@@ -160,7 +160,7 @@ class CsrMatrix:
         if rc != _lib.ES_ERR_NOT_CONVERGED:
             _lib.check(rc, "es_leja_fetch")
         if tm:
-            tm.add(ev0, ev1, res.matvecs)
+            tm.add(ev0, ev1, res.matvecs, res.passes)
         return res
 
     def _leja(self, v, p_out, dd, xi, alpha, shift, tol, gdiag=None):
@@ -184,7 +184,7 @@ class CsrMatrix:
         if rc != _lib.ES_ERR_NOT_CONVERGED:
             _lib.check(rc, "es_leja_fetch")
         if tm:
-            tm.add(ev0, ev1, res.matvecs)
+            tm.add(ev0, ev1, res.matvecs, res.passes)
         return res
 
     def __repr__(self):

@@ -228,7 +228,7 @@ class StencilOperator:
         if rc != _lib.ES_ERR_NOT_CONVERGED:
             _lib.check(rc, "es_leja_fetch")
         if tm:
-            tm.add(ev0, ev1, res.matvecs)
+            tm.add(ev0, ev1, res.matvecs, res.passes)
         del keep
         return res
 

@@ -1101,3 +1101,46 @@ def test_two_node_pass_edges_vs_oracle(dims, bc, nodes, monkeypatch):
     ref, _ = orc.newton_stencil(spec, orc.Interp(lo, hi, "phi1", -2e-4, it.xi, it.dd), v, 0.0, gdiag=gd)
     assert mv == nodes
     assert np.asarray(p).tobytes() == ref.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("graph", [True, False])
+def test_two_node_tail_pass_bitwise(graph, monkeypatch):
+    """A two-node series runs node k alone when node k-1 met the term test
+    for the first time (the series then usually stops at k).  Over a sweep
+    of tolerances -- stops at odd and even k, and first hits that do not
+    stop (the pass pairing then shifts by one) -- p and the matvec counts
+    equal the plain two-node and the one-node series bit for bit, and the
+    pass count never exceeds the plain pairing's."""
+    from paper_1309_4616_b200 import timing
+
+    if not graph:
+        monkeypatch.setenv("ES_NO_GRAPH", "1")
+    g = es.Grid3D(72, 40, 44)
+    op = es.StencilOperator(g, BCS["homogeneous"])
+    iv = es.gershgorin_interval(op).widened(30.0)
+    rng = np.random.default_rng(12)
+    v = torch.from_numpy(rng.standard_normal(g.n)).cuda()
+    gdiag = torch.from_numpy(rng.random(g.n) * 30.0).cuda()
+    it = es.make_interpolant(iv, "phi1", -3e-4, 60, 1e-8)
+    stops = set()
+    for tol in np.logspace(-13, -3, 31):
+        runs = {}
+        for tb, tail in (("0", "1"), ("1", "0"), ("1", "1")):
+            monkeypatch.setenv("ES_TB", tb)
+            monkeypatch.setenv("ES_TB_TAIL", tail)
+            with timing.SeriesTimer() as tm:
+                p, mv = es.newton_apply(op, it, v, float(tol), gdiag=gdiag)
+            runs[(tb, tail)] = (p, mv, tm.passes())
+        p0, m0, _ = runs[("0", "1")]
+        for key in (("1", "0"), ("1", "1")):
+            p, m, _ = runs[key]
+            assert m == m0, (tol, key, m, m0)
+            assert torch.equal(p, p0), (tol, key)
+        plain, tail = runs[("1", "0")][2], runs[("1", "1")][2]
+        assert plain == (m0 + 1) // 2, (tol, plain, m0)
+        assert tail <= plain + 1 and 2 * tail >= m0, (tol, tail, plain, m0)
+        stops.add(m0 & 1)
+    monkeypatch.delenv("ES_TB")
+    monkeypatch.delenv("ES_TB_TAIL")
+    assert stops == {0, 1}, stops
