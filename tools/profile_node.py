@@ -29,14 +29,14 @@ if a.config == "C5":
     torch.cuda.synchronize()
     print("nodes", mv)
     sys.exit(0)
-dims = {"C3": (512, 512, 512), "C2": (4096, 4096, 1), "C4": (1024, 1024, 1024)}[a.config]
+dims = {"C3": (512, 512, 512), "C2": (4096, 4096, 1), "C4": (1024, 1024, 1024), "C1": (256, 256, 1)}[a.config]
 g = es.Grid3D(*dims)
 bc = es.BoundaryCondition.neumann() if a.config == "C2" else es.BoundaryCondition.homogeneous()
 op = es.StencilOperator(g, bc, coeff=es.radial_coeff if a.config == "C2" else None)
 lo, hi = es.gershgorin_bounds(op)
 it = es.make_interpolant(es.SpectralInterval(lo, hi), "phi1", -2.5e-5, a.nodes, 1e-8)
 v = torch.rand(g.n, dtype=torch.float64, device="cuda")
-gd = torch.rand(g.n, dtype=torch.float64, device="cuda") if a.config != "C2" else None
+gd = torch.rand(g.n, dtype=torch.float64, device="cuda") if a.config in ("C3", "C4") else None
 for _ in range(2):
     p, mv = es.newton_apply(op, it, v, 0.0, gdiag=gd)
 torch.cuda.synchronize()
