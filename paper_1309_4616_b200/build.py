@@ -21,7 +21,7 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libexpstencil_b200.so")
-SOURCES = ["capi.cu", "stencil.cu", "csr.cu", "pointwise.cu", "graph.cu", "f32.cu", "step.cu", "csr_generic.cu"]
+SOURCES = ["capi.cu", "stencil.cu", "csr.cu", "pointwise.cu", "graph.cu", "f32.cu", "step.cu", "csr_generic.cu", "series_small.cu"]
 HEADERS = ["es_common.cuh", "es_host.h", "stencil.cuh", "series.cuh", "stencil_tma.cuh", "stencil_tb.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

@@ -37,19 +37,23 @@ int current_device() {
 
 struct Pinned {
     int device = -1;
-    SeriesState *host = nullptr;
+    SeriesState *host = nullptr;  // [2]
+    unsigned long long *word = nullptr;
 };
 static thread_local Pinned t_pinned;
 
-int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaStream_t stream) {
-    Pinned &p = t_pinned;
-    if (p.device != current_device() || !p.host) {
-        if (cudaMallocHost(&p.host, sizeof(SeriesState)) != cudaSuccess) return check_launch("pinned state");
-        p.device = current_device();
+static int pinned(Pinned *&p) {
+    p = &t_pinned;
+    if (p->device != current_device() || !p->host) {
+        if (cudaMallocHost(&p->host, 2 * sizeof(SeriesState)) != cudaSuccess ||
+            cudaMallocHost(&p->word, sizeof(unsigned long long)) != cudaSuccess)
+            return check_launch("pinned state");
+        p->device = current_device();
     }
-    cudaMemcpyAsync(p.host, state_dev, sizeof(SeriesState), cudaMemcpyDeviceToHost, stream);
-    if (cudaStreamSynchronize(stream) != cudaSuccess) return check_launch("series sync");
-    const SeriesState &st = *p.host;
+    return ES_OK;
+}
+
+static int state_result(const SeriesState &st, es_series_result *res) {
     res->matvecs = st.k;
     res->converged = st.converged;
     res->last_term = st.last_term;
@@ -61,6 +65,31 @@ int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaS
         return set_error(ES_ERR_CUDA, "peer-memory series: a peer did not arrive within the timeout (node %d)", st.k);
     if (!st.converged)
         return set_error(ES_ERR_NOT_CONVERGED, "Newton series did not converge within degree %d", st.k);
+    return ES_OK;
+}
+
+int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaStream_t stream) {
+    Pinned *p;
+    int rc = pinned(p);
+    if (rc) return rc;
+    cudaMemcpyAsync(p->host, state_dev, sizeof(SeriesState), cudaMemcpyDeviceToHost, stream);
+    if (cudaStreamSynchronize(stream) != cudaSuccess) return check_launch("series sync");
+    return state_result(p->host[0], res);
+}
+
+int read_series_states2(const SeriesState *a, es_series_result *ra, int *rc_a, const SeriesState *b,
+                        es_series_result *rb, int *rc_b, const unsigned long long *word_dev,
+                        unsigned long long *word_host, cudaStream_t stream) {
+    Pinned *p;
+    int rc = pinned(p);
+    if (rc) return rc;
+    cudaMemcpyAsync(p->host, a, sizeof(SeriesState), cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(p->host + 1, b, sizeof(SeriesState), cudaMemcpyDeviceToHost, stream);
+    if (word_dev) cudaMemcpyAsync(p->word, word_dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
+    if (cudaStreamSynchronize(stream) != cudaSuccess) return check_launch("series sync");
+    if (word_dev) *word_host = *p->word;
+    *rc_a = state_result(p->host[0], ra);
+    *rc_b = state_result(p->host[1], rb);
     return ES_OK;
 }
 

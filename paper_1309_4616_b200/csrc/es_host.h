@@ -31,6 +31,11 @@ SeriesState *series_state_ptr(void *ws);
 size_t series_state_offset();
 void launch_state_trivial(void *ws, cudaStream_t stream);
 int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaStream_t stream);
+// two series' states (and optionally one device word) with ONE stream sync;
+// returns each series' own read_series_state status in rc_a / rc_b
+int read_series_states2(const SeriesState *a, es_series_result *ra, int *rc_a, const SeriesState *b,
+                        es_series_result *rb, int *rc_b, const unsigned long long *word_dev,
+                        unsigned long long *word_host, cudaStream_t stream);
 
 struct StencilPlan {
     bool tma;  // v2 TMA-pipelined kernel (else the register-queue v1 kernel)
@@ -96,6 +101,23 @@ int run_exprb_finish(const es_stencil_desc *d, const double *u, double *u_out, c
                      int ndd, double alpha, double shift, double tol, double h, const double *scratch, void *ws,
                      size_t ws_bytes, es_step_result *res, cudaStream_t s);
 int launch_combustion(const double *u, double *out, int64_t n, unsigned long long *bad_dev, cudaStream_t st);
+int launch_fill_u64(unsigned long long *p, unsigned long long a, unsigned long long b, cudaStream_t st);
+
+// persistent small-grid series (series_small.cu)
+struct SeriesParams;
+bool small_series_ok(const es_stencil_desc *d, const StencilPlan &pl, bool gd, int nseries);
+int small_prepare(const es_stencil_desc *d, const double *v, double *p_out, const double *dd, const double *xi,
+                  int ndd, double alpha, double shift, double tol, const double *gdiag, void *ws, size_t ws_bytes,
+                  int nseries, SeriesParams *hp, SeriesParams **dparams, StencilPlan *plan, bool *ok,
+                  cudaStream_t stream);
+int launch_series_init(const SeriesParams *hp, SeriesParams *dparams, cudaStream_t stream);
+int launch_expeuler_small_init(const SeriesParams *ha, SeriesParams *da, const SeriesParams *hb, SeriesParams *db,
+                               unsigned long long *bad, int64_t n, cudaStream_t stream);
+int launch_series_small(const es_stencil_desc *d, const SeriesParams *dparams, const StencilPlan &pl, bool gd,
+                        cudaStream_t stream);
+int launch_expeuler_small(const es_stencil_desc *d, const SeriesParams *pa, const SeriesParams *pb,
+                          const StencilPlan &pl, const double *u, double *gn, const double *source, int nonlin,
+                          double h, unsigned long long *bad, cudaStream_t stream);
 int launch_axpy(const double *y, const double *z, double h, double *out, int64_t n, cudaStream_t st);
 int launch_scale(const double *x, double s, double *out, int64_t n, cudaStream_t st);
 int launch_combustion_f32(const float *u, float *out, int64_t n, cudaStream_t stream);

@@ -105,6 +105,11 @@ int launch_combustion(const double *u, double *out, int64_t n, unsigned long lon
     return check_launch("combustion");
 }
 
+int launch_fill_u64(unsigned long long *p, unsigned long long a, unsigned long long b, cudaStream_t st) {
+    k_fill_u64<<<1, 32, 0, st>>>(p, a, b);
+    return check_launch("fill");
+}
+
 int launch_axpy(const double *y, const double *z, double h, double *out, int64_t n, cudaStream_t st) {
     if (n > 0) k_axpy<<<grid_for(n), 256, 0, st>>>(y, z, h, out, n);
     return check_launch("axpy");

@@ -223,6 +223,26 @@ ES_DEV bool tb_two(const SeriesParams &P, int k) {
     return !(P.tail1 && P.tol > 0.0 && P.state->consecutive == 1);
 }
 
+// Publish a series' parameters and clear its state and tickets (k_series_init,
+// and the merged init of the small-grid exponential-Euler step); the block's
+// threads share the ticket reset.
+ES_DEV void series_init_body(const SeriesParams &p, SeriesParams *dst) {
+    if (threadIdx.x == 0) {
+        *dst = p;
+        SeriesState &st = *p.state;
+        st.k = 0;
+        st.consecutive = 0;
+        st.pass = 0;
+        st.done = 0;
+        st.converged = 0;
+        st.last_term = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+        st.last_pnorm = 0.0;
+        *p.global_cnt = 0u;
+        if (p.work) *p.work = 0u;
+    }
+    for (int i = threadIdx.x; i < p.nchunks; i += blockDim.x) p.chunk_cnt[i] = 0u;
+}
+
 // Node k's pass description from the device state (k = last completed + 1).
 ES_DEV Pass node_pass(const SeriesParams &P, int k) {
     Pass ps;

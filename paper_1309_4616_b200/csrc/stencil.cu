@@ -277,22 +277,7 @@ __global__ void k_publish_maps(const TmaMaps maps, TmaMaps *dst) {
 }
 
 // Series prologue: publish the parameters, clear the state and the tickets.
-__global__ void k_series_init(const SeriesParams p, SeriesParams *dst) {
-    if (threadIdx.x == 0) {
-        *dst = p;
-        SeriesState &st = *p.state;
-        st.k = 0;
-        st.consecutive = 0;
-        st.pass = 0;
-        st.done = 0;
-        st.converged = 0;
-        st.last_term = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-        st.last_pnorm = 0.0;
-        *p.global_cnt = 0u;
-        if (p.work) *p.work = 0u;
-    }
-    for (int i = threadIdx.x; i < p.nchunks; i += blockDim.x) p.chunk_cnt[i] = 0u;
-}
+__global__ void k_series_init(const SeriesParams p, SeriesParams *dst) { series_init_body(p, dst); }
 
 // Series epilogue: the result lives in pbuf[k & 1]; move it to p_out
 // (pbuf[1]) when the last node was even.
@@ -749,7 +734,7 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
                           const double *halo_lo, const double *halo_hi, bool dist, void *ws, size_t ws_bytes,
                           SeriesSetup &S, cudaStream_t stream, const double *halo_lo_1 = nullptr,
                           const double *halo_hi_1 = nullptr, int allow_tb = 1, const double *g_lo = nullptr,
-                          const double *g_hi = nullptr) {
+                          const double *g_hi = nullptr, bool maps_needed = true) {
     S.n = d->nx * d->ny * d->lz;
     char *w = static_cast<char *>(ws);
     S.pl = plan_stencil(d, {v, p_out, gdiag, halo_lo, halo_hi, (const void *)(w + 0)}, true);
@@ -823,7 +808,7 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     hp.dist = dist ? 1 : 0;
     hp.tail1 = env_int("ES_TB_TAIL", 1) ? 1 : 0;
     S.dparams = reinterpret_cast<SeriesParams *>(w + L.params);
-    if (pl.tma) {
+    if (pl.tma && maps_needed) {
         TmaMaps maps;
         std::memset(&maps, 0, sizeof(maps));
         int rc = encode_w(&maps.m[MAP_WA_V], &maps.m[MAP_WB_V], v, d, pl.dim2);
@@ -863,6 +848,33 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     return ES_OK;
 }
 
+// Small single-plane grids: parameters of a persistent series
+// (series_small.cu) published like the graph path's, without TMA maps;
+// *ok = false when the persistent form does not apply.
+int small_prepare(const es_stencil_desc *d, const double *v, double *p_out, const double *dd, const double *xi,
+                  int ndd, double alpha, double shift, double tol, const double *gdiag, void *ws, size_t ws_bytes,
+                  int nseries, SeriesParams *hp, SeriesParams **dparams, StencilPlan *plan, bool *ok,
+                  cudaStream_t stream) {
+    *ok = false;
+    if (ndd < 2 || d->nx * d->ny * d->lz == 0) return ES_OK;
+    const StencilPlan pl = plan_stencil(d, {v, p_out, gdiag, (const void *)ws}, true);
+    if (!small_series_ok(d, pl, gdiag != nullptr, nseries)) return ES_OK;
+    SeriesSetup S;
+    const int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, nullptr, nullptr, false, ws,
+                                  ws_bytes, S, stream, nullptr, nullptr, 0, nullptr, nullptr, false);
+    if (rc) return rc;
+    *hp = S.hp;
+    *dparams = S.dparams;
+    *plan = S.pl;
+    *ok = true;
+    return ES_OK;
+}
+
+int launch_series_init(const SeriesParams *hp, SeriesParams *dparams, cudaStream_t stream) {
+    k_series_init<<<1, 256, 0, stream>>>(*hp, dparams);
+    return check_launch("series init");
+}
+
 int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out, const double *dd,
                        const double *xi, int ndd, double alpha, double shift, double tol,
                        const double *gdiag, void *ws, size_t ws_bytes, es_series_result *res,
@@ -878,6 +890,21 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
         int rc = check_launch("scale");
         if (rc || !res) return rc;
         return read_series_state(series_state_ptr(ws), res, stream);
+    }
+    {  // tiny grids: the whole series in one persistent launch (series_small.cu)
+        SeriesParams hp;
+        SeriesParams *dp = nullptr;
+        StencilPlan sp;
+        bool ok = false;
+        int rc = small_prepare(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, ws, ws_bytes, 1, &hp, &dp, &sp,
+                               &ok, stream);
+        if (rc) return rc;
+        if (ok) {
+            if ((rc = launch_series_init(&hp, dp, stream))) return rc;
+            if ((rc = launch_series_small(d, dp, sp, gdiag != nullptr, stream))) return rc;
+            if (!res) return ES_OK;
+            return read_series_state(hp.state, res, stream);
+        }
     }
     SeriesSetup S;
     int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, nullptr, nullptr, false, ws,

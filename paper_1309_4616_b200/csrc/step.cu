@@ -21,6 +21,7 @@
 
 #include "es_common.cuh"
 #include "es_host.h"
+#include "stencil.cuh"
 
 namespace es {
 
@@ -78,14 +79,44 @@ int run_expeuler_step(const es_stencil_desc *d, const double *u, double *u_out, 
     if (rc) return rc;
     const bool phi = nonlin == ES_NONLIN_COMBUSTION || source != nullptr;
     double *g = scratch, *z = scratch + n;
-    cudaEventRecord(f->t0, s);
+    // tiny grids: both series, g(u) - b and the combination in ONE persistent
+    // launch (series_small.cu); otherwise two concurrent series graphs
+    bool fused = false;
     if (phi) {
+        SeriesParams ha, hb;
+        SeriesParams *da = nullptr, *db = nullptr;
+        StencilPlan pa, pb;
+        bool oka = false, okb = false;
+        rc = small_prepare(d, u, u_out, dd_exp, xi, ndd_exp, alpha, shift, tol, nullptr, ws_exp, ws_bytes, 2, &ha, &da,
+                           &pa, &oka, s);
+        if (!rc && oka)
+            rc = small_prepare(d, g, z, dd_phi, xi, ndd_phi, alpha, shift, tol, nullptr, ws_phi, ws_bytes, 2, &hb, &db,
+                               &pb, &okb, s);
+        if (rc) return rc;
+        if (oka && okb && pa.nchunks == pb.nchunks && pa.chunk == pb.chunk) {
+            cudaEventRecord(f->t0, s);
+            if ((rc = launch_expeuler_small_init(&ha, da, &hb, db, f->bad, n, s))) return rc;
+            if ((rc = launch_expeuler_small(d, da, db, pa, u, g, source, nonlin, h, f->bad, s))) return rc;
+            cudaEventRecord(f->t1, s);
+            // both states and the domain word with one sync
+            int rca = ES_OK, rcb = ES_OK;
+            rc = read_series_states2(series_state_ptr(ws_exp), &res->exp_series, &rca, series_state_ptr(ws_phi),
+                                     &res->phi1_series, &rcb, f->bad, f->bad_host, s);
+            if (!rc) rc = series_status(rca, &res->status_exp);
+            if (!rc) rc = series_status(rcb, &res->status_phi1);
+            if (rc) return rc;
+            fused = true;
+        }
+    }
+    if (!fused) cudaEventRecord(f->t0, s);
+    if (phi && !fused) {
         cudaEventRecord(f->fork, s);
         cudaStreamWaitEvent(f->side, f->fork, 0);
     }
-    rc = run_stencil_series(d, u, u_out, dd_exp, xi, ndd_exp, alpha, shift, tol, nullptr, ws_exp, ws_bytes, nullptr,
-                            s);
-    if (!rc && phi) {
+    if (!fused)
+        rc = run_stencil_series(d, u, u_out, dd_exp, xi, ndd_exp, alpha, shift, tol, nullptr, ws_exp, ws_bytes, nullptr,
+                                s);
+    if (!rc && phi && !fused) {
         if (nonlin == ES_NONLIN_COMBUSTION) {
             rc = launch_combustion(u, g, n, f->bad, f->side);
             if (!rc && source) rc = launch_axpy(g, source, -1.0, g, n, f->side);  // g(u) - b (integrator.py:121)
@@ -100,16 +131,18 @@ int run_expeuler_step(const es_stencil_desc *d, const double *u, double *u_out, 
         cudaStreamWaitEvent(s, f->join, 0);
     }
     if (rc) return rc;
-    cudaEventRecord(f->t1, s);
-    if (phi) {
+    if (!fused) cudaEventRecord(f->t1, s);
+    if (phi && !fused) {
         k_axpy_if<<<grid_for(n), 256, 0, s>>>(u_out, z, h, u_out, n, series_state_ptr(ws_exp),
                                               series_state_ptr(ws_phi));
         if ((rc = check_launch("step combination"))) return rc;
     }
-    rc = series_status(read_series_state(series_state_ptr(ws_exp), &res->exp_series, s), &res->status_exp);
-    if (!rc && phi)
-        rc = series_status(read_series_state(series_state_ptr(ws_phi), &res->phi1_series, s), &res->status_phi1);
-    if (rc) return rc;
+    if (!fused) {
+        rc = series_status(read_series_state(series_state_ptr(ws_exp), &res->exp_series, s), &res->status_exp);
+        if (!rc && phi)
+            rc = series_status(read_series_state(series_state_ptr(ws_phi), &res->phi1_series, s), &res->status_phi1);
+        if (rc) return rc;
+    }
     cudaEventElapsedTime(&res->series_ms, f->t0, f->t1);
     if (phi && nonlin == ES_NONLIN_COMBUSTION && *f->bad_host < (unsigned long long)n) {
         res->first_bad = (int64_t)*f->bad_host;

@@ -1144,3 +1144,84 @@ def test_two_node_tail_pass_bitwise(graph, monkeypatch):
     monkeypatch.delenv("ES_TB")
     monkeypatch.delenv("ES_TB_TAIL")
     assert stops == {0, 1}, stops
+
+
+SMALL_CASES = [((256, 256), "homogeneous", None, False, 1e-8), ((128, 96), "neumann", "radial", False, 1e-10),
+               ((64, 70), "none", None, True, 1e-9), ((250, 33), "homogeneous", coeff_d, True, 0.0),
+               ((512, 40), "neumann", coeff_d, False, 1e-12), ((2, 3), "homogeneous", None, False, 1e-8)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,bc,coeff,gd,tol", SMALL_CASES)
+def test_small_series_bitwise(dims, bc, coeff, gd, tol, monkeypatch):
+    """The persistent small-grid series (one cooperative launch, grid barrier
+    per node; series_small.cu) equals the graph path (ES_SMALL=0) bit for
+    bit -- p, matvec counts, last term and |p| -- for every ghost mode,
+    coefficient kind, with and without a g' diagonal, tol > 0 and fixed
+    degree, and the oracle too."""
+    nx, ny = dims
+    g = es.Grid3D(nx, ny, 1)
+    op = es.StencilOperator(g, BCS[bc], coeff=es.radial_coeff if coeff == "radial" else coeff)
+    iv = es.gershgorin_interval(op)
+    iv = iv.widened(25.0) if gd else iv
+    it = es.make_interpolant(iv, "phi1", -12.0 / max(abs(iv.a), abs(iv.b)), 70, 1e-8)
+    rng = np.random.default_rng(nx * 7 + ny)
+    v = torch.from_numpy(rng.standard_normal(g.n)).cuda()
+    gdiag = torch.from_numpy(rng.random(g.n) * 25.0).cuda() if gd else None
+    out = {}
+    for small in ("0", "1"):
+        monkeypatch.setenv("ES_SMALL", small)
+        out[small] = es.newton_apply(op, it, v, tol, gdiag=gdiag)
+    monkeypatch.delenv("ES_SMALL")
+    (ref, mv), (got, mv2) = out["0"], out["1"]
+    assert mv2 == mv, (dims, bc, mv, mv2)
+    assert torch.equal(got, ref), (dims, bc)
+
+
+@pytest.mark.gpu
+def test_small_series_convergence_error_matches(monkeypatch):
+    """Degree exhausted with tol > 0: both paths raise ConvergenceError with
+    the same residual and degree."""
+    g = es.Grid3D(96, 64, 1)
+    op = es.StencilOperator(g, BCS["homogeneous"])
+    it = es.make_interpolant(es.gershgorin_interval(op), "phi1", -5e-2, 6, 1e-8)
+    v = torch.from_numpy(np.random.default_rng(5).standard_normal(g.n)).cuda()
+    msgs = []
+    for small in ("0", "1"):
+        monkeypatch.setenv("ES_SMALL", small)
+        with pytest.raises(es.ConvergenceError) as ei:
+            es.newton_apply(op, it, v, 1e-14)
+        msgs.append((ei.value.residual, ei.value.degree))
+    monkeypatch.delenv("ES_SMALL")
+    assert msgs[0] == msgs[1], msgs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("source", [False, True])
+def test_small_expeuler_step_bitwise(source, monkeypatch):
+    """The fused small-grid exponential-Euler step (both series, g(u) - b in
+    the kernel, u + h z) equals the two-graph step bit for bit, and a point
+    outside the combustion domain still raises DomainError with its index."""
+    g = es.Grid3D(256, 256, 1)
+    op = es.StencilOperator(g, BCS["homogeneous"])
+    rng = np.random.default_rng(21)
+    u0 = 1.0 + 0.1 * rng.random(g.n)
+    b = 0.01 * rng.standard_normal(g.n) if source else None
+    prob = es.SemilinearProblem(operator=op, nonlinearity=es.combustion_g, u0=u0, boundary_source=b)
+    res = {}
+    for small in ("0", "1"):
+        monkeypatch.setenv("ES_SMALL", small)
+        res[small] = es.exponential_euler_step(prob, u0, 2e-3, 1e-4)
+    u_ref, st_ref = res["0"]
+    u_got, st_got = res["1"]
+    assert (st_got.matvecs_exp, st_got.matvecs_phi1) == (st_ref.matvecs_exp, st_ref.matvecs_phi1)
+    assert np.array_equal(u_got, u_ref)
+    bad = u0.copy()
+    bad[777] = -1.0
+    for small in ("0", "1"):
+        monkeypatch.setenv("ES_SMALL", small)
+        with pytest.raises(es.DomainError) as ei:
+            es.exponential_euler_step(es.SemilinearProblem(operator=op, nonlinearity=es.combustion_g, u0=bad),
+                                      bad, 2e-3, 1e-4)
+        assert "777" in str(ei.value)
+    monkeypatch.delenv("ES_SMALL")
