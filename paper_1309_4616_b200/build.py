@@ -22,7 +22,8 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libexpstencil_b200.so")
 SOURCES = ["capi.cu", "stencil.cu", "csr.cu", "pointwise.cu", "graph.cu", "f32.cu", "step.cu", "csr_generic.cu", "series_small.cu"]
-HEADERS = ["es_common.cuh", "es_host.h", "stencil.cuh", "series.cuh", "stencil_tma.cuh", "stencil_tb.cuh"]
+HEADERS = ["es_common.cuh", "es_host.h", "stencil.cuh", "series.cuh", "stencil_tma.cuh", "stencil_tb.cuh",
+           "stencil_tb2d.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",
@@ -41,7 +42,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    # every file under csrc/ (a header missing from HEADERS must not leave a stale build)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(REPO, "include", "expstencil_b200.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))

@@ -10,6 +10,7 @@
 #include "es_host.h"
 #include "series.cuh"
 #include "stencil_tma.cuh"
+#include "stencil_tb2d.cuh"
 #include "stencil_tb.cuh"
 
 #include <cudaTypedefs.h>
@@ -262,6 +263,16 @@ __global__ void __launch_bounds__(TB_THREADS, TB_MINB) k_node_tb(const SeriesPar
     tb_pass<COEFF, GD>(Pp, k, tb_two(P, k), tsmem);
 }
 
+// Two Leja nodes per pass on a single-plane grid (stencil_tb2d.cuh).
+template <bool STAGED>
+__global__ void __launch_bounds__(T2_THREADS, T2_MINB) k_node_tb2d(const SeriesParams *__restrict__ Pp) {
+    extern __shared__ __align__(128) char tsmem[];
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    const int k = P.state->k + 1;
+    tb2_pass<STAGED>(Pp, k, tb_two(P, k), tsmem);
+}
+
 __global__ void __launch_bounds__(256) k_slice_reduce2(const SeriesParams *__restrict__ Pp) {
     const SeriesParams &P = *Pp;
     if (P.state->done) return;
@@ -469,7 +480,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // MK_W2 / MK_G2 / MK_P2 / MK_GH2: the two-node pass's tiles (stencil_tb.cuh)
-enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3, MK_W2 = 4, MK_G2 = 5, MK_P2 = 6, MK_GH2 = 7 };
+enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3, MK_W2 = 4, MK_G2 = 5, MK_P2 = 6, MK_GH2 = 7, MK_WTAIL8 = 8 };
 
 // TMA descriptor of a slab-shaped fp64 vector (x fastest); OOB reads are
 // zero-filled, which is the homogeneous Dirichlet ghost rule.
@@ -493,7 +504,7 @@ static int encode_map(CUtensorMap *m, const double *base, const es_stencil_desc 
         dims[0] = (cuuint64_t)d->nx;
         dims[1] = (cuuint64_t)d->ny;
         strides[0] = (cuuint64_t)d->nx * 8;
-        box[0] = kind == MK_WTAIL ? 4 : 256;
+        box[0] = kind == MK_WTAIL ? 4 : kind == MK_WTAIL8 ? 8 : 256;
         box[1] = 1;
     } else {
         rank = 3;
@@ -716,7 +727,8 @@ struct SeriesSetup {
     SeriesParams hp;
     SeriesParams *dparams;
     int64_t n;
-    bool tb = false;  // two nodes per pass (k_node_tb + k_slice_reduce2)
+    bool tb = false;   // two nodes per pass (k_node_tb + k_slice_reduce2)
+    bool tb2 = false;  // two nodes per pass on a single-plane grid (k_node_tb2d + k_slice_reduce2)
     bool staged = false;  // sampled coefficient through the PG ring (ES_COEFF_STAGED)
 };
 
@@ -752,6 +764,18 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     S.tb = pl.tma && allow_tb > 0 && !pl.dim2 && !dist && (d->mode == ES_MODE_ZERO || d->mode == ES_MODE_NEUMANN) &&
            env_int("ES_TB", 1) &&
            (!halos || (allow_tb == 2 && d->coeff_kind != ES_COEFF_ARRAY && d->lz >= 2));
+    // two nodes per pass on single-plane grids (stencil_tb2d.cuh): Dirichlet
+    // or Neumann, no coefficient or the staged sampled D, no g' (C2: 48
+    // instead of 2 x 40 B/point per two nodes).  The one-node plan's row
+    // chunks stay the norm slices; items span 4 of them.
+    S.tb2 = pl.tma && pl.dim2 && allow_tb > 0 && !dist && !halos && !gdiag &&
+            (d->mode == ES_MODE_ZERO || d->mode == ES_MODE_NEUMANN) && d->coeff_kind != ES_COEFF_RADIAL &&
+            env_int("ES_TB", 1) && env_int("ES_TB2D", 1);
+    int chunk2 = 0;
+    if (S.tb2) {
+        chunk2 = pl.chunk * std::max(1, env_int("ES_TB2CHUNK", 4));
+        pl.items = (int64_t)((d->nx + T2_TX - 1) / T2_TX) * ((d->ny + chunk2 - 1) / chunk2);
+    }
     if (S.tb) {
         pl.chunk = std::max(1, env_int("ES_TBCHUNK", 32));
         pl.grid.z = (unsigned)((d->lz + pl.chunk - 1) / pl.chunk);
@@ -764,7 +788,12 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     ApplyFn af;
     S.lp = pl;
     if (pl.tma) {
-        if (S.tb) {
+        if (S.tb2) {
+            S.staged = d->coeff_kind == ES_COEFF_ARRAY;
+            S.nf = S.staged ? k_node_tb2d<true> : k_node_tb2d<false>;
+            finish_tma_plan(S.lp, (const void *)S.nf,
+                            S.staged ? (size_t)Tb2Layout<true>::BYTES : (size_t)Tb2Layout<false>::BYTES, T2_THREADS);
+        } else if (S.tb) {
             S.nf = gdiag ? pick_node_tb<true>(d->coeff_kind) : pick_node_tb<false>(d->coeff_kind);
             finish_tma_plan(S.lp, (const void *)S.nf,
                             gdiag ? (size_t)TbLayout<true>::BYTES : (size_t)TbLayout<false>::BYTES, TB_THREADS);
@@ -807,6 +836,8 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     hp.maps = nullptr;
     hp.dist = dist ? 1 : 0;
     hp.tail1 = env_int("ES_TB_TAIL", 1) ? 1 : 0;
+    hp.norm_chunk = pl.chunk;
+    if (S.tb2) hp.chunk_len = chunk2;  // items of the two-node 2D pass
     S.dparams = reinterpret_cast<SeriesParams *>(w + L.params);
     if (pl.tma && maps_needed) {
         TmaMaps maps;
@@ -821,6 +852,12 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
         if (!rc) rc = encode_map(&maps.m[MAP_HHI], halo_hi, d, pl.dim2, MK_HALO);
         if (!rc) rc = encode_map(&maps.m[MAP_HLO_1], halo_lo_1, d, pl.dim2, MK_HALO);
         if (!rc) rc = encode_map(&maps.m[MAP_HHI_1], halo_hi_1, d, pl.dim2, MK_HALO);
+        if (S.tb2) {
+            if (!rc) rc = encode_map(&maps.m[MAP_T2_W8_V], v, d, true, MK_WTAIL8);
+            if (!rc) rc = encode_map(&maps.m[MAP_T2_W8_0], hp.wbuf[0], d, true, MK_WTAIL8);
+            if (!rc) rc = encode_map(&maps.m[MAP_T2_W8_1], hp.wbuf[1], d, true, MK_WTAIL8);
+            if (!rc) rc = encode_map(&maps.m[MAP_T2_G4], S.staged ? d->coeff : nullptr, d, true, MK_WTAIL);
+        }
         if (S.tb) {
             if (!rc) rc = encode_map(&maps.m[MAP_T_V], v, d, false, MK_W2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_0], hp.wbuf[0], d, false, MK_W2);
@@ -910,7 +947,7 @@ int run_stencil_series(const es_stencil_desc *d, const double *v, double *p_out,
     int rc = prepare_series(d, v, p_out, dd, xi, ndd, alpha, shift, tol, gdiag, nullptr, nullptr, false, ws,
                             ws_bytes, S, stream);
     if (rc) return rc;
-    NodeFn rf = S.tb ? k_slice_reduce2 : k_slice_reduce;
+    NodeFn rf = S.tb || S.tb2 ? k_slice_reduce2 : k_slice_reduce;
     GraphKernel gk[2] = {{(const void *)S.nf, S.lp.grid, S.lp.block, S.lp.smem},
                          {(const void *)rf, dim3((unsigned)S.pl.nslices), dim3(256), 0}};
     unsigned long long handle = 0;

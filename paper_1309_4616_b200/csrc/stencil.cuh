@@ -82,6 +82,9 @@ struct SeriesParams {
     // series usually stops there, and a two-node pass would compute a node
     // nobody reads.  Decisions are unchanged (bitwise).
     int tail1;
+    // two-node 2D pass (stencil_tb2d.cuh): rows per slice of the one-node 2D
+    // plan, whose (chunk, 512-wide tile, warp) norm layout the pass keeps
+    int norm_chunk;
 };
 
 // One pass: what a node (or a plain fused apply) reads and writes.

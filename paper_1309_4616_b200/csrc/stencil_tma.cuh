@@ -52,7 +52,9 @@ enum {
     // two-node pass (stencil_tb.cuh): w tiles with a two-point halo, g' tiles with a one-point halo
     MAP_T_V, MAP_T_0, MAP_T_1, MAP_T_G, MAP_T_PV,
     // two-node pass on a peer-memory slab: two-plane w halos by parity, g' boundary planes
-    MAP_T_HLO0, MAP_T_HLO1, MAP_T_HHI0, MAP_T_HHI1, MAP_T_GLO, MAP_T_GHI, MAP_T_P0, MAP_T_P1, MAP_COUNT
+    MAP_T_HLO0, MAP_T_HLO1, MAP_T_HHI0, MAP_T_HHI1, MAP_T_GLO, MAP_T_GHI, MAP_T_P0, MAP_T_P1,
+    // two-node 2D pass (stencil_tb2d.cuh): 8-wide tails of the w rows, the 4-wide tail of the staged D
+    MAP_T2_W8_V, MAP_T2_W8_0, MAP_T2_W8_1, MAP_T2_G4, MAP_COUNT
 };
 
 struct alignas(64) TmaMaps {

@@ -1225,3 +1225,40 @@ def test_small_expeuler_step_bitwise(source, monkeypatch):
                                       bad, 2e-3, 1e-4)
         assert "777" in str(ei.value)
     monkeypatch.delenv("ES_SMALL")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("graph", [True, False])
+def test_two_node_2d_bitwise(graph, monkeypatch):
+    """Two Leja nodes per pass on single-plane grids (stencil_tb2d.cuh) equal
+    the one-node series bit for bit -- p and matvec counts -- for Dirichlet
+    and Neumann, no coefficient and the staged sampled D, odd and even node
+    counts, tiles cut by the domain (nx not a multiple of 256), row chunks cut
+    by ny, fixed degree and tol > 0 (small-grid persistent path off)."""
+    monkeypatch.setenv("ES_SMALL", "0")
+    if not graph:
+        monkeypatch.setenv("ES_NO_GRAPH", "1")
+    cases = [((1000, 77), "neumann", "radial", 1e-10), ((512, 64), "homogeneous", None, 0.0),
+             ((770, 130), "homogeneous", coeff_d, 1e-8), ((258, 33), "neumann", None, 1e-12),
+             ((2048, 40), "neumann", "radial", 0.0)]
+    for (nx, ny), bc, coeff, tol in cases:
+        g = es.Grid3D(nx, ny, 1)
+        op = es.StencilOperator(g, BCS[bc], coeff=es.radial_coeff if coeff == "radial" else coeff)
+        iv = es.gershgorin_interval(op)
+        for nodes in (37, 40):
+            it = es.make_interpolant(iv, "phi1", -9.0 / max(abs(iv.a), abs(iv.b)), nodes, 1e-8)
+            v = torch.from_numpy(np.random.default_rng(nx + ny).standard_normal(g.n)).cuda()
+            out = {}
+            for tb in ("0", "1"):
+                monkeypatch.setenv("ES_TB2D", tb)
+                try:
+                    out[tb] = es.newton_apply(op, it, v, tol)
+                except es.ConvergenceError as e:
+                    out[tb] = (e.residual, e.degree)
+            monkeypatch.delenv("ES_TB2D")
+            a, b = out["0"], out["1"]
+            assert b[1] == a[1], ((nx, ny), bc, nodes)
+            if isinstance(a[0], torch.Tensor):
+                assert torch.equal(b[0], a[0]), ((nx, ny), bc, nodes)
+            else:
+                assert a == b
