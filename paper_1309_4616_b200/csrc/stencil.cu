@@ -219,7 +219,9 @@ __global__ void __launch_bounds__(256) k_slice_p2p2(const SeriesParams *__restri
     const int pass = P.state->pass, par = (pass + 1) & 1;
     if (blockIdx.x == 0 && threadIdx.x == 0 && P.work) *P.work = 0u;
     const double2 *w = reinterpret_cast<const double2 *>(P.wbuf[pass & 1]);  // w_{k+1} (w_k: one-node pass)
-    double2 *lo = reinterpret_cast<double2 *>(P.peer_lo[par]), *hi = reinterpret_cast<double2 *>(P.peer_hi[par]);
+    // pushed by the pass itself (peer_in_node, x2): nothing to copy here
+    double2 *lo = P.peer_in_node ? nullptr : reinterpret_cast<double2 *>(P.peer_lo[par]);
+    double2 *hi = P.peer_in_node ? nullptr : reinterpret_cast<double2 *>(P.peer_hi[par]);
     const int64_t two_planes = P.g.nx * P.g.ny, lz = P.g.lz;  // two planes = nx ny double2
     if (lo || hi) {
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < two_planes;
@@ -254,13 +256,13 @@ __global__ void __launch_bounds__(256) k_p2p_init2(const SeriesParams *__restric
 }
 
 // Two Leja nodes per pass (stencil_tb.cuh) and its reduction / decisions.
-template <int COEFF, bool GD>
+template <int COEFF, bool GD, bool PEER>
 __global__ void __launch_bounds__(TB_THREADS, TB_MINB) k_node_tb(const SeriesParams *__restrict__ Pp) {
     extern __shared__ __align__(128) char tsmem[];
     const SeriesParams &P = *Pp;
     if (P.state->done) return;
     const int k = P.state->k + 1;
-    tb_pass<COEFF, GD>(Pp, k, tb_two(P, k), tsmem);
+    tb_pass<COEFF, GD, PEER>(Pp, k, tb_two(P, k), tsmem);
 }
 
 // Two Leja nodes per pass on a single-plane grid (stencil_tb2d.cuh).
@@ -732,12 +734,12 @@ struct SeriesSetup {
     bool staged = false;  // sampled coefficient through the PG ring (ES_COEFF_STAGED)
 };
 
-template <bool GD>
+template <bool GD, bool PEER = false>
 static NodeFn pick_node_tb(int coeff) {
     switch (coeff) {
-        case ES_COEFF_RADIAL: return k_node_tb<ES_COEFF_RADIAL, GD>;
-        case ES_COEFF_ARRAY: return k_node_tb<ES_COEFF_ARRAY, GD>;
-        default: return k_node_tb<ES_COEFF_NONE, GD>;
+        case ES_COEFF_RADIAL: return k_node_tb<ES_COEFF_RADIAL, GD, PEER>;
+        case ES_COEFF_ARRAY: return k_node_tb<ES_COEFF_ARRAY, GD, PEER>;
+        default: return k_node_tb<ES_COEFF_NONE, GD, PEER>;
     }
 }
 
@@ -1097,6 +1099,14 @@ int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double 
                                      "array, lz >= 2, ES_TB not 0)");
     if (x->slice_offset < 0 || x->slice_offset + S.pl.nslices > x->total_slices)
         return set_error(ES_ERR_ARG, "slice offset / total do not cover this slab's %d slices", S.pl.nslices);
+    if (S.tb && env_int("ES_PEER_IN_NODE", 1)) {
+        // x2: the pass itself pushes the boundary planes to the neighbours
+        // (overlapped with the sweep); the slice kernel only fences and joins
+        S.nf = gdiag ? pick_node_tb<true, true>(d->coeff_kind) : pick_node_tb<false, true>(d->coeff_kind);
+        finish_tma_plan(S.lp, (const void *)S.nf,
+                        gdiag ? (size_t)TbLayout<true>::BYTES : (size_t)TbLayout<false>::BYTES, TB_THREADS);
+        S.hp.peer_in_node = 1;
+    }
     SeriesParams &hp = S.hp;
     hp.p2p = 1;
     hp.nranks = x->nranks;

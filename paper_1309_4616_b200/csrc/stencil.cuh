@@ -85,6 +85,9 @@ struct SeriesParams {
     // two-node 2D pass (stencil_tb2d.cuh): rows per slice of the one-node 2D
     // plan, whose (chunk, 512-wide tile, warp) norm layout the pass keeps
     int norm_chunk;
+    // peer-memory two-node slab series: the pass pushes its boundary planes to
+    // the neighbours itself (k_slice_p2p2 only fences and joins the round)
+    int peer_in_node;
 };
 
 // One pass: what a node (or a plain fused apply) reads and writes.

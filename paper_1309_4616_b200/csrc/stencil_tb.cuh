@@ -98,6 +98,7 @@ struct TbLayout {
 // Norm partials keep the one-node kernel's (chunk, 64 x 8 tile, row) layout.
 struct TbItems {
     int tiles_x, ntiles8, ntiles, nchunks, chunk_len, L;
+    int edges_first;  // slab of a peer-memory series: both boundary chunks first (their halo pushes overlap the rest)
 };
 
 ES_DEV TbItems tb_items_of(const Geom &g, int chunk_len) {
@@ -108,6 +109,7 @@ ES_DEV TbItems tb_items_of(const Geom &g, int chunk_len) {
     it.L = (int)g.lz;
     it.chunk_len = chunk_len;
     it.nchunks = (it.L + chunk_len - 1) / chunk_len;
+    it.edges_first = (g.halo_lo != nullptr || g.halo_hi != nullptr) && it.nchunks > 2;
     return it;
 }
 
@@ -118,6 +120,7 @@ struct TbItem {
 ES_DEV TbItem tb_item_at(const TbItems &its, int i) {
     TbItem r;
     r.chunk = i / its.ntiles;
+    if (its.edges_first) r.chunk = r.chunk == 0 ? 0 : r.chunk == 1 ? its.nchunks - 1 : r.chunk - 1;
     const int t = i % its.ntiles, tx = t % its.tiles_x, ty = t / its.tiles_x;
     r.x0 = tx * 64;
     r.y0 = ty * TB_TY;
@@ -442,7 +445,7 @@ ES_DEV void tb_group_a(const Geom &g, const SeriesParams *P, int k, const TbItem
     }
 }
 
-template <int COEFF, bool GD>
+template <int COEFF, bool GD, bool PEER>
 ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, const TbItems &its, char *smem) {
     using Lt = TbLayout<GD>;
     const TbBars B = tb_bars<GD>(smem);
@@ -457,6 +460,24 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
     const double alpha = P->alpha, dk = P->dd[k];
     const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
     const double pscale = k == 1 ? P->dd[0] : 1.0;  // first pass: P tiles hold v, p_0 = dd_0 v
+    // PEER (x2): the w this pass writes -- w_{k+1}, or w_k on a one-node pass --
+    // also goes straight to the neighbours' two-plane halo buffers of the next
+    // pass's parity as it is computed (planes 0, 1 below, L-2, L-1 above),
+    // overlapped with the rest of the sweep; k_slice_p2p2 then only fences
+    double *peer_lo = nullptr, *peer_hi = nullptr;
+    if constexpr (PEER) {
+        const int par = (pass + 1) & 1;
+        peer_lo = P->peer_lo[par];
+        peer_hi = P->peer_hi[par];
+    }
+    auto push = [&](int64_t plane_idx, int64_t in_plane, double2 val) {
+        if constexpr (PEER) {
+            if (peer_lo && plane_idx < 2)
+                *reinterpret_cast<double2 *>(peer_lo + plane_idx * plane + in_plane) = val;
+            if (peer_hi && plane_idx >= its.L - 2)
+                *reinterpret_cast<double2 *>(peer_hi + (plane_idx - (its.L - 2)) * plane + in_plane) = val;
+        }
+    };
     Ring<Lt::SG> gr;
     Ring<Lt::SP> pr;
     Ring<TB_SV> vr;
@@ -509,7 +530,10 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                     if (act[h]) {
                         const int64_t off = off0 + h * drow;
                         *reinterpret_cast<double2 *>(pk_dst + off) = make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
-                        if (!two) *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
+                        if (!two) {
+                            *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
+                            push(j, ya[h] * nx + xa, vk);
+                        }
                         acc_w0[h] = add(acc_w0[h], add(mul(vk.x, vk.x), mul(vk.y, vk.y)));
                         acc_p0[h] = add(acc_p0[h], add(mul(pk_cur[2 * h], pk_cur[2 * h]),
                                                        mul(pk_cur[2 * h + 1], pk_cur[2 * h + 1])));
@@ -557,6 +581,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                     const int64_t off = off0 - plane + h * drow;  // plane jc = j - 1
                     *reinterpret_cast<double2 *>(w1_dst + off) = make_double2(wn[2 * h], wn[2 * h + 1]);
                     *reinterpret_cast<double2 *>(pk1_dst + off) = make_double2(pn[2 * h], pn[2 * h + 1]);
+                    push(jc, ya[h] * nx + xa, make_double2(wn[2 * h], wn[2 * h + 1]));
                     acc_w1[h] = add(acc_w1[h], add(mul(wn[2 * h], wn[2 * h]), mul(wn[2 * h + 1], wn[2 * h + 1])));
                     acc_p1[h] = add(acc_p1[h], add(mul(pn[2 * h], pn[2 * h]), mul(pn[2 * h + 1], pn[2 * h + 1])));
                 }
@@ -602,9 +627,10 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
             }
         }
     }
+    if constexpr (PEER) __threadfence_system();  // the halo pushes, before the slice kernel's arrival
 }
 
-template <int COEFF, bool GD>
+template <int COEFF, bool GD, bool PEER = false>
 ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
     using Lt = TbLayout<GD>;
     // a private copy: the ring waits' memory clobbers would otherwise make
@@ -655,7 +681,7 @@ ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
     } else if (warp < TB_AW) {
         tb_group_a<COEFF, GD>(g, P, k, its, smem);
     } else {
-        tb_group_c<COEFF, GD>(g, P, k, two, its, smem);
+        tb_group_c<COEFF, GD, PEER>(g, P, k, two, its, smem);
     }
 }
 

@@ -732,7 +732,7 @@ def _p2p_run(op, ranks, it, v, tol, rounds, only=None, gdiag=None):
     for q in launched:
         res = _lib.SeriesResult()
         rc = lib.es_leja_fetch(ptr(q["ws"]), ctypes.byref(res), q["stream"].cuda_stream)
-        out.append((rc, res.matvecs, q["p"].cpu().numpy()))
+        out.append((rc, res.matvecs, q["p"].cpu().numpy(), res.passes))
     torch.cuda.synchronize()
     return out
 
@@ -755,7 +755,10 @@ def test_p2p_slab_series_emulated_ranks_bitwise(graph, two, monkeypatch):
         assert [o[0] for o in outs] == [0, 0, 0]
         assert [o[1] for o in outs] == [mv] * 3
         assert np.concatenate([o[2] for o in outs]).tobytes() == ref.tobytes()
-        rounds += ((mv + 1) // 2 if two else mv) + 1  # consecutive series continue the counters
+        # consecutive series continue the counters: round 0 + one per pass (a
+        # two-node series may end with a one-node tail pass)
+        assert len({o[3] for o in outs}) == 1
+        rounds += outs[0][3] + 1
 
 
 @pytest.mark.parametrize("two", [False, True])
