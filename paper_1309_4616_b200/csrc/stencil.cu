@@ -1099,9 +1099,13 @@ int run_p2p_series(const es_stencil_desc *d, const es_p2p_desc *x, const double 
                                      "array, lz >= 2, ES_TB not 0)");
     if (x->slice_offset < 0 || x->slice_offset + S.pl.nslices > x->total_slices)
         return set_error(ES_ERR_ARG, "slice offset / total do not cover this slab's %d slices", S.pl.nslices);
-    if (S.tb && env_int("ES_PEER_IN_NODE", 1)) {
+    if (S.tb && env_int("ES_PEER_IN_NODE", gdiag ? 1 : 0)) {
         // x2: the pass itself pushes the boundary planes to the neighbours
-        // (overlapped with the sweep); the slice kernel only fences and joins
+        // (overlapped with the sweep); the slice kernel only fences and joins.
+        // Default for the Rosenbrock (g') series -- C4 -- where it measured
+        // 75.8 vs 79.3 ms (2 emulated 1024^3 slabs, 16 nodes); without g' the
+        // PEER build of the pass spills and the copy stays in the slice kernel
+        // (64.6 vs 67.5 ms), tools/p2p_timing.py
         S.nf = gdiag ? pick_node_tb<true, true>(d->coeff_kind) : pick_node_tb<false, true>(d->coeff_kind);
         finish_tma_plan(S.lp, (const void *)S.nf,
                         gdiag ? (size_t)TbLayout<true>::BYTES : (size_t)TbLayout<false>::BYTES, TB_THREADS);

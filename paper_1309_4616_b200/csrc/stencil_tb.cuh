@@ -460,24 +460,18 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
     const double alpha = P->alpha, dk = P->dd[k];
     const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
     const double pscale = k == 1 ? P->dd[0] : 1.0;  // first pass: P tiles hold v, p_0 = dd_0 v
-    // PEER (x2): the w this pass writes -- w_{k+1}, or w_k on a one-node pass --
-    // also goes straight to the neighbours' two-plane halo buffers of the next
-    // pass's parity as it is computed (planes 0, 1 below, L-2, L-1 above),
-    // overlapped with the rest of the sweep; k_slice_p2p2 then only fences
+    // PEER (x2): when an item of a boundary chunk is done, its group-C threads
+    // copy what they just wrote of planes 0, 1 / L-2, L-1 (the w this pass
+    // writes: w_{k+1}, or w_k on a one-node pass) into the neighbours'
+    // two-plane halo buffers of the next pass's parity -- boundary chunks are
+    // swept first, so the NVLink stores overlap the rest of the sweep; the
+    // inner loop is untouched and k_slice_p2p2 only fences
     double *peer_lo = nullptr, *peer_hi = nullptr;
     if constexpr (PEER) {
         const int par = (pass + 1) & 1;
         peer_lo = P->peer_lo[par];
         peer_hi = P->peer_hi[par];
     }
-    auto push = [&](int64_t plane_idx, int64_t in_plane, double2 val) {
-        if constexpr (PEER) {
-            if (peer_lo && plane_idx < 2)
-                *reinterpret_cast<double2 *>(peer_lo + plane_idx * plane + in_plane) = val;
-            if (peer_hi && plane_idx >= its.L - 2)
-                *reinterpret_cast<double2 *>(peer_hi + (plane_idx - (its.L - 2)) * plane + in_plane) = val;
-        }
-    };
     Ring<Lt::SG> gr;
     Ring<Lt::SP> pr;
     Ring<TB_SV> vr;
@@ -530,10 +524,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                     if (act[h]) {
                         const int64_t off = off0 + h * drow;
                         *reinterpret_cast<double2 *>(pk_dst + off) = make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
-                        if (!two) {
-                            *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
-                            push(j, ya[h] * nx + xa, vk);
-                        }
+                        if (!two) *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
                         acc_w0[h] = add(acc_w0[h], add(mul(vk.x, vk.x), mul(vk.y, vk.y)));
                         acc_p0[h] = add(acc_p0[h], add(mul(pk_cur[2 * h], pk_cur[2 * h]),
                                                        mul(pk_cur[2 * h + 1], pk_cur[2 * h + 1])));
@@ -581,7 +572,6 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                     const int64_t off = off0 - plane + h * drow;  // plane jc = j - 1
                     *reinterpret_cast<double2 *>(w1_dst + off) = make_double2(wn[2 * h], wn[2 * h + 1]);
                     *reinterpret_cast<double2 *>(pk1_dst + off) = make_double2(pn[2 * h], pn[2 * h + 1]);
-                    push(jc, ya[h] * nx + xa, make_double2(wn[2 * h], wn[2 * h + 1]));
                     acc_w1[h] = add(acc_w1[h], add(mul(wn[2 * h], wn[2 * h]), mul(wn[2 * h + 1], wn[2 * h + 1])));
                     acc_p1[h] = add(acc_p1[h], add(mul(pn[2 * h], pn[2 * h]), mul(pn[2 * h + 1], pn[2 * h + 1])));
                 }
@@ -608,6 +598,22 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
         if constexpr (GD) {  // G(me)
             warp_arrive(&B.gempty[gr.slot]);
             gr.next();
+        }
+        if constexpr (PEER) {  // this thread's own stores of the boundary planes, read back and pushed
+            if ((peer_lo && it.mb < 2) || (peer_hi && it.me > its.L - 2)) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (!act[h]) continue;
+                    const int64_t in_plane = ya[h] * nx + xa;
+                    for (int z = it.mb; z < it.me; ++z) {
+                        const bool lo = peer_lo && z < 2, hi = peer_hi && z >= its.L - 2;
+                        if (!lo && !hi) continue;
+                        const double2 val = *reinterpret_cast<const double2 *>(w1_dst + z * plane + in_plane);
+                        if (lo) *reinterpret_cast<double2 *>(peer_lo + z * plane + in_plane) = val;
+                        if (hi) *reinterpret_cast<double2 *>(peer_hi + (z - (its.L - 2)) * plane + in_plane) = val;
+                    }
+                }
+            }
         }
         // (chunk, tile, row-warp) partials of both nodes, one-node kernel layout
 #pragma unroll

@@ -805,7 +805,7 @@ def test_p2p_missing_peer_times_out_instead_of_hanging():
     ranks, keep = _p2p_ranks(op, [(0, 8), (8, 16)], timeout_ns=200_000_000, two=True)
     it = es.make_interpolant(es.gershgorin_interval(op), "exp", -1e-3, 20, 1e-8)
     v = np.random.default_rng(1).standard_normal(g.n)
-    (rc, mv, _), = _p2p_run(op, ranks, it, v, 0.0, 0, only=[0])
+    (rc, mv, _, _), = _p2p_run(op, ranks, it, v, 0.0, 0, only=[0])
     assert rc == _lib.ES_ERR_CUDA and "peer" in _lib.last_error()
 
 
