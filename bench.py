@@ -396,7 +396,10 @@ class CsrStepper:
         ex = getattr(self.op, "exchange", "none")
         if ex == "nccl":
             return 3 * stats.matvecs + 2
-        return 2 * stats.matvecs + (3 if ex == "p2p" else 2)
+        m = stats.matvecs
+        if getattr(self.op, "two_node_passes", lambda: False)():
+            m = (m + 1) // 2  # (node + reduce) per two-node pass
+        return 2 * m + (3 if ex == "p2p" else 2)
 
 
 class Stepper:

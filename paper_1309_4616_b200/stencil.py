@@ -239,8 +239,14 @@ class StencilOperator:
         import os
 
         g = self.grid
-        return (os.environ.get("ES_TB", "1") != "0" and g.nz > 1 and g.nx % 2 == 0
+        base = (os.environ.get("ES_TB", "1") != "0" and g.nx % 2 == 0
                 and self.bc.kind in ("homogeneous", "neumann") and os.environ.get("ES_KERNEL", "") != "v1")
+        if g.nz > 1:
+            return base
+        # single-plane grids (stencil_tb2d.cuh): not where the persistent
+        # small-grid series takes over (series_small.cu)
+        small = os.environ.get("ES_SMALL", "1") != "0" and g.nx <= 512 and g.nx * g.ny <= (1 << 20)
+        return base and os.environ.get("ES_TB2D", "1") != "0" and not small
 
     def __repr__(self):
         g = self.grid
