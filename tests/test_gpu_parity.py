@@ -1265,3 +1265,30 @@ def test_two_node_2d_bitwise(graph, monkeypatch):
                 assert torch.equal(b[0], a[0]), ((nx, ny), bc, nodes)
             else:
                 assert a == b
+
+
+@pytest.mark.parametrize("tol", [0.0, 1e-8])
+def test_partitioned_stencil_series_runs_on_slabs(tol):
+    """PartitionedStencil's series runs slab by slab (es_leja_dist_* per slab,
+    seam planes exchanged per node): bitwise the one-domain series for
+    chunk-aligned slabs incl. matvec counts, one ledger entry per node of
+    2 (m-1) nx ny scalars; a non-aligned partition keeps p bitwise at fixed
+    degree."""
+    g = es.Grid3D(64, 40, 48)
+    op = es.StencilOperator(g, es.BoundaryCondition.homogeneous())
+    it = es.make_interpolant(es.gershgorin_interval(op), "phi1", -4e-4, 40, 1e-8)
+    v = np.random.default_rng(31).standard_normal(g.n)
+    ref, mv = es.newton_apply(op, it, v, tol)
+    for m in (2, 3):
+        w = es.PartitionedStencil(op, es.make_partition(g, m))  # 24/24, 16/16/16: 8-plane aligned
+        got, mv2 = es.newton_apply(w, it, v, tol)
+        assert mv2 == mv and got.tobytes() == ref.tobytes(), m
+        assert w.ledger.apply_count == mv and w.ledger.last_scalars() == 2 * (m - 1) * 64 * 40
+    if tol == 0.0:
+        g5 = es.Grid3D(64, 40, 45)
+        op5 = es.StencilOperator(g5, es.BoundaryCondition.neumann())
+        it5 = es.make_interpolant(es.gershgorin_interval(op5), "exp", -4e-4, 25, 1e-8)
+        v5 = np.random.default_rng(32).standard_normal(g5.n)
+        ref5, _ = es.newton_apply(op5, it5, v5, 0.0)
+        got5, _ = es.newton_apply(es.PartitionedStencil(op5, es.make_partition(g5, 4)), it5, v5, 0.0)
+        assert got5.tobytes() == ref5.tobytes()
