@@ -81,6 +81,7 @@ cudaGraphExec_t series_graph(const GraphKernel *ks, int nk, const void *dparams,
         key.push_back(ks[i].smem);
     }
     std::lock_guard<std::mutex> lk(g_mu);
+    if (env_int("ES_GRAPH_NOCACHE", 0)) key.push_back(g_cache.size() + 1);  // diagnostics: a fresh graph per series
     auto it = g_cache.find(key);
     if (it == g_cache.end()) {
         Entry e;

@@ -109,25 +109,28 @@ int run_expeuler_step(const es_stencil_desc *d, const double *u, double *u_out, 
         }
     }
     if (!fused) cudaEventRecord(f->t0, s);
+    // ES_STEP_SERIAL=1: the phi1 series on the caller's stream after the exp
+    // series (diagnostics; the default forks it onto a side stream)
+    cudaStream_t side = env_int("ES_STEP_SERIAL", 0) ? s : f->side;
     if (phi && !fused) {
         cudaEventRecord(f->fork, s);
-        cudaStreamWaitEvent(f->side, f->fork, 0);
+        cudaStreamWaitEvent(side, f->fork, 0);
     }
     if (!fused)
         rc = run_stencil_series(d, u, u_out, dd_exp, xi, ndd_exp, alpha, shift, tol, nullptr, ws_exp, ws_bytes, nullptr,
                                 s);
     if (!rc && phi && !fused) {
         if (nonlin == ES_NONLIN_COMBUSTION) {
-            rc = launch_combustion(u, g, n, f->bad, f->side);
-            if (!rc && source) rc = launch_axpy(g, source, -1.0, g, n, f->side);  // g(u) - b (integrator.py:121)
+            rc = launch_combustion(u, g, n, f->bad, side);
+            if (!rc && source) rc = launch_axpy(g, source, -1.0, g, n, side);  // g(u) - b (integrator.py:121)
         } else {
-            rc = launch_scale(source, -1.0, g, n, f->side);
+            rc = launch_scale(source, -1.0, g, n, side);
         }
         if (!rc)
             rc = run_stencil_series(d, g, z, dd_phi, xi, ndd_phi, alpha, shift, tol, nullptr, ws_phi, ws_bytes,
-                                    nullptr, f->side);
-        cudaMemcpyAsync(f->bad_host, f->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, f->side);
-        cudaEventRecord(f->join, f->side);
+                                    nullptr, side);
+        cudaMemcpyAsync(f->bad_host, f->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, side);
+        cudaEventRecord(f->join, side);
         cudaStreamWaitEvent(s, f->join, 0);
     }
     if (rc) return rc;
