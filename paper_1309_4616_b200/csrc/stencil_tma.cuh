@@ -94,15 +94,26 @@ ES_DEV void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 ES_DEV void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
 }
+#ifndef ES_MBAR_HINT
+#define ES_MBAR_HINT 0  // try_wait suspend-time hint in ns (0: the system limit)
+#endif
 ES_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t a = su32(bar);
     uint32_t ok = 0;
     do {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
+        if constexpr (ES_MBAR_HINT > 0) {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+                : "=r"(ok)
+                : "r"(a), "r"(parity), "n"(ES_MBAR_HINT)
+                : "memory");
+        } else {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(ok)
+                : "r"(a), "r"(parity)
+                : "memory");
+        }
     } while (!ok);
 }
 ES_DEV void tma_acquire(const CUtensorMap *m) {

@@ -219,6 +219,7 @@ class _StepWorkspace:
                        and np.array_equal(ei.xi, pi.xi))
         self._ws_phi = None
         self._scratch = None
+        self._call = None  # cached C-call arguments (_fused_step)
 
     def _fused_step(self, u: torch.Tensor):
         """Both series concurrently, g_n and y + h z on the device, one host
@@ -231,26 +232,31 @@ class _StepWorkspace:
         n = u.numel()
         if n != op.n:
             return None
-        d, keep = op.desc()
-        nbytes = lib.es_leja_stencil_workspace_bytes(ctypes.byref(d))
-        if self._ws_phi is None:
-            self._ws_phi = Workspace()
-        if self._scratch is None or self._scratch.numel() < 2 * n:
-            self._scratch = empty(2 * n)
-        ws_exp, ws_phi = op._ws.get(nbytes), self._ws_phi.get(nbytes)
-        dde, xi = self.exp_interp.device_coeffs()
-        ddp, _ = self.phi_interp.device_coeffs()
-        iv = self.exp_interp.interval
-        gamma = iv.halfspan
-        nonlin = _lib.ES_NONLIN_COMBUSTION if pr.nonlinearity is combustion_g else _lib.ES_NONLIN_NONE
-        src = pr._b_dev if pr.boundary_source is not None else None
+        c = self._call
+        if c is None or c["dev"] != u.device:
+            # everything but the state pointers is fixed for this (A, h): built once
+            d, keep = op.desc()
+            nbytes = lib.es_leja_stencil_workspace_bytes(ctypes.byref(d))
+            if self._ws_phi is None:
+                self._ws_phi = Workspace()
+            if self._scratch is None or self._scratch.numel() < 2 * n:
+                self._scratch = empty(2 * n)
+            ws_exp, ws_phi = op._ws.get(nbytes), self._ws_phi.get(nbytes)
+            dde, xi = self.exp_interp.device_coeffs()
+            ddp, _ = self.phi_interp.device_coeffs()
+            iv = self.exp_interp.interval
+            gamma = iv.halfspan
+            nonlin = _lib.ES_NONLIN_COMBUSTION if pr.nonlinearity is combustion_g else _lib.ES_NONLIN_NONE
+            src = pr._b_dev if pr.boundary_source is not None else None
+            res = _lib.StepResult()
+            c = self._call = dict(dev=u.device, keep=(d, keep, ws_exp, ws_phi, dde, xi, ddp, src), res=res,
+                                  head=(ctypes.byref(d),),
+                                  mid=(ptr(dde), dde.numel(), ptr(ddp), ddp.numel(), ptr(xi), 1.0 / gamma,
+                                       iv.center / gamma, float(self.tol), float(self.h), nonlin, ptr(src),
+                                       ptr(self._scratch), ptr(ws_exp), ptr(ws_phi), nbytes, ctypes.byref(res)))
         out = empty(n)
-        res = _lib.StepResult()
-        rc = lib.es_expeuler_step(ctypes.byref(d), ptr(u), ptr(out), ptr(dde), dde.numel(), ptr(ddp), ddp.numel(),
-                                  ptr(xi), 1.0 / gamma, iv.center / gamma, float(self.tol), float(self.h), nonlin,
-                                  ptr(src), ptr(self._scratch), ptr(ws_exp), ptr(ws_phi), nbytes,
-                                  ctypes.byref(res), stream_handle())
-        del keep
+        res = c["res"]
+        rc = lib.es_expeuler_step(*c["head"], ptr(u), ptr(out), *c["mid"], stream_handle())
         if rc in (_lib.ES_ERR_DOMAIN, _lib.ES_ERR_NOT_CONVERGED):
             return None
         _lib.check(rc, "es_expeuler_step")

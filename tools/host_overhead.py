@@ -37,3 +37,31 @@ for _ in range(n):
     ws.step(u, 0.0)
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+# the C call alone, arguments prebuilt (what remains without the Python layer)
+import ctypes  # noqa: E402
+
+from paper_1309_4616_b200 import _lib  # noqa: E402
+from paper_1309_4616_b200.device import ptr, stream_handle  # noqa: E402
+
+lib = _lib.load()
+d, keep = op.desc()
+nbytes = lib.es_leja_stencil_workspace_bytes(ctypes.byref(d))
+ws.step(u, 0.0)
+ws_exp, ws_phi = op._ws.get(nbytes), ws._ws_phi.get(nbytes)
+dde, xi = ws.exp_interp.device_coeffs()
+ddp, _ = ws.phi_interp.device_coeffs()
+iv = ws.exp_interp.interval
+out = torch.empty_like(u)
+res = _lib.StepResult()
+args = (ctypes.byref(d), ptr(u), ptr(out), ptr(dde), dde.numel(), ptr(ddp), ddp.numel(), ptr(xi), 1.0 / iv.halfspan,
+        iv.center / iv.halfspan, 1e-8, 1e-5, _lib.ES_NONLIN_COMBUSTION, None, ptr(ws._scratch), ptr(ws_exp),
+        ptr(ws_phi), nbytes, ctypes.byref(res), stream_handle())
+for _ in range(20):
+    lib.es_expeuler_step(*args)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(n):
+    lib.es_expeuler_step(*args)
+torch.cuda.synchronize()
+print(f"C call alone per step {1e6 * (time.perf_counter() - t0) / n:.1f} us; kernel {res.series_ms * 1e3:.1f} us")
