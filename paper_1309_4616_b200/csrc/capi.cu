@@ -53,7 +53,7 @@ static int pinned(Pinned *&p) {
     return ES_OK;
 }
 
-static int state_result(const SeriesState &st, es_series_result *res) {
+int series_result_of(const SeriesState &st, es_series_result *res) {
     res->matvecs = st.k;
     res->converged = st.converged;
     res->last_term = st.last_term;
@@ -74,7 +74,7 @@ int read_series_state(const SeriesState *state_dev, es_series_result *res, cudaS
     if (rc) return rc;
     cudaMemcpyAsync(p->host, state_dev, sizeof(SeriesState), cudaMemcpyDeviceToHost, stream);
     if (cudaStreamSynchronize(stream) != cudaSuccess) return check_launch("series sync");
-    return state_result(p->host[0], res);
+    return series_result_of(p->host[0], res);
 }
 
 int read_series_states2(const SeriesState *a, es_series_result *ra, int *rc_a, const SeriesState *b,
@@ -88,8 +88,8 @@ int read_series_states2(const SeriesState *a, es_series_result *ra, int *rc_a, c
     if (word_dev) cudaMemcpyAsync(p->word, word_dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
     if (cudaStreamSynchronize(stream) != cudaSuccess) return check_launch("series sync");
     if (word_dev) *word_host = *p->word;
-    *rc_a = state_result(p->host[0], ra);
-    *rc_b = state_result(p->host[1], rb);
+    *rc_a = series_result_of(p->host[0], ra);
+    *rc_b = series_result_of(p->host[1], rb);
     return ES_OK;
 }
 

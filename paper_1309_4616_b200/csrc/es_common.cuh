@@ -68,4 +68,11 @@ struct SeriesState {
     int pad_;
 };
 
+// Outcome of the fused small-grid exponential-Euler step, written by the
+// kernel into host-mapped pinned memory (series_small.cu, step.cu)
+struct SmallStepRecord {
+    SeriesState a, b;
+    unsigned long long bad;
+};
+
 }  // namespace es

@@ -115,9 +115,11 @@ int launch_expeuler_small_init(const SeriesParams *ha, SeriesParams *da, const S
                                unsigned long long *bad, int64_t n, cudaStream_t stream);
 int launch_series_small(const es_stencil_desc *d, const SeriesParams *dparams, const StencilPlan &pl, bool gd,
                         cudaStream_t stream);
+struct SmallStepRecord;
 int launch_expeuler_small(const es_stencil_desc *d, const SeriesParams *pa, const SeriesParams *pb,
                           const StencilPlan &pl, const double *u, double *gn, const double *source, int nonlin,
-                          double h, unsigned long long *bad, cudaStream_t stream);
+                          double h, unsigned long long *bad, SmallStepRecord *rec, cudaStream_t stream);
+int series_result_of(const SeriesState &st, es_series_result *res);
 int launch_axpy(const double *y, const double *z, double h, double *out, int64_t n, cudaStream_t st);
 int launch_scale(const double *x, double s, double *out, int64_t n, cudaStream_t st);
 int launch_combustion_f32(const float *u, float *out, int64_t n, cudaStream_t stream);

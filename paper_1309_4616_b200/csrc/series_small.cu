@@ -321,7 +321,8 @@ template <int COEFF, int ROWS>
 __global__ void __launch_bounds__(SMALL_THREADS) k_expeuler_small(const SeriesParams *__restrict__ PA,
                                                                   const SeriesParams *__restrict__ PB, const double *u,
                                                                   double *gn, const double *source, int nonlin,
-                                                                  double h, unsigned long long *bad, int ipc) {
+                                                                  double h, unsigned long long *bad, int ipc,
+                                                                  SmallStepRecord *rec) {
     __shared__ SmallShared sh;
     const int C = (int)gridDim.x / 2;  // CTAs per series
     const bool is_b = (int)blockIdx.x >= C;
@@ -372,6 +373,21 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_expeuler_small(const SeriesPa
     if (!skip) small_series<COEFF, false, ROWS>(P, g, c0, ipc, C, round0, sh, p, conv);
     // every CTA of both series: y and z complete, both states written
     small_barrier(PA->work, 2u * (unsigned)C);
+    if (rec && blockIdx.x == 0 && t == 0) {  // both outcomes straight into host-mapped memory (no copies)
+        rec->a = *PA->state;
+        SeriesState sb;
+        sb.k = __ldcg(&PB->state->k);
+        sb.consecutive = __ldcg(&PB->state->consecutive);
+        sb.done = __ldcg(&PB->state->done);
+        sb.converged = __ldcg(&PB->state->converged);
+        sb.last_term = __ldcg(&PB->state->last_term);
+        sb.last_pnorm = __ldcg(&PB->state->last_pnorm);
+        sb.pass = __ldcg(&PB->state->pass);
+        sb.pad_ = 0;
+        rec->b = sb;
+        rec->bad = __ldcg(bad);
+        __threadfence_system();
+    }
     if (is_b || !act) return;
     const bool ok = conv == 1 && __ldcg(&PB->state->converged) == 1 && __ldcg(&PB->state->k) > 0;
     if (!ok) return;
@@ -497,10 +513,10 @@ int launch_expeuler_small_init(const SeriesParams *ha, SeriesParams *da, const S
 
 int launch_expeuler_small(const es_stencil_desc *d, const SeriesParams *pa, const SeriesParams *pb,
                           const StencilPlan &pl, const double *u, double *gn, const double *source, int nonlin,
-                          double h, unsigned long long *bad, cudaStream_t stream) {
+                          double h, unsigned long long *bad, SmallStepRecord *rec, cudaStream_t stream) {
     int ipc = items_per_cta(pl);
-    void *args[] = {(void *)&pa, (void *)&pb, (void *)&u,   (void *)&gn, (void *)&source,
-                    (void *)&nonlin, (void *)&h, (void *)&bad, (void *)&ipc};
+    void *args[] = {(void *)&pa,     (void *)&pb, (void *)&u,   (void *)&gn,  (void *)&source,
+                    (void *)&nonlin, (void *)&h,  (void *)&bad, (void *)&ipc, (void *)&rec};
     if (cudaLaunchCooperativeKernel(expeuler_fn(d->coeff_kind, rows_for(pl)), dim3(2u * (unsigned)ctas_for(pl)),
                                     dim3(SMALL_THREADS), args, 0, stream) != cudaSuccess)
         return check_launch("small-grid exponential Euler step");

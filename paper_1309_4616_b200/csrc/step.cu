@@ -18,6 +18,7 @@
 // series that ran out of nodes leaves y / F / g_n intact for the caller's
 // halving rescue (matfunc.py:328-373).
 #include <cmath>
+#include <cstring>
 
 #include "es_common.cuh"
 #include "es_host.h"
@@ -32,6 +33,7 @@ struct Fork {
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr, t0 = nullptr, t1 = nullptr;
     unsigned long long *bad = nullptr, *bad_host = nullptr;
+    SmallStepRecord *rec_host = nullptr, *rec_dev = nullptr;  // host-mapped outcome of the small-grid step
 };
 thread_local Fork t_fork;
 
@@ -44,7 +46,9 @@ int fork_resources(Fork *&f) {
         cudaEventCreateWithFlags(&f->join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&f->t0) != cudaSuccess || cudaEventCreate(&f->t1) != cudaSuccess ||
         cudaMalloc(&f->bad, 2 * sizeof(unsigned long long)) != cudaSuccess ||  // k_fill_u64 writes two words
-        cudaMallocHost(&f->bad_host, sizeof(unsigned long long)) != cudaSuccess)
+        cudaMallocHost(&f->bad_host, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaHostAlloc(&f->rec_host, sizeof(SmallStepRecord), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&f->rec_dev, f->rec_host, 0) != cudaSuccess)
         return check_launch("step resources");
     f->device = dev;
     return ES_OK;
@@ -96,14 +100,15 @@ int run_expeuler_step(const es_stencil_desc *d, const double *u, double *u_out, 
         if (oka && okb && pa.nchunks == pb.nchunks && pa.chunk == pb.chunk) {
             cudaEventRecord(f->t0, s);
             if ((rc = launch_expeuler_small_init(&ha, da, &hb, db, f->bad, n, s))) return rc;
-            if ((rc = launch_expeuler_small(d, da, db, pa, u, g, source, nonlin, h, f->bad, s))) return rc;
+            if ((rc = launch_expeuler_small(d, da, db, pa, u, g, source, nonlin, h, f->bad, f->rec_dev, s))) return rc;
             cudaEventRecord(f->t1, s);
-            // both states and the domain word with one sync
-            int rca = ES_OK, rcb = ES_OK;
-            rc = read_series_states2(series_state_ptr(ws_exp), &res->exp_series, &rca, series_state_ptr(ws_phi),
-                                     &res->phi1_series, &rcb, f->bad, f->bad_host, s);
-            if (!rc) rc = series_status(rca, &res->status_exp);
-            if (!rc) rc = series_status(rcb, &res->status_phi1);
+            // both states and the domain word arrive in host-mapped memory: one sync, no copies
+            if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("small-grid step sync");
+            SmallStepRecord rec;
+            std::memcpy(&rec, f->rec_host, sizeof(rec));  // written by the kernel, complete after the sync
+            *f->bad_host = rec.bad;
+            rc = series_status(series_result_of(rec.a, &res->exp_series), &res->status_exp);
+            if (!rc) rc = series_status(series_result_of(rec.b, &res->phi1_series), &res->status_phi1);
             if (rc) return rc;
             fused = true;
         }
