@@ -868,6 +868,7 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
             if (!rc) rc = encode_map(&maps.m[MAP_T_PV], v, d, false, MK_P2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_P0], hp.pbuf[0], d, false, MK_P2);
             if (!rc) rc = encode_map(&maps.m[MAP_T_P1], hp.pbuf[1], d, false, MK_P2);
+            if (!rc) rc = encode_map(&maps.m[MAP_T_GP], gdiag, d, false, MK_P2);
             if (halos) {  // two-plane w halos by parity, g' boundary planes of the neighbours
                 es_stencil_desc d2 = *d;
                 d2.lz = 2;

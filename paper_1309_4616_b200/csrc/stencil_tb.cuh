@@ -57,8 +57,15 @@ constexpr int TB_GX = 68, TB_GY = TB_TY + 2;  // g': x0-2 .. x0+65, y0-1 .. y0+T
 #ifndef TB_SV
 #define TB_SV 5  // w_k window planes in flight between the warp groups (>= 4: j-2 .. j+1)
 #endif
+// TB_GP: group C's g' (interior of its output plane) rides in the P stage of
+// that plane instead of the shared G ring, so G slots are released by group
+// A alone and the ring no longer couples A to C's lag (A's top stall was the
+// G-full wait); the G ring shrinks to pay for the larger P stages
+#ifndef TB_GP
+#define TB_GP 0  // measured slower (573 vs 556 us per 512^3 node; shallower G / P rings), kept as an option
+#endif
 #ifndef TB_SG
-#define TB_SG 5
+#define TB_SG (TB_GP ? 3 : 5)
 #endif
 #ifndef TB_SP
 #define TB_SP 4
@@ -81,7 +88,8 @@ struct TbLayout {
     static constexpr int SW = GD ? TB_SW_GD : TB_SW_NG, SG = GD ? TB_SG : 0, SP = TB_SP;
     static constexpr int W_STAGE = (TB_WX * TB_WY * 8 + 127) & ~127;
     static constexpr int G_STAGE = (TB_GX * TB_GY * 8 + 127) & ~127;
-    static constexpr int P_STAGE = 64 * TB_TY * 8;
+    static constexpr int P_PLANE = 64 * TB_TY * 8;                     // p_{k-1} tile
+    static constexpr int P_STAGE = (GD && TB_GP ? 2 : 1) * P_PLANE;  // + g' tile of the same plane (TB_GP)
     static constexpr int V_SLOT = TB_EX * TB_EY * 8;
     static constexpr int W_OFF = 0;
     static constexpr int G_OFF = W_OFF + SW * W_STAGE;
@@ -132,6 +140,7 @@ ES_DEV TbItem tb_item_at(const TbItems &its, int i) {
 
 struct TbMaps {
     const CUtensorMap *w, *g, *p;
+    const CUtensorMap *gp = nullptr;  // g' interior tiles (64 x TB_TY) riding in the P stages (TB_GP)
     // peer-memory slabs: the neighbours' two w planes (this pass's parity) and g' planes, or null
     const CUtensorMap *hlo = nullptr, *hhi = nullptr, *glo = nullptr, *ghi = nullptr;
 };
@@ -187,6 +196,8 @@ ES_DEV void tb_produce(const Geom &g, const TbItems &its, const TbMaps &mp, char
                 if (up >= (uint32_t)Lt::SP) mbar_wait(&pempty[s], ((up / Lt::SP) - 1) & 1);
                 mbar_expect_tx(&pfull[s], Lt::P_STAGE);
                 tma_load(smem + Lt::P_OFF + s * Lt::P_STAGE, mp.p, &pfull[s], it.x0, it.y0, tg);
+                if constexpr (GD && TB_GP)
+                    tma_load(smem + Lt::P_OFF + s * Lt::P_STAGE + Lt::P_PLANE, mp.gp, &pfull[s], it.x0, it.y0, tg);
                 ++up;
             }
         }
@@ -497,7 +508,8 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
         // w_k at this thread's pairs of planes j-2, j-1 (centre values kept in
         // registers across planes: the zm / c of the next plane's stencil)
         double2 vm1[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}, vc1[2] = {vm1[0], vm1[1]};
-        uint32_t s1 = 0;  // V slot of plane j-1
+        uint32_t s1 = 0;      // V slot of plane j-1
+        uint32_t p_prev = 0;  // P slot of plane j-1 (TB_GP: held for its g')
 #pragma unroll 2
         for (int j = it.mb - 1; j <= it.me; ++j) {
             if (j > it.mb - 1) mbar_wait(&B.vfull[vr.slot], vr.phase);
@@ -509,6 +521,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                 vcur[h] = *reinterpret_cast<const double2 *>(Vj + (cw + TB_CW * h + 1) * TB_EX + 2 * q + 2);
             // ---- B: p_k of plane j (+ node k norms)
             double pk_cur[4] = {0.0, 0.0, 0.0, 0.0};
+            const uint32_t p_held = p_prev;  // P stage of plane j-1 (its g' serves part C below, TB_GP)
             if (j >= it.mb && j < it.me) {
                 mbar_wait(&B.pfull[pr.slot], pr.phase);
                 const double *Pc = reinterpret_cast<const double *>(smem + Lt::P_OFF + pr.slot * Lt::P_STAGE);
@@ -530,7 +543,11 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                                                        mul(pk_cur[2 * h + 1], pk_cur[2 * h + 1])));
                     }
                 }
-                warp_arrive(&B.pempty[pr.slot]);
+                if constexpr (GD && TB_GP) {
+                    p_prev = pr.slot;  // kept until part C of plane j (next iteration) read its g'
+                } else {
+                    warp_arrive(&B.pempty[pr.slot]);
+                }
                 pr.next();
             }
             // ---- C: w_{k+1}, p_{k+1} of plane j-1 (+ node k+1 norms); both rows side by side
@@ -538,7 +555,9 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
             if (two && jc >= it.mb && jc < it.me) {
                 const double *Vc = vslot(s1);
                 const double *Gc = nullptr;
-                if constexpr (GD) {
+                if constexpr (GD && TB_GP) {  // g' tile of plane j-1 in its (held) P stage, 64-wide rows
+                    Gc = reinterpret_cast<const double *>(smem + Lt::P_OFF + p_held * Lt::P_STAGE + Lt::P_PLANE);
+                } else if constexpr (GD) {
                     mbar_wait(&B.gfull[gr.slot], gr.phase);  // complete already; orders the TMA bytes for C
                     Gc = reinterpret_cast<const double *>(smem + Lt::G_OFF + gr.slot * Lt::G_STAGE);
                 }
@@ -557,7 +576,8 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                         l1 = mul(tb_coeff<COEFF>(g, xa + 1, ya[h], jc), l1);
                     }
                     if constexpr (GD) {
-                        const double2 gv = *reinterpret_cast<const double2 *>(Gc + (r + 1) * TB_GX + 2 * q + 2);
+                        const double2 gv = TB_GP ? *reinterpret_cast<const double2 *>(Gc + r * 64 + 2 * q)
+                                                 : *reinterpret_cast<const double2 *>(Gc + (r + 1) * TB_GX + 2 * q + 2);
                         l0 = sub(l0, mul(gv.x, cc.x));
                         l1 = sub(l1, mul(gv.y, cc.y));
                     }
@@ -576,7 +596,9 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                     acc_p1[h] = add(acc_p1[h], add(mul(pn[2 * h], pn[2 * h]), mul(pn[2 * h + 1], pn[2 * h + 1])));
                 }
             }
-            if constexpr (GD) {
+            if constexpr (GD && TB_GP) {
+                if (jc >= it.mb && jc < it.me) warp_arrive(&B.pempty[p_held]);  // P(j-1): p and g' both read
+            } else if constexpr (GD) {
                 if (jc >= it.mb - 1) {  // G(j-1): C's share of the release
                     warp_arrive(&B.gempty[gr.slot]);
                     gr.next();
@@ -595,7 +617,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
             off0 += plane;
         }
         warp_arrive(&B.vempty[s1]);  // V(me)
-        if constexpr (GD) {  // G(me)
+        if constexpr (GD && !TB_GP) {  // G(me)
             warp_arrive(&B.gempty[gr.slot]);
             gr.next();
         }
@@ -651,6 +673,7 @@ ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
               &M.m[k == 1 ? MAP_T_PV : ((k - 1) & 1) ? MAP_T_P1 : MAP_T_P0]};
     if (g.halo_lo) mp.hlo = &M.m[(pass & 1) ? MAP_T_HLO1 : MAP_T_HLO0];  // pass p reads halo parity p & 1
     if (g.halo_hi) mp.hhi = &M.m[(pass & 1) ? MAP_T_HHI1 : MAP_T_HHI0];
+    if (GD && TB_GP) mp.gp = &M.m[MAP_T_GP];
     if (GD && g.halo_lo) mp.glo = &M.m[MAP_T_GLO];
     if (GD && g.halo_hi) mp.ghi = &M.m[MAP_T_GHI];
     if (threadIdx.x == 0) {
@@ -661,7 +684,7 @@ ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
         }
         for (int s = 0; s < Lt::SG; ++s) {
             mbar_init(&B.gfull[s], 1);
-            mbar_init(&B.gempty[s], TB_AW + TB_CW);  // A and C groups
+            mbar_init(&B.gempty[s], TB_GP ? TB_AW : TB_AW + TB_CW);  // A (and C unless TB_GP)
         }
         for (int s = 0; s < Lt::SP; ++s) {
             mbar_init(&B.pfull[s], 1);
@@ -680,7 +703,7 @@ ES_DEV void tb_pass(const SeriesParams *P, int k, bool two, char *smem) {
             tma_acquire(mp.w);
             if (GD) tma_acquire(mp.g);
             tma_acquire(mp.p);
-            for (const CUtensorMap *h : {mp.hlo, mp.hhi, mp.glo, mp.ghi})
+            for (const CUtensorMap *h : {mp.hlo, mp.hhi, mp.glo, mp.ghi, mp.gp})
                 if (h) tma_acquire(h);
             tb_produce<GD>(g, its, mp, smem, true, P->work);
         }

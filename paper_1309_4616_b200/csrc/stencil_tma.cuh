@@ -54,7 +54,9 @@ enum {
     // two-node pass on a peer-memory slab: two-plane w halos by parity, g' boundary planes
     MAP_T_HLO0, MAP_T_HLO1, MAP_T_HHI0, MAP_T_HHI1, MAP_T_GLO, MAP_T_GHI, MAP_T_P0, MAP_T_P1,
     // two-node 2D pass (stencil_tb2d.cuh): 8-wide tails of the w rows, the 4-wide tail of the staged D
-    MAP_T2_W8_V, MAP_T2_W8_0, MAP_T2_W8_1, MAP_T2_G4, MAP_COUNT
+    MAP_T2_W8_V, MAP_T2_W8_0, MAP_T2_W8_1, MAP_T2_G4,
+    // two-node pass (TB_GP): g' interior tiles riding in the P stages
+    MAP_T_GP, MAP_COUNT
 };
 
 struct alignas(64) TmaMaps {
