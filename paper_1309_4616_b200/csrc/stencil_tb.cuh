@@ -65,10 +65,10 @@ constexpr int TB_GX = 68, TB_GY = TB_TY + 2;  // g': x0-2 .. x0+65, y0-1 .. y0+T
 #define TB_GP 0  // measured slower (573 vs 556 us per 512^3 node; shallower G / P rings), kept as an option
 #endif
 #ifndef TB_SG
-#define TB_SG (TB_GP ? 3 : 5)
+#define TB_SG (TB_GP ? 3 : 6)
 #endif
 #ifndef TB_SP
-#define TB_SP 4
+#define TB_SP 5
 #endif
 #ifndef TB_SW_GD
 #if TB_TY == 8
