@@ -40,7 +40,13 @@ namespace es {
 constexpr int T2_WX = T2_TX + 8;            // w_{k-1}: x0-4 .. x0+T2_TX+3
 constexpr int T2_EX = T2_TX + 4;            // w_k window / D: x0-2 .. x0+T2_TX+1
 constexpr int T2_PAIRS = T2_EX / 2;         // window pairs
-constexpr int T2_AW = 5, T2_CW = 4;         // group A / C warps
+#ifndef T2_AWARPS
+#define T2_AWARPS 5  // group A warps
+#endif
+#ifndef T2_CWARPS
+#define T2_CWARPS 4  // group C warps
+#endif
+constexpr int T2_AW = T2_AWARPS, T2_CW = T2_CWARPS;
 constexpr int T2_NA = 32 * T2_AW, T2_NC = 32 * T2_CW;
 constexpr int T2_THREADS = 32 * (T2_AW + T2_CW + 1);
 #ifndef T2_MINB
