@@ -68,13 +68,20 @@ static_assert(T2_NC * 2 * T2_CPT == T2_TX && T2_APT <= 2 && (T2_TX == 256 || T2_
 #ifndef T2_SV
 #define T2_SV 6
 #endif
+// T2_DP: group C's D (interior of its output row) rides in the P stage of
+// that row, so G stages are released by group A alone (no A-C coupling
+// through the G ring; shared memory is plentiful in 2D)
+#ifndef T2_DP
+#define T2_DP 1
+#endif
 
 template <bool STAGED>
 struct Tb2Layout {
     static constexpr int SW = T2_SW, SG = STAGED ? T2_SG : 0, SP = T2_SP, SV = T2_SV;
     static constexpr int W_STAGE = (T2_WX * 8 + 127) & ~127;
     static constexpr int G_STAGE = (T2_EX * 8 + 127) & ~127;
-    static constexpr int P_STAGE = T2_TX * 8;
+    static constexpr int P_ROW = T2_TX * 8;
+    static constexpr int P_STAGE = (STAGED && T2_DP ? 2 : 1) * P_ROW;  // p_{k-1} row (+ D row interior, T2_DP)
     static constexpr int V_SLOT = T2_EX * 8;
     static constexpr int W_OFF = 0;
     static constexpr int G_OFF = W_OFF + SW * W_STAGE;
@@ -118,6 +125,7 @@ struct Tb2Maps {
     const CUtensorMap *wa, *wb8;  // w_{k-1}: 256- and 8-wide row boxes
     const CUtensorMap *ga, *gb4;  // staged D: 256- and 4-wide row boxes
     const CUtensorMap *p;         // p_{k-1} (or v): 256-wide row box
+    const CUtensorMap *dp;        // staged D: 256-wide row box at x0 (T2_DP)
 };
 
 template <bool STAGED>
@@ -192,6 +200,11 @@ ES_DEV void tb2_produce(const Geom &g, const Tb2Items &its, const Tb2Maps &mp, c
                 char *dst = smem + Lt::P_OFF + s * Lt::P_STAGE;
 #pragma unroll
                 for (int b = 0; b < T2_TX / 256; ++b) tma_load(dst + 256 * 8 * b, mp.p, &B.pfull[s], it.x0 + 256 * b, tg);
+                if constexpr (STAGED && T2_DP) {
+#pragma unroll
+                    for (int b = 0; b < T2_TX / 256; ++b)
+                        tma_load(dst + Lt::P_ROW + 256 * 8 * b, mp.dp, &B.pfull[s], it.x0 + 256 * b, tg);
+                }
                 ++up;
             }
         }
@@ -423,6 +436,7 @@ ES_DEV void tb2_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
             pk_prev[h] = vm1[h] = vc1[h] = make_double2(0.0, 0.0);
         }
         uint32_t s1 = 0;
+        uint32_t p_prev = 0;  // P slot of row j-1 (T2_DP: held for its D)
         int64_t off0 = (int64_t)(it.mb - 1) * nx + it.x0 + 2 * c;  // element offset of pair h = 0 in row j
         auto flush = [&](double (&aw)[T2_CPT], double (&ap)[T2_CPT], int row, int64_t node_half) {
 #pragma unroll
@@ -454,6 +468,7 @@ ES_DEV void tb2_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
             double2 pk_cur[T2_CPT];
 #pragma unroll
             for (int h = 0; h < T2_CPT; ++h) pk_cur[h] = make_double2(0.0, 0.0);
+            const uint32_t p_held = p_prev;  // P stage of row j-1 (its D serves part C below, T2_DP)
             if (j >= it.mb && j < it.me) {
                 mbar_wait(&B.pfull[pr.slot], pr.phase);
                 const double *Pc = reinterpret_cast<const double *>(smem + Lt::P_OFF + pr.slot * Lt::P_STAGE);
@@ -471,7 +486,10 @@ ES_DEV void tb2_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
                     acc_w0[h] = add(acc_w0[h], add(mul(vcur[h].x, vcur[h].x), mul(vcur[h].y, vcur[h].y)));
                     acc_p0[h] = add(acc_p0[h], add(mul(pk_cur[h].x, pk_cur[h].x), mul(pk_cur[h].y, pk_cur[h].y)));
                 }
-                warp_arrive(&B.pempty[pr.slot]);
+                if constexpr (STAGED && T2_DP)
+                    p_prev = pr.slot;  // kept until part C of row j (next iteration) read its D
+                else
+                    warp_arrive(&B.pempty[pr.slot]);
                 pr.next();
                 if ((j + 1) % CL == 0 || j + 1 == it.me) flush(acc_w0, acc_p0, j, 0);
             }
@@ -479,8 +497,10 @@ ES_DEV void tb2_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
             const int jc = j - 1;
             if (two && jc >= it.mb && jc < it.me) {
                 const double *Vc = vslot(s1);
-                const double *Gc = nullptr;
-                if constexpr (STAGED) {
+                const double *Gc = nullptr;  // D of row j-1, indexed from x0 - 2
+                if constexpr (STAGED && T2_DP) {
+                    Gc = reinterpret_cast<const double *>(smem + Lt::P_OFF + p_held * Lt::P_STAGE + Lt::P_ROW) - 2;
+                } else if constexpr (STAGED) {
                     mbar_wait(&B.gfull[gr.slot], gr.phase);  // complete already; orders the TMA bytes for C
                     Gc = reinterpret_cast<const double *>(smem + Lt::G_OFF + gr.slot * Lt::G_STAGE);
                 }
@@ -511,7 +531,9 @@ ES_DEV void tb2_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
                 }
                 if ((jc + 1) % CL == 0 || jc + 1 == it.me) flush(acc_w1, acc_p1, jc, half);
             }
-            if constexpr (STAGED) {
+            if constexpr (STAGED && T2_DP) {
+                if (jc >= it.mb && jc < it.me) warp_arrive(&B.pempty[p_held]);  // P(j-1): p and D both read
+            } else if constexpr (STAGED) {
                 if (jc >= it.mb - 1) {  // G(j-1): C's share of the release
                     warp_arrive(&B.gempty[gr.slot]);
                     gr.next();
@@ -529,7 +551,7 @@ ES_DEV void tb2_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
             off0 += nx;
         }
         warp_arrive(&B.vempty[s1]);  // V(me)
-        if constexpr (STAGED) {  // G(me)
+        if constexpr (STAGED && !T2_DP) {  // G(me)
             warp_arrive(&B.gempty[gr.slot]);
             gr.next();
         }
@@ -547,7 +569,7 @@ ES_DEV void tb2_pass(const SeriesParams *P, int k, bool two, char *smem) {
     const int wi = pass == 0 ? 0 : (pass & 1) ? 1 : 2;  // v, wbuf[0], wbuf[1]
     const Tb2Maps mp{&M.m[wi == 0 ? MAP_WA_V : wi == 1 ? MAP_WA_0 : MAP_WA_1],
                      &M.m[wi == 0 ? MAP_T2_W8_V : wi == 1 ? MAP_T2_W8_0 : MAP_T2_W8_1], &M.m[MAP_G],
-                     &M.m[MAP_T2_G4], &M.m[k == 1 ? MAP_WA_V : ((k - 1) & 1) ? MAP_P_1 : MAP_P_0]};
+                     &M.m[MAP_T2_G4], &M.m[k == 1 ? MAP_WA_V : ((k - 1) & 1) ? MAP_P_1 : MAP_P_0], &M.m[MAP_G]};
     if (threadIdx.x == 0) {
         const Tb2Bars<STAGED> B(smem);
         for (int s = 0; s < Lt::SW; ++s) {
@@ -556,7 +578,7 @@ ES_DEV void tb2_pass(const SeriesParams *P, int k, bool two, char *smem) {
         }
         for (int s = 0; s < Lt::SG; ++s) {
             mbar_init(&B.gfull[s], 1);
-            mbar_init(&B.gempty[s], T2_AW + T2_CW);
+            mbar_init(&B.gempty[s], STAGED && T2_DP ? T2_AW : T2_AW + T2_CW);
         }
         for (int s = 0; s < Lt::SP; ++s) {
             mbar_init(&B.pfull[s], 1);
