@@ -266,13 +266,13 @@ __global__ void __launch_bounds__(TB_THREADS, TB_MINB) k_node_tb(const SeriesPar
 }
 
 // Two Leja nodes per pass on a single-plane grid (stencil_tb2d.cuh).
-template <bool STAGED>
+template <bool STAGED, bool R8>
 __global__ void __launch_bounds__(T2_THREADS, T2_MINB) k_node_tb2d(const SeriesParams *__restrict__ Pp) {
     extern __shared__ __align__(128) char tsmem[];
     const SeriesParams &P = *Pp;
     if (P.state->done) return;
     const int k = P.state->k + 1;
-    tb2_pass<STAGED>(Pp, k, tb_two(P, k), tsmem);
+    tb2_pass<STAGED, R8>(Pp, k, tb_two(P, k), tsmem);
 }
 
 __global__ void __launch_bounds__(256) k_slice_reduce2(const SeriesParams *__restrict__ Pp) {
@@ -482,7 +482,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // MK_W2 / MK_G2 / MK_P2 / MK_GH2: the two-node pass's tiles (stencil_tb.cuh)
-enum MapKind { MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3, MK_W2 = 4, MK_G2 = 5, MK_P2 = 6, MK_GH2 = 7, MK_WTAIL8 = 8 };
+enum MapKind {
+    MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3, MK_W2 = 4, MK_G2 = 5, MK_P2 = 6, MK_GH2 = 7, MK_WTAIL8 = 8,
+    MK_R8W = 9, MK_R8P = 10  // 2D row as 8-element chunks: (T2_TX + 16) window / T2_TX interior
+};
 
 // TMA descriptor of a slab-shaped fp64 vector (x fastest); OOB reads are
 // zero-filled, which is the homogeneous Dirichlet ghost rule.
@@ -494,7 +497,17 @@ static int encode_map(CUtensorMap *m, const double *base, const es_stencil_desc 
     cuuint64_t dims[3], strides[2];
     cuuint32_t box[3], estr[3] = {1, 1, 1};
     cuuint32_t rank;
-    if (kind == MK_HALO || kind == MK_GH2) {  // one (ny, nx) plane, same box as the 3D W (g') tiles
+    if (kind == MK_R8W || kind == MK_R8P) {  // (8, nx/8, ny) view of a single-plane grid (nx % 8 == 0)
+        rank = 3;
+        dims[0] = 8;
+        dims[1] = (cuuint64_t)d->nx / 8;
+        dims[2] = (cuuint64_t)d->ny;
+        strides[0] = 64;
+        strides[1] = (cuuint64_t)d->nx * 8;
+        box[0] = 8;
+        box[1] = (kind == MK_R8W ? T2_RX : T2_TX) / 8;
+        box[2] = 1;
+    } else if (kind == MK_HALO || kind == MK_GH2) {  // one (ny, nx) plane, same box as the 3D W (g') tiles
         rank = 2;
         dims[0] = (cuuint64_t)d->nx;
         dims[1] = (cuuint64_t)d->ny;
@@ -731,6 +744,7 @@ struct SeriesSetup {
     int64_t n;
     bool tb = false;   // two nodes per pass (k_node_tb + k_slice_reduce2)
     bool tb2 = false;  // two nodes per pass on a single-plane grid (k_node_tb2d + k_slice_reduce2)
+    bool r8 = false;   // ... with the (8, nx/8, ny) row view (one TMA per row window)
     bool staged = false;  // sampled coefficient through the PG ring (ES_COEFF_STAGED)
 };
 
@@ -792,7 +806,9 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
     if (pl.tma) {
         if (S.tb2) {
             S.staged = d->coeff_kind == ES_COEFF_ARRAY;
-            S.nf = S.staged ? k_node_tb2d<true> : k_node_tb2d<false>;
+            S.r8 = d->nx % 8 == 0 && env_int("ES_TB2R8", 1);
+            S.nf = S.staged ? (S.r8 ? k_node_tb2d<true, true> : k_node_tb2d<true, false>)
+                            : (S.r8 ? k_node_tb2d<false, true> : k_node_tb2d<false, false>);
             finish_tma_plan(S.lp, (const void *)S.nf,
                             S.staged ? (size_t)Tb2Layout<true>::BYTES : (size_t)Tb2Layout<false>::BYTES, T2_THREADS);
         } else if (S.tb) {
@@ -859,6 +875,16 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
             if (!rc) rc = encode_map(&maps.m[MAP_T2_W8_0], hp.wbuf[0], d, true, MK_WTAIL8);
             if (!rc) rc = encode_map(&maps.m[MAP_T2_W8_1], hp.wbuf[1], d, true, MK_WTAIL8);
             if (!rc) rc = encode_map(&maps.m[MAP_T2_G4], S.staged ? d->coeff : nullptr, d, true, MK_WTAIL);
+            if (S.r8) {
+                if (!rc) rc = encode_map(&maps.m[MAP_T2R_W_V], v, d, true, MK_R8W);
+                if (!rc) rc = encode_map(&maps.m[MAP_T2R_W_0], hp.wbuf[0], d, true, MK_R8W);
+                if (!rc) rc = encode_map(&maps.m[MAP_T2R_W_1], hp.wbuf[1], d, true, MK_R8W);
+                if (!rc) rc = encode_map(&maps.m[MAP_T2R_G], S.staged ? d->coeff : nullptr, d, true, MK_R8W);
+                if (!rc) rc = encode_map(&maps.m[MAP_T2R_P_V], v, d, true, MK_R8P);
+                if (!rc) rc = encode_map(&maps.m[MAP_T2R_P_0], hp.pbuf[0], d, true, MK_R8P);
+                if (!rc) rc = encode_map(&maps.m[MAP_T2R_P_1], hp.pbuf[1], d, true, MK_R8P);
+                if (!rc) rc = encode_map(&maps.m[MAP_T2R_D], S.staged ? d->coeff : nullptr, d, true, MK_R8P);
+            }
         }
         if (S.tb) {
             if (!rc) rc = encode_map(&maps.m[MAP_T_V], v, d, false, MK_W2);

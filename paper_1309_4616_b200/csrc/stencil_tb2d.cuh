@@ -39,6 +39,11 @@ namespace es {
 #endif
 constexpr int T2_WX = T2_TX + 8;            // w_{k-1}: x0-4 .. x0+T2_TX+3
 constexpr int T2_EX = T2_TX + 4;            // w_k window / D: x0-2 .. x0+T2_TX+1
+// R8 (nx % 8 == 0): the row viewed as 8-element chunks -- a 3D tensor map
+// (8, nx/8, ny) whose box (8, TX/8 + 2, 1) covers x0-8 .. x0+TX+7 contiguously
+// -- so a w or D row window is ONE TMA (two on the plain row maps: boxes are
+// at most 256 wide); the producer's issue rate was the pass's limit
+constexpr int T2_RX = T2_TX + 16;           // R8 row window: x0-8 .. x0+T2_TX+7
 constexpr int T2_PAIRS = T2_EX / 2;         // window pairs
 #ifndef T2_AWARPS
 #define T2_AWARPS 5  // group A warps
@@ -78,8 +83,8 @@ static_assert(T2_NC * 2 * T2_CPT == T2_TX && T2_APT <= 2 && (T2_TX == 256 || T2_
 template <bool STAGED>
 struct Tb2Layout {
     static constexpr int SW = T2_SW, SG = STAGED ? T2_SG : 0, SP = T2_SP, SV = T2_SV;
-    static constexpr int W_STAGE = (T2_WX * 8 + 127) & ~127;
-    static constexpr int G_STAGE = (T2_EX * 8 + 127) & ~127;
+    static constexpr int W_STAGE = (T2_RX * 8 + 127) & ~127;  // holds either window
+    static constexpr int G_STAGE = (T2_RX * 8 + 127) & ~127;
     static constexpr int P_ROW = T2_TX * 8;
     static constexpr int P_STAGE = (STAGED && T2_DP ? 2 : 1) * P_ROW;  // p_{k-1} row (+ D row interior, T2_DP)
     static constexpr int V_SLOT = T2_EX * 8;
@@ -153,7 +158,7 @@ ES_DEV int tb2_row(const Geom &g, int t) {
     return t;
 }
 
-template <bool STAGED>
+template <bool STAGED, bool R8>
 ES_DEV void tb2_produce(const Geom &g, const Tb2Items &its, const Tb2Maps &mp, char *smem, unsigned *work) {
     using Lt = Tb2Layout<STAGED>;
     const Tb2Bars<STAGED> B(smem);
@@ -170,12 +175,17 @@ ES_DEV void tb2_produce(const Geom &g, const Tb2Items &its, const Tb2Maps &mp, c
                 const uint32_t s = uw % Lt::SW;
                 if (uw >= (uint32_t)Lt::SW) mbar_wait(&B.wempty[s], ((uw / Lt::SW) - 1) & 1);
                 itemq[s] = i;
-                mbar_expect_tx(&B.wfull[s], T2_WX * 8);
+                mbar_expect_tx(&B.wfull[s], (R8 ? T2_RX : T2_WX) * 8);
                 char *dst = smem + Lt::W_OFF + s * Lt::W_STAGE;
                 const int r = tb2_row(g, t);
+                if constexpr (R8) {
+                    tma_load(dst, mp.wa, &B.wfull[s], 0, (it.x0 - 8) / 8, r);
+                } else {
 #pragma unroll
-                for (int b = 0; b < T2_TX / 256; ++b) tma_load(dst + 256 * 8 * b, mp.wa, &B.wfull[s], it.x0 - 4 + 256 * b, r);
-                tma_load(dst + T2_TX * 8, mp.wb8, &B.wfull[s], it.x0 + T2_TX - 4, r);
+                    for (int b = 0; b < T2_TX / 256; ++b)
+                        tma_load(dst + 256 * 8 * b, mp.wa, &B.wfull[s], it.x0 - 4 + 256 * b, r);
+                    tma_load(dst + T2_TX * 8, mp.wb8, &B.wfull[s], it.x0 + T2_TX - 4, r);
+                }
                 ++uw;
             }
             const int tg = t - 1;  // G(t-1), P(t-1): what consumer row t-1 needs besides W(t)
@@ -183,13 +193,17 @@ ES_DEV void tb2_produce(const Geom &g, const Tb2Items &its, const Tb2Maps &mp, c
                 if (tg >= it.mb - 1 && tg <= it.me) {
                     const uint32_t s = ug % Lt::SG;
                     if (ug >= (uint32_t)Lt::SG) mbar_wait(&B.gempty[s], ((ug / Lt::SG) - 1) & 1);
-                    mbar_expect_tx(&B.gfull[s], T2_EX * 8);
+                    mbar_expect_tx(&B.gfull[s], (R8 ? T2_RX : T2_EX) * 8);
                     char *dst = smem + Lt::G_OFF + s * Lt::G_STAGE;
                     const int r = tb2_row(g, tg);
+                    if constexpr (R8) {
+                        tma_load(dst, mp.ga, &B.gfull[s], 0, (it.x0 - 8) / 8, r);
+                    } else {
 #pragma unroll
-                    for (int b = 0; b < T2_TX / 256; ++b)
-                        tma_load(dst + 256 * 8 * b, mp.ga, &B.gfull[s], it.x0 - 2 + 256 * b, r);
-                    tma_load(dst + T2_TX * 8, mp.gb4, &B.gfull[s], it.x0 + T2_TX - 2, r);
+                        for (int b = 0; b < T2_TX / 256; ++b)
+                            tma_load(dst + 256 * 8 * b, mp.ga, &B.gfull[s], it.x0 - 2 + 256 * b, r);
+                        tma_load(dst + T2_TX * 8, mp.gb4, &B.gfull[s], it.x0 + T2_TX - 2, r);
+                    }
                     ++ug;
                 }
             }
@@ -198,12 +212,18 @@ ES_DEV void tb2_produce(const Geom &g, const Tb2Items &its, const Tb2Maps &mp, c
                 if (up >= (uint32_t)Lt::SP) mbar_wait(&B.pempty[s], ((up / Lt::SP) - 1) & 1);
                 mbar_expect_tx(&B.pfull[s], Lt::P_STAGE);
                 char *dst = smem + Lt::P_OFF + s * Lt::P_STAGE;
-#pragma unroll
-                for (int b = 0; b < T2_TX / 256; ++b) tma_load(dst + 256 * 8 * b, mp.p, &B.pfull[s], it.x0 + 256 * b, tg);
-                if constexpr (STAGED && T2_DP) {
+                if constexpr (R8) {
+                    tma_load(dst, mp.p, &B.pfull[s], 0, it.x0 / 8, tg);
+                    if constexpr (STAGED && T2_DP) tma_load(dst + Lt::P_ROW, mp.dp, &B.pfull[s], 0, it.x0 / 8, tg);
+                } else {
 #pragma unroll
                     for (int b = 0; b < T2_TX / 256; ++b)
-                        tma_load(dst + Lt::P_ROW + 256 * 8 * b, mp.dp, &B.pfull[s], it.x0 + 256 * b, tg);
+                        tma_load(dst + 256 * 8 * b, mp.p, &B.pfull[s], it.x0 + 256 * b, tg);
+                    if constexpr (STAGED && T2_DP) {
+#pragma unroll
+                        for (int b = 0; b < T2_TX / 256; ++b)
+                            tma_load(dst + Lt::P_ROW + 256 * 8 * b, mp.dp, &B.pfull[s], it.x0 + 256 * b, tg);
+                    }
                 }
                 ++up;
             }
@@ -223,9 +243,10 @@ ES_DEV void a2_group_sync() { asm volatile("bar.sync 2, %0;" ::"n"(T2_NA) : "mem
 // points outside the domain masked to the zero ghost.  Neumann: window
 // points outside the domain take w_k of the mirrored point, and stencils at
 // the domain edge use the point itself as the ghost.
-template <bool STAGED>
+template <bool STAGED, bool R8>
 ES_DEV double2 tb2_pair(const Geom &g, const double *Wm, const double *Wc, const double *Wp, const double *Gj,
                         int x0, int e, double alpha, double beta, bool neu, double wx, double wy, double wz) {
+    constexpr int WO = R8 ? 8 : 4, GO = R8 ? 8 : 2;  // window origins x0 - WO (w_{k-1}), x0 - GO (D)
     const int64_t nx = g.nx;
     const int64_t xa = x0 - 2 + 2 * e;
     double out[2];
@@ -234,7 +255,7 @@ ES_DEV double2 tb2_pair(const Geom &g, const double *Wm, const double *Wc, const
         int64_t x = xa + h;
         const bool in = x >= 0 && x < nx;
         if (neu) x = min(max(x, (int64_t)0), nx - 1);
-        const int o = (int)(x - (x0 - 4));  // W index
+        const int o = (int)(x - (x0 - WO));  // W index
         const double c = Wc[o];
         double xm = Wc[o - 1], xp = Wc[o + 1];
         if (neu) {
@@ -243,7 +264,7 @@ ES_DEV double2 tb2_pair(const Geom &g, const double *Wm, const double *Wc, const
         }
         const double z = neu ? c : 0.0;
         double lap = lap7(c, xm, xp, Wm[o], Wp[o], z, z, wx, wy, wz);
-        if constexpr (STAGED) lap = mul(Gj[x - (x0 - 2)], lap);
+        if constexpr (STAGED) lap = mul(Gj[x - (x0 - GO)], lap);
         const double w = add(mul(alpha, lap), mul(beta, c));
         out[h] = (neu || in) ? w : 0.0;
     }
@@ -253,10 +274,11 @@ ES_DEV double2 tb2_pair(const Geom &g, const double *Wm, const double *Wc, const
 // tb2_pair where neither point needs a ghost rule: x0-2+2e .. +1 inside
 // [1, nx-2] (Neumann) / the domain (Dirichlet: TMA's zero fill is the
 // ghost of w_{k-1}; points outside are masked by the caller).  Pair loads.
-template <bool STAGED>
+template <bool STAGED, bool R8>
 ES_DEV double2 tb2_pair_fast(const double *Wm, const double *Wc, const double *Wp, const double *Gj, int e,
                              double alpha, double beta, bool neu, double wx, double wy, double wz) {
-    const int o = 2 + 2 * e;  // W index of x = x0 - 2 + 2e
+    constexpr int WO = R8 ? 8 : 4, GO = R8 ? 8 : 2;
+    const int o = WO - 2 + 2 * e;  // W index of x = x0 - 2 + 2e
     const double2 c = *reinterpret_cast<const double2 *>(Wc + o);
     const double2 ym = *reinterpret_cast<const double2 *>(Wm + o);
     const double2 yp = *reinterpret_cast<const double2 *>(Wp + o);
@@ -264,14 +286,14 @@ ES_DEV double2 tb2_pair_fast(const double *Wm, const double *Wc, const double *W
     double l0 = lap7(c.x, Wc[o - 1], c.y, ym.x, yp.x, z0, z0, wx, wy, wz);
     double l1 = lap7(c.y, c.x, Wc[o + 2], ym.y, yp.y, z1, z1, wx, wy, wz);
     if constexpr (STAGED) {
-        const double2 d = *reinterpret_cast<const double2 *>(Gj + 2 * e);
+        const double2 d = *reinterpret_cast<const double2 *>(Gj + GO - 2 + 2 * e);
         l0 = mul(d.x, l0);
         l1 = mul(d.y, l1);
     }
     return make_double2(add(mul(alpha, l0), mul(beta, c.x)), add(mul(alpha, l1), mul(beta, c.y)));
 }
 
-template <bool STAGED>
+template <bool STAGED, bool R8>
 ES_DEV void tb2_group_a(const Geom &g, const SeriesParams *P, int k, const Tb2Items &its, char *smem) {
     using Lt = Tb2Layout<STAGED>;
     const Tb2Bars<STAGED> B(smem);
@@ -343,7 +365,7 @@ ES_DEV void tb2_group_a(const Geom &g, const SeriesParams *P, int k, const Tb2It
 #pragma unroll
                     for (int h = 0; h < T2_APT; ++h) {
                         const int e = valid[h] ? a + T2_NA * h : 0;  // a spare lane computes pair 0, stores nothing
-                        wk[h] = tb2_pair_fast<STAGED>(Wm, Wc, Wp, Gj, e, alpha, beta_k, neu, wx, wy, wz);
+                        wk[h] = tb2_pair_fast<STAGED, R8>(Wm, Wc, Wp, Gj, e, alpha, beta_k, neu, wx, wy, wz);
                         if (!neu) wk[h] = make_double2(in0[h] ? wk[h].x : 0.0, in1[h] ? wk[h].y : 0.0);
                     }
 #pragma unroll
@@ -355,8 +377,8 @@ ES_DEV void tb2_group_a(const Geom &g, const SeriesParams *P, int k, const Tb2It
                         if (!valid[h]) continue;
                         const int e = a + T2_NA * h;
                         *reinterpret_cast<double2 *>(Vj + 2 * e) =
-                            fast[h] ? tb2_pair_fast<STAGED>(Wm, Wc, Wp, Gj, e, alpha, beta_k, neu, wx, wy, wz)
-                                    : tb2_pair<STAGED>(g, Wm, Wc, Wp, Gj, it.x0, e, alpha, beta_k, neu, wx, wy, wz);
+                            fast[h] ? tb2_pair_fast<STAGED, R8>(Wm, Wc, Wp, Gj, e, alpha, beta_k, neu, wx, wy, wz)
+                                    : tb2_pair<STAGED, R8>(g, Wm, Wc, Wp, Gj, it.x0, e, alpha, beta_k, neu, wx, wy, wz);
                     }
                 }
                 if (neu && j == 0) {  // the mirrored row below the domain = w_k of row 0
@@ -558,7 +580,7 @@ ES_DEV void tb2_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
     }
 }
 
-template <bool STAGED>
+template <bool STAGED, bool R8>
 ES_DEV void tb2_pass(const SeriesParams *P, int k, bool two, char *smem) {
     using Lt = Tb2Layout<STAGED>;
     const Geom g = P->g;
@@ -567,9 +589,13 @@ ES_DEV void tb2_pass(const SeriesParams *P, int k, bool two, char *smem) {
     const int pass = P->state->pass;
     // W: w_{k-1} (v on the first pass; pass p writes wbuf[p & 1]); P: p_{k-1} (v on the first pass)
     const int wi = pass == 0 ? 0 : (pass & 1) ? 1 : 2;  // v, wbuf[0], wbuf[1]
-    const Tb2Maps mp{&M.m[wi == 0 ? MAP_WA_V : wi == 1 ? MAP_WA_0 : MAP_WA_1],
-                     &M.m[wi == 0 ? MAP_T2_W8_V : wi == 1 ? MAP_T2_W8_0 : MAP_T2_W8_1], &M.m[MAP_G],
-                     &M.m[MAP_T2_G4], &M.m[k == 1 ? MAP_WA_V : ((k - 1) & 1) ? MAP_P_1 : MAP_P_0], &M.m[MAP_G]};
+    const int pi = k == 1 ? 0 : ((k - 1) & 1) ? 2 : 1;  // p_{k-1}: v, pbuf[0], pbuf[1]
+    const Tb2Maps mp = R8 ? Tb2Maps{&M.m[MAP_T2R_W_V + wi], nullptr, &M.m[MAP_T2R_G], nullptr, &M.m[MAP_T2R_P_V + pi],
+                                    &M.m[MAP_T2R_D]}
+                          : Tb2Maps{&M.m[wi == 0 ? MAP_WA_V : wi == 1 ? MAP_WA_0 : MAP_WA_1],
+                                    &M.m[wi == 0 ? MAP_T2_W8_V : wi == 1 ? MAP_T2_W8_0 : MAP_T2_W8_1], &M.m[MAP_G],
+                                    &M.m[MAP_T2_G4], &M.m[k == 1 ? MAP_WA_V : ((k - 1) & 1) ? MAP_P_1 : MAP_P_0],
+                                    &M.m[MAP_G]};
     if (threadIdx.x == 0) {
         const Tb2Bars<STAGED> B(smem);
         for (int s = 0; s < Lt::SW; ++s) {
@@ -594,17 +620,15 @@ ES_DEV void tb2_pass(const SeriesParams *P, int k, bool two, char *smem) {
     const int warp = threadIdx.x / 32;
     if (warp == T2_AW + T2_CW) {
         if ((threadIdx.x & 31) == 0) {
-            tma_acquire(mp.wa);
-            tma_acquire(mp.wb8);
-            if (STAGED) {
-                tma_acquire(mp.ga);
-                tma_acquire(mp.gb4);
-            }
-            tma_acquire(mp.p);
-            tb2_produce<STAGED>(g, its, mp, smem, P->work);
+            for (const CUtensorMap *m : {mp.wa, mp.wb8, mp.p})
+                if (m) tma_acquire(m);
+            if (STAGED)
+                for (const CUtensorMap *m : {mp.ga, mp.gb4, mp.dp})
+                    if (m) tma_acquire(m);
+            tb2_produce<STAGED, R8>(g, its, mp, smem, P->work);
         }
     } else if (warp < T2_AW) {
-        tb2_group_a<STAGED>(g, P, k, its, smem);
+        tb2_group_a<STAGED, R8>(g, P, k, its, smem);
     } else {
         tb2_group_c<STAGED>(g, P, k, two, its, smem);
     }

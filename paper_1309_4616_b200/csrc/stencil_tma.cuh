@@ -56,7 +56,10 @@ enum {
     // two-node 2D pass (stencil_tb2d.cuh): 8-wide tails of the w rows, the 4-wide tail of the staged D
     MAP_T2_W8_V, MAP_T2_W8_0, MAP_T2_W8_1, MAP_T2_G4,
     // two-node pass (TB_GP): g' interior tiles riding in the P stages
-    MAP_T_GP, MAP_COUNT
+    MAP_T_GP,
+    // two-node 2D pass, R8 row view (8, nx/8, ny): w windows (v, wbuf[0], wbuf[1]), D window,
+    // p rows (v, pbuf[0], pbuf[1]), D row interior
+    MAP_T2R_W_V, MAP_T2R_W_0, MAP_T2R_W_1, MAP_T2R_G, MAP_T2R_P_V, MAP_T2R_P_0, MAP_T2R_P_1, MAP_T2R_D, MAP_COUNT
 };
 
 struct alignas(64) TmaMaps {
