@@ -11,6 +11,7 @@
 #include "series.cuh"
 #include "stencil_tma.cuh"
 #include "stencil_tb2d.cuh"
+#include "stencil_tb2r.cuh"
 #include "stencil_tb.cuh"
 
 #include <cudaTypedefs.h>
@@ -275,6 +276,16 @@ __global__ void __launch_bounds__(T2_THREADS, T2_MINB) k_node_tb2d(const SeriesP
     tb2_pass<STAGED, R8>(Pp, k, tb_two(P, k), tsmem);
 }
 
+// Two Leja nodes per pass on a single-plane grid, T3_R rows per stage (stencil_tb2r.cuh).
+template <bool STAGED>
+__global__ void __launch_bounds__(T2_THREADS, 2) k_node_tb2r(const SeriesParams *__restrict__ Pp) {
+    extern __shared__ __align__(128) char tsmem[];
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    const int k = P.state->k + 1;
+    tb3_pass<STAGED, T3_R>(Pp, k, tb_two(P, k), tsmem);
+}
+
 __global__ void __launch_bounds__(256) k_slice_reduce2(const SeriesParams *__restrict__ Pp) {
     const SeriesParams &P = *Pp;
     if (P.state->done) return;
@@ -484,7 +495,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // MK_W2 / MK_G2 / MK_P2 / MK_GH2: the two-node pass's tiles (stencil_tb.cuh)
 enum MapKind {
     MK_W = 0, MK_WTAIL = 1, MK_P = 2, MK_HALO = 3, MK_W2 = 4, MK_G2 = 5, MK_P2 = 6, MK_GH2 = 7, MK_WTAIL8 = 8,
-    MK_R8W = 9, MK_R8P = 10  // 2D row as 8-element chunks: (T2_TX + 16) window / T2_TX interior
+    MK_R8W = 9, MK_R8P = 10,  // 2D row as 8-element chunks: (T2_TX + 16) window / T2_TX interior
+    MK_R8W_R = 11, MK_R8P_R = 12  // ... T3_R rows per box
 };
 
 // TMA descriptor of a slab-shaped fp64 vector (x fastest); OOB reads are
@@ -497,7 +509,7 @@ static int encode_map(CUtensorMap *m, const double *base, const es_stencil_desc 
     cuuint64_t dims[3], strides[2];
     cuuint32_t box[3], estr[3] = {1, 1, 1};
     cuuint32_t rank;
-    if (kind == MK_R8W || kind == MK_R8P) {  // (8, nx/8, ny) view of a single-plane grid (nx % 8 == 0)
+    if (kind == MK_R8W || kind == MK_R8P || kind == MK_R8W_R || kind == MK_R8P_R) {  // (8, nx/8, ny) row view
         rank = 3;
         dims[0] = 8;
         dims[1] = (cuuint64_t)d->nx / 8;
@@ -505,8 +517,8 @@ static int encode_map(CUtensorMap *m, const double *base, const es_stencil_desc 
         strides[0] = 64;
         strides[1] = (cuuint64_t)d->nx * 8;
         box[0] = 8;
-        box[1] = (kind == MK_R8W ? T2_RX : T2_TX) / 8;
-        box[2] = 1;
+        box[1] = (kind == MK_R8W || kind == MK_R8W_R ? T2_RX : T2_TX) / 8;
+        box[2] = kind == MK_R8W_R || kind == MK_R8P_R ? T3_R : 1;
     } else if (kind == MK_HALO || kind == MK_GH2) {  // one (ny, nx) plane, same box as the 3D W (g') tiles
         rank = 2;
         dims[0] = (cuuint64_t)d->nx;
@@ -745,6 +757,7 @@ struct SeriesSetup {
     bool tb = false;   // two nodes per pass (k_node_tb + k_slice_reduce2)
     bool tb2 = false;  // two nodes per pass on a single-plane grid (k_node_tb2d + k_slice_reduce2)
     bool r8 = false;   // ... with the (8, nx/8, ny) row view (one TMA per row window)
+    bool rows = false; // ... and stages of T3_R rows (k_node_tb2r)
     bool staged = false;  // sampled coefficient through the PG ring (ES_COEFF_STAGED)
 };
 
@@ -807,10 +820,19 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
         if (S.tb2) {
             S.staged = d->coeff_kind == ES_COEFF_ARRAY;
             S.r8 = d->nx % 8 == 0 && env_int("ES_TB2R8", 1);
-            S.nf = S.staged ? (S.r8 ? k_node_tb2d<true, true> : k_node_tb2d<true, false>)
-                            : (S.r8 ? k_node_tb2d<false, true> : k_node_tb2d<false, false>);
-            finish_tma_plan(S.lp, (const void *)S.nf,
-                            S.staged ? (size_t)Tb2Layout<true>::BYTES : (size_t)Tb2Layout<false>::BYTES, T2_THREADS);
+            S.rows = S.r8 && env_int("ES_TB2R", 0) && chunk2 % T3_R == 0;  // multi-row stages (measured slower: off)
+            if (S.rows) {
+                S.nf = S.staged ? k_node_tb2r<true> : k_node_tb2r<false>;
+                finish_tma_plan(S.lp, (const void *)S.nf,
+                                S.staged ? (size_t)Tb3Layout<true, T3_R>::BYTES : (size_t)Tb3Layout<false, T3_R>::BYTES,
+                                T2_THREADS);
+            } else {
+                S.nf = S.staged ? (S.r8 ? k_node_tb2d<true, true> : k_node_tb2d<true, false>)
+                                : (S.r8 ? k_node_tb2d<false, true> : k_node_tb2d<false, false>);
+                finish_tma_plan(S.lp, (const void *)S.nf,
+                                S.staged ? (size_t)Tb2Layout<true>::BYTES : (size_t)Tb2Layout<false>::BYTES,
+                                T2_THREADS);
+            }
         } else if (S.tb) {
             S.nf = gdiag ? pick_node_tb<true>(d->coeff_kind) : pick_node_tb<false>(d->coeff_kind);
             finish_tma_plan(S.lp, (const void *)S.nf,
@@ -875,6 +897,16 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
             if (!rc) rc = encode_map(&maps.m[MAP_T2_W8_0], hp.wbuf[0], d, true, MK_WTAIL8);
             if (!rc) rc = encode_map(&maps.m[MAP_T2_W8_1], hp.wbuf[1], d, true, MK_WTAIL8);
             if (!rc) rc = encode_map(&maps.m[MAP_T2_G4], S.staged ? d->coeff : nullptr, d, true, MK_WTAIL);
+            if (S.rows) {
+                if (!rc) rc = encode_map(&maps.m[MAP_T3_W_V], v, d, true, MK_R8W_R);
+                if (!rc) rc = encode_map(&maps.m[MAP_T3_W_0], hp.wbuf[0], d, true, MK_R8W_R);
+                if (!rc) rc = encode_map(&maps.m[MAP_T3_W_1], hp.wbuf[1], d, true, MK_R8W_R);
+                if (!rc) rc = encode_map(&maps.m[MAP_T3_G], S.staged ? d->coeff : nullptr, d, true, MK_R8W_R);
+                if (!rc) rc = encode_map(&maps.m[MAP_T3_P_V], v, d, true, MK_R8P_R);
+                if (!rc) rc = encode_map(&maps.m[MAP_T3_P_0], hp.pbuf[0], d, true, MK_R8P_R);
+                if (!rc) rc = encode_map(&maps.m[MAP_T3_P_1], hp.pbuf[1], d, true, MK_R8P_R);
+                if (!rc) rc = encode_map(&maps.m[MAP_T3_D], S.staged ? d->coeff : nullptr, d, true, MK_R8P_R);
+            }
             if (S.r8) {
                 if (!rc) rc = encode_map(&maps.m[MAP_T2R_W_V], v, d, true, MK_R8W);
                 if (!rc) rc = encode_map(&maps.m[MAP_T2R_W_0], hp.wbuf[0], d, true, MK_R8W);

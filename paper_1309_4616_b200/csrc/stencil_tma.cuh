@@ -59,7 +59,9 @@ enum {
     MAP_T_GP,
     // two-node 2D pass, R8 row view (8, nx/8, ny): w windows (v, wbuf[0], wbuf[1]), D window,
     // p rows (v, pbuf[0], pbuf[1]), D row interior
-    MAP_T2R_W_V, MAP_T2R_W_0, MAP_T2R_W_1, MAP_T2R_G, MAP_T2R_P_V, MAP_T2R_P_0, MAP_T2R_P_1, MAP_T2R_D, MAP_COUNT
+    MAP_T2R_W_V, MAP_T2R_W_0, MAP_T2R_W_1, MAP_T2R_G, MAP_T2R_P_V, MAP_T2R_P_0, MAP_T2R_P_1, MAP_T2R_D,
+    // ... with R-row stages (stencil_tb2r.cuh): the same arrays, boxes of T3_R rows
+    MAP_T3_W_V, MAP_T3_W_0, MAP_T3_W_1, MAP_T3_G, MAP_T3_P_V, MAP_T3_P_0, MAP_T3_P_1, MAP_T3_D, MAP_COUNT
 };
 
 struct alignas(64) TmaMaps {
