@@ -1231,14 +1231,15 @@ def test_small_expeuler_step_bitwise(source, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("graph", [True, False])
-def test_two_node_2d_bitwise(graph, monkeypatch):
+@pytest.mark.parametrize("graph,rows", [(True, "0"), (False, "0"), (True, "1")])
+def test_two_node_2d_bitwise(graph, rows, monkeypatch):
     """Two Leja nodes per pass on single-plane grids (stencil_tb2d.cuh) equal
     the one-node series bit for bit -- p and matvec counts -- for Dirichlet
     and Neumann, no coefficient and the staged sampled D, odd and even node
     counts, tiles cut by the domain (nx not a multiple of 256), row chunks cut
     by ny, fixed degree and tol > 0 (small-grid persistent path off)."""
     monkeypatch.setenv("ES_SMALL", "0")
+    monkeypatch.setenv("ES_TB2R", rows)  # "1": the R-row-stage variant where nx % 8 == 0 (stencil_tb2r.cuh)
     if not graph:
         monkeypatch.setenv("ES_NO_GRAPH", "1")
     cases = [((1000, 77), "neumann", "radial", 1e-10), ((512, 64), "homogeneous", None, 0.0),
