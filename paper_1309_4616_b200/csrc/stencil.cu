@@ -12,6 +12,7 @@
 #include "stencil_tma.cuh"
 #include "stencil_tb2d.cuh"
 #include "stencil_tb2r.cuh"
+#include "stencil_tb2m.cuh"
 #include "stencil_tb.cuh"
 
 #include <cudaTypedefs.h>
@@ -274,6 +275,16 @@ __global__ void __launch_bounds__(T2_THREADS, T2_MINB) k_node_tb2d(const SeriesP
     if (P.state->done) return;
     const int k = P.state->k + 1;
     tb2_pass<STAGED, R8>(Pp, k, tb_two(P, k), tsmem);
+}
+
+// Two Leja nodes per pass on a single-plane grid, row-marching warps (stencil_tb2m.cuh).
+template <bool STAGED, bool NEU>
+__global__ void __launch_bounds__(TM_THREADS, TM_MINB) k_node_tb2m(const SeriesParams *__restrict__ Pp) {
+    extern __shared__ __align__(128) char tsmem[];
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    const int k = P.state->k + 1;
+    tm_pass<STAGED, NEU>(Pp, k, tb_two(P, k), tsmem);
 }
 
 // Two Leja nodes per pass on a single-plane grid, T3_R rows per stage (stencil_tb2r.cuh).
@@ -758,6 +769,7 @@ struct SeriesSetup {
     bool tb2 = false;  // two nodes per pass on a single-plane grid (k_node_tb2d + k_slice_reduce2)
     bool r8 = false;   // ... with the (8, nx/8, ny) row view (one TMA per row window)
     bool rows = false; // ... and stages of T3_R rows (k_node_tb2r)
+    bool march = false; // ... row-marching warps (k_node_tb2m)
     bool staged = false;  // sampled coefficient through the PG ring (ES_COEFF_STAGED)
 };
 
@@ -802,8 +814,13 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
             env_int("ES_TB", 1) && env_int("ES_TB2D", 1);
     int chunk2 = 0;
     if (S.tb2) {
-        chunk2 = pl.chunk * std::max(1, env_int("ES_TB2CHUNK", 4));
-        pl.items = (int64_t)((d->nx + T2_TX - 1) / T2_TX) * ((d->ny + chunk2 - 1) / chunk2);
+        // row-marching warps (stencil_tb2m.cuh; 4096^2: 158 vs 207 us per pass
+        // of the group A / group C kernel), items of 3 norm chunks (24 rows at
+        // 4096^2: 158 us; 16 / 32 / 40 rows: 160 / 162 / 162 us)
+        S.march = env_int("ES_TB2M", 1) != 0;
+        chunk2 = pl.chunk * std::max(1, env_int("ES_TB2CHUNK", S.march ? 3 : 4));
+        const int tx = S.march ? TM_TX : T2_TX;
+        pl.items = (int64_t)((d->nx + tx - 1) / tx) * ((d->ny + chunk2 - 1) / chunk2);
     }
     if (S.tb) {
         pl.chunk = std::max(1, env_int("ES_TBCHUNK", 32));
@@ -820,8 +837,15 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
         if (S.tb2) {
             S.staged = d->coeff_kind == ES_COEFF_ARRAY;
             S.r8 = d->nx % 8 == 0 && env_int("ES_TB2R8", 1);
-            S.rows = S.r8 && env_int("ES_TB2R", 0) && chunk2 % T3_R == 0;  // multi-row stages (measured slower: off)
-            if (S.rows) {
+            S.rows = !S.march && S.r8 && env_int("ES_TB2R", 0) && chunk2 % T3_R == 0;  // multi-row stages (measured slower: off)
+            if (S.march) {
+                S.r8 = false;
+                const bool neu = d->mode == ES_MODE_NEUMANN;
+                S.nf = S.staged ? (neu ? k_node_tb2m<true, true> : k_node_tb2m<true, false>)
+                                : (neu ? k_node_tb2m<false, true> : k_node_tb2m<false, false>);
+                finish_tma_plan(S.lp, (const void *)S.nf,
+                                S.staged ? (size_t)TmLayout<true>::BYTES : (size_t)TmLayout<false>::BYTES, TM_THREADS);
+            } else if (S.rows) {
                 S.nf = S.staged ? k_node_tb2r<true> : k_node_tb2r<false>;
                 finish_tma_plan(S.lp, (const void *)S.nf,
                                 S.staged ? (size_t)Tb3Layout<true, T3_R>::BYTES : (size_t)Tb3Layout<false, T3_R>::BYTES,

@@ -1231,8 +1231,9 @@ def test_small_expeuler_step_bitwise(source, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("graph,rows", [(True, "0"), (False, "0"), (True, "1")])
-def test_two_node_2d_bitwise(graph, rows, monkeypatch):
+@pytest.mark.parametrize("graph,rows,march", [(True, "0", "0"), (False, "0", "0"), (True, "1", "0"),
+                                               (True, "0", "1"), (False, "0", "1")])
+def test_two_node_2d_bitwise(graph, rows, march, monkeypatch):
     """Two Leja nodes per pass on single-plane grids (stencil_tb2d.cuh) equal
     the one-node series bit for bit -- p and matvec counts -- for Dirichlet
     and Neumann, no coefficient and the staged sampled D, odd and even node
@@ -1240,6 +1241,7 @@ def test_two_node_2d_bitwise(graph, rows, monkeypatch):
     by ny, fixed degree and tol > 0 (small-grid persistent path off)."""
     monkeypatch.setenv("ES_SMALL", "0")
     monkeypatch.setenv("ES_TB2R", rows)  # "1": the R-row-stage variant where nx % 8 == 0 (stencil_tb2r.cuh)
+    monkeypatch.setenv("ES_TB2M", march)  # "1": the row-marching variant (stencil_tb2m.cuh)
     if not graph:
         monkeypatch.setenv("ES_NO_GRAPH", "1")
     cases = [((1000, 77), "neumann", "radial", 1e-10), ((512, 64), "homogeneous", None, 0.0),
