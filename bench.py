@@ -622,9 +622,12 @@ def run_b200(args, cfg):
         passes = max(tm.passes(), 1)
         two_p, one_p = tm.pass_mix()
         launch_s = series_s / passes
-        # a two-node pass reads w, p (+g') and writes w'', p', p''; the one-node
-        # tail pass of a series reads w, p (+g') and writes w', p'
-        bytes_all = (two_p * (cfg["bytes_per_node"] + 8) + one_p * cfg["bytes_per_node"]) * n_local
+        # a two-node pass reads w, p (+g') and writes w'', p'' -- and p' only
+        # where the series could stop at its first node (tol > 0 with the
+        # one-node tail pass disabled, ES_TB_TAIL=0; csrc/series.cuh
+        # tb_store_pk); the one-node tail pass reads w, p (+g') and writes w', p'
+        pk_stored = cfg["tol"] > 0 and os.environ.get("ES_TB_TAIL", "1") == "0"
+        bytes_all = (two_p * (cfg["bytes_per_node"] + (8 if pk_stored else 0)) + one_p * cfg["bytes_per_node"]) * n_local
         bytes_launch = bytes_all / passes
         achieved = bytes_launch / launch_s / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

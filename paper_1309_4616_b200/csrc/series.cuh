@@ -223,6 +223,13 @@ ES_DEV bool tb_two(const SeriesParams &P, int k) {
     return !(P.tail1 && P.tol > 0.0 && P.state->consecutive == 1);
 }
 
+// Must a two-node pass (k, k + 1) store p_k?  Only if the series can stop at
+// node k.  It cannot when tb_two holds and either tol == 0 (stops only at
+// ndd - 1 >= k + 1) or tail1 (the pass started with consecutive == 0, so node
+// k leaves it at most 1): p_k is then an intermediate nobody reads -- its
+// norm is taken in registers and the next pass starts from p_{k+1}.
+ES_DEV bool tb_store_pk(const SeriesParams &P, bool two) { return !two || (P.tol > 0.0 && !P.tail1); }
+
 // Publish a series' parameters and clear its state and tickets (k_series_init,
 // and the merged init of the small-grid exponential-Euler step); the block's
 // threads share the ticket reset.

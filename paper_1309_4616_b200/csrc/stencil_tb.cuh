@@ -468,6 +468,7 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
     const int pass = P->state->pass;
     double *w1_dst = P->wbuf[pass & 1];  // w_{k+1}, or w_k on a one-node pass
     double *pk_dst = P->pbuf[k & 1], *pk1_dst = P->pbuf[(k + 1) & 1];
+    const bool store_pk = tb_store_pk(*P, two);
     const double alpha = P->alpha, dk = P->dd[k];
     const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
     const double pscale = k == 1 ? P->dd[0] : 1.0;  // first pass: P tiles hold v, p_0 = dd_0 v
@@ -536,7 +537,8 @@ ES_DEV void tb_group_c(const Geom &g, const SeriesParams *P, int k, bool two, co
                     pk_cur[2 * h + 1] = add(p1, mul(dk, vk.y));
                     if (act[h]) {
                         const int64_t off = off0 + h * drow;
-                        *reinterpret_cast<double2 *>(pk_dst + off) = make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
+                        if (store_pk)
+                            *reinterpret_cast<double2 *>(pk_dst + off) = make_double2(pk_cur[2 * h], pk_cur[2 * h + 1]);
                         if (!two) *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
                         acc_w0[h] = add(acc_w0[h], add(mul(vk.x, vk.x), mul(vk.y, vk.y)));
                         acc_p0[h] = add(acc_p0[h], add(mul(pk_cur[2 * h], pk_cur[2 * h]),

@@ -427,6 +427,7 @@ ES_DEV void tb2_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
     const int pass = P->state->pass;
     double *w1_dst = P->wbuf[pass & 1];  // w_{k+1}, or w_k on a one-node pass
     double *pk_dst = P->pbuf[k & 1], *pk1_dst = P->pbuf[(k + 1) & 1];
+    const bool store_pk = tb_store_pk(*P, two);
     const double alpha = P->alpha, dk = P->dd[k];
     const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
     const double pscale = k == 1 ? P->dd[0] : 1.0;  // first pass: P rows hold v, p_0 = dd_0 v
@@ -503,7 +504,7 @@ ES_DEV void tb2_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
 #pragma unroll
                 for (int h = 0; h < T2_CPT; ++h) {
                     if (!act[h]) continue;
-                    *reinterpret_cast<double2 *>(pk_dst + off0 + 256 * h) = pk_cur[h];
+                    if (store_pk) *reinterpret_cast<double2 *>(pk_dst + off0 + 256 * h) = pk_cur[h];
                     if (!two) *reinterpret_cast<double2 *>(w1_dst + off0 + 256 * h) = vcur[h];  // next pass starts from w_k
                     acc_w0[h] = add(acc_w0[h], add(mul(vcur[h].x, vcur[h].x), mul(vcur[h].y, vcur[h].y)));
                     acc_p0[h] = add(acc_p0[h], add(mul(pk_cur[h].x, pk_cur[h].x), mul(pk_cur[h].y, pk_cur[h].y)));

@@ -210,6 +210,7 @@ ES_DEV void tm_compute(const Geom &g, const SeriesParams *P, int k, bool two, co
     const int pass = P->state->pass;
     double *const w1_dst = P->wbuf[pass & 1];  // w_{k+1}, or w_k on a one-node pass
     double *const pk_dst = P->pbuf[k & 1], *const pk1_dst = P->pbuf[(k + 1) & 1];
+    const bool store_pk = tb_store_pk(*P, two);
     double *const part = P->part;
     const double alpha = P->alpha, beta_k = sub(-P->shift, P->xi[k - 1]), dk = P->dd[k];
     const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
@@ -326,7 +327,7 @@ ES_DEV void tm_compute(const Geom &g, const SeriesParams *P, int k, bool two, co
                     pk[h] = make_double2(add(mul(pscale, po.x), mul(dk, wk[h].x)),
                                          add(mul(pscale, po.y), mul(dk, wk[h].y)));
                     if (in0[h]) {
-                        *reinterpret_cast<double2 *>(pk_row + 64 * h) = pk[h];
+                        if (store_pk) *reinterpret_cast<double2 *>(pk_row + 64 * h) = pk[h];
                         if (!two) *reinterpret_cast<double2 *>(wk_row + 64 * h) = wk[h];  // next pass starts from w_k
                         acc_w0[h] = add(acc_w0[h], add(mul(wk[h].x, wk[h].x), mul(wk[h].y, wk[h].y)));
                         acc_p0[h] = add(acc_p0[h], add(mul(pk[h].x, pk[h].x), mul(pk[h].y, pk[h].y)));

@@ -274,6 +274,7 @@ ES_DEV void tb3_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
     const int pass = P->state->pass;
     double *w1_dst = P->wbuf[pass & 1];  // w_{k+1}, or w_k on a one-node pass
     double *pk_dst = P->pbuf[k & 1], *pk1_dst = P->pbuf[(k + 1) & 1];
+    const bool store_pk = tb_store_pk(*P, two);
     const double alpha = P->alpha, dk = P->dd[k];
     const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
     const double pscale = k == 1 ? P->dd[0] : 1.0;  // first pass: P rows hold v, p_0 = dd_0 v
@@ -335,7 +336,7 @@ ES_DEV void tb3_group_c(const Geom &g, const SeriesParams *P, int k, bool two, c
                 pk[r] = make_double2(add(mul(pscale, po.x), mul(dk, vk.x)), add(mul(pscale, po.y), mul(dk, vk.y)));
                 if (act) {
                     const int64_t off = (int64_t)j * nx + xa;
-                    *reinterpret_cast<double2 *>(pk_dst + off) = pk[r];
+                    if (store_pk) *reinterpret_cast<double2 *>(pk_dst + off) = pk[r];
                     if (!two) *reinterpret_cast<double2 *>(w1_dst + off) = vk;  // the next pass starts from w_k
                     acc_w0 = add(acc_w0, add(mul(vk.x, vk.x), mul(vk.y, vk.y)));
                     acc_p0 = add(acc_p0, add(mul(pk[r].x, pk[r].x), mul(pk[r].y, pk[r].y)));
