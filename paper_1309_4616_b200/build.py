@@ -23,7 +23,7 @@ OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libexpstencil_b200.so")
 SOURCES = ["capi.cu", "stencil.cu", "csr.cu", "pointwise.cu", "graph.cu", "f32.cu", "step.cu", "csr_generic.cu", "series_small.cu"]
 HEADERS = ["es_common.cuh", "es_host.h", "stencil.cuh", "series.cuh", "stencil_tma.cuh", "stencil_tb.cuh",
-           "stencil_tb2d.cuh", "stencil_tb2m.cuh"]
+           "stencil_tb2d.cuh", "stencil_tb2m.cuh", "stencil_tb3m.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",

@@ -13,6 +13,7 @@
 #include "stencil_tb2d.cuh"
 #include "stencil_tb2r.cuh"
 #include "stencil_tb2m.cuh"
+#include "stencil_tb3m.cuh"
 #include "stencil_tb.cuh"
 
 #include <cudaTypedefs.h>
@@ -285,6 +286,16 @@ __global__ void __launch_bounds__(TM_THREADS, TM_MINB) k_node_tb2m(const SeriesP
     if (P.state->done) return;
     const int k = P.state->k + 1;
     tm_pass<STAGED, NEU>(Pp, k, tb_two(P, k), tsmem);
+}
+
+// Two Leja nodes per pass on one 3D domain, plane-marching warps (stencil_tb3m.cuh).
+template <bool GD, bool NEU>
+__global__ void __launch_bounds__(T3M_THREADS, 1) k_node_tb3m(const SeriesParams *__restrict__ Pp) {
+    extern __shared__ __align__(128) char tsmem[];
+    const SeriesParams &P = *Pp;
+    if (P.state->done) return;
+    const int k = P.state->k + 1;
+    t3m_pass<GD, NEU>(Pp, k, tb_two(P, k), tsmem);
 }
 
 // Two Leja nodes per pass on a single-plane grid, T3_R rows per stage (stencil_tb2r.cuh).
@@ -857,6 +868,14 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
                                 S.staged ? (size_t)Tb2Layout<true>::BYTES : (size_t)Tb2Layout<false>::BYTES,
                                 T2_THREADS);
             }
+        } else if (S.tb && !halos && d->coeff_kind == ES_COEFF_NONE && env_int("ES_TB3M", 1)) {
+            // plane-marching warps (stencil_tb3m.cuh; 512^3 Rosenbrock pass
+            // ~1.01 -> ~0.96-0.99 ms, 626 -> 447 M warp instructions)
+            const bool neu = d->mode == ES_MODE_NEUMANN;
+            S.nf = gdiag ? (neu ? k_node_tb3m<true, true> : k_node_tb3m<true, false>)
+                         : (neu ? k_node_tb3m<false, true> : k_node_tb3m<false, false>);
+            finish_tma_plan(S.lp, (const void *)S.nf,
+                            gdiag ? (size_t)T3mLayout<true>::BYTES : (size_t)T3mLayout<false>::BYTES, T3M_THREADS);
         } else if (S.tb) {
             S.nf = gdiag ? pick_node_tb<true>(d->coeff_kind) : pick_node_tb<false>(d->coeff_kind);
             finish_tma_plan(S.lp, (const void *)S.nf,

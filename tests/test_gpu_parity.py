@@ -1060,11 +1060,13 @@ def test_f32_combustion_and_f32_csr(golden):
 # ---- two Leja nodes per pass (stencil_tb.cuh, opt-in ES_TB=1) ---------------
 
 
-@pytest.mark.parametrize("graph", [True, False])
-def test_two_node_pass_bitwise(graph, monkeypatch):
+@pytest.mark.parametrize("graph,march", [(True, "0"), (False, "0"), (True, "1"), (False, "1")])
+def test_two_node_pass_bitwise(graph, march, monkeypatch):
     """Temporal blocking: same p, same matvec counts as one node per pass,
     for Dirichlet / Neumann, coefficient kinds, a g' diagonal, odd and even
-    node counts, ragged tiles and chunks."""
+    node counts, ragged tiles and chunks; march "1": the plane-marching
+    kernel (stencil_tb3m.cuh) where it applies (coefficient none)."""
+    monkeypatch.setenv("ES_TB3M", march)
     if not graph:
         monkeypatch.setenv("ES_NO_GRAPH", "1")
     cases = [((64, 40, 48), "homogeneous", None, False, 1e-8), ((70, 18, 21), "neumann", None, True, 1e-10),
@@ -1088,10 +1090,12 @@ def test_two_node_pass_bitwise(graph, monkeypatch):
 @pytest.mark.parametrize("dims,bc,nodes", [((6, 4, 2), "homogeneous", 7), ((10, 9, 3), "neumann", 8),
                                            ((130, 17, 33), "homogeneous", 9), ((64, 8, 64), "neumann", 2),
                                            ((66, 10, 35), "homogeneous", 3), ((2, 2, 5), "neumann", 6)])
-def test_two_node_pass_edges_vs_oracle(dims, bc, nodes, monkeypatch):
+@pytest.mark.parametrize("march", ["0", "1"])
+def test_two_node_pass_edges_vs_oracle(dims, bc, nodes, march, monkeypatch):
     """Two-node passes on tiny / ragged grids (tiles cut by the domain in x, y
     and z, one- and two-plane slabs, odd and even node counts, g' diagonal)
-    against the oracle, bitwise, at fixed degree."""
+    against the oracle, bitwise, at fixed degree (both 3D two-node kernels)."""
+    monkeypatch.setenv("ES_TB3M", march)
     g = es.Grid3D(*dims)
     op = es.StencilOperator(g, BCS[bc])
     lo, hi = es.gershgorin_bounds(op)
@@ -1107,8 +1111,8 @@ def test_two_node_pass_edges_vs_oracle(dims, bc, nodes, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("graph", [True, False])
-def test_two_node_tail_pass_bitwise(graph, monkeypatch):
+@pytest.mark.parametrize("graph,march", [(True, "0"), (False, "0"), (True, "1")])
+def test_two_node_tail_pass_bitwise(graph, march, monkeypatch):
     """A two-node series runs node k alone when node k-1 met the term test
     for the first time (the series then usually stops at k).  Over a sweep
     of tolerances -- stops at odd and even k, and first hits that do not
@@ -1117,6 +1121,7 @@ def test_two_node_tail_pass_bitwise(graph, monkeypatch):
     pass count never exceeds the plain pairing's."""
     from paper_1309_4616_b200 import timing
 
+    monkeypatch.setenv("ES_TB3M", march)
     if not graph:
         monkeypatch.setenv("ES_NO_GRAPH", "1")
     g = es.Grid3D(72, 40, 44)
