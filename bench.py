@@ -633,7 +633,8 @@ def run_b200(args, cfg):
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": profiled_traffic(args.config + "_tb"),
                     "kernel": ("k_node_tb2m (two fused Leja nodes per HBM pass, row-marching 2D)" if cfg["dims"][2] == 1
-                               else "k_node_tb (two fused Leja nodes per HBM pass)"), "bytes_per_launch": bytes_launch,
+                               else "k_node_tb3m (two fused Leja nodes per HBM pass, plane-marching 3D)"),
+                    "bytes_per_launch": bytes_launch,
                     "bytes_per_point": bytes_launch / n_local, "launch_us": launch_s * 1e6, "launches": passes,
                     "two_node_passes": two_p, "one_node_passes": one_p,
                     "node_us": node_s * 1e6,

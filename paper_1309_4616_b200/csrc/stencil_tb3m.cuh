@@ -38,6 +38,9 @@ namespace es {
 #ifndef T3M_S
 #define T3M_S 6  // stages (planes) in flight
 #endif
+#ifndef T3M_PKR
+#define T3M_PKR 0  // 1: re-derive p_k(j-1) from its (still held) P stage instead of carrying it
+#endif
 #ifndef T3M_NW
 #define T3M_NW 8  // compute warps: rows w + T3M_NW h of the 16-row tile
 #endif
@@ -342,6 +345,18 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
             if (two && jc >= it.mb && jc < it.me) {
                 const double *Vc = vrow + ((u - 1) & 1) * Lt::V_SLOT;  // w_k(j-1) with its ring
                 const double *Gp = reinterpret_cast<const double *>(smem + ((s - 1) % T3M_S) * Lt::STAGE + Lt::G_OFF);
+                double2 pkp[R];  // p_k(j-1)
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                    if constexpr (T3M_PKR) {  // the same expression on the same operands: bitwise the carried value
+                        const double2 po = *reinterpret_cast<const double2 *>(
+                            smem + ((s - 1) % T3M_S) * Lt::STAGE + Lt::P_OFF + 8 * op[h]);
+                        pkp[h] = make_double2(add(mul(pscale, po.x), mul(dk, uc[h].x)),
+                                              add(mul(pscale, po.y), mul(dk, uc[h].y)));
+                    } else {
+                        pkp[h] = pk_prev[h];
+                    }
+                }
 #pragma unroll
                 for (int h = 0; h < R; ++h) {
                     const double2 cc = uc[h];
@@ -375,7 +390,7 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
                     const double2 wn = make_double2(add(mul(alpha, l0), mul(beta_k1, cc.x)),
                                                     add(mul(alpha, l1), mul(beta_k1, cc.y)));
                     const double2 pn =
-                        make_double2(add(pk_prev[h].x, mul(dk1, wn.x)), add(pk_prev[h].y, mul(dk1, wn.y)));
+                        make_double2(add(pkp[h].x, mul(dk1, wn.x)), add(pkp[h].y, mul(dk1, wn.y)));
                     if (in0[h]) {
                         *reinterpret_cast<double2 *>(wn_row + h * drow) = wn;
                         *reinterpret_cast<double2 *>(pn_row + h * drow) = pn;
