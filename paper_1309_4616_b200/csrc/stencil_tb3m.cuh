@@ -41,6 +41,13 @@ namespace es {
 #ifndef T3M_PKR
 #define T3M_PKR 0  // 1: re-derive p_k(j-1) from its (still held) P stage instead of carrying it
 #endif
+#ifndef T3M_LAG
+// planes between a step's w_k (A part) and its w_{k+1} (C part): 1 or 2.  2
+// makes the two fp64 chains of a step independent but holds four stages
+// (two planes of prefetch at 6 stages): measured 1.12 vs 1.00 ms per 512^3 pass
+#define T3M_LAG 1
+#endif
+constexpr int T3M_NV = T3M_LAG + 1;  // shared w_k plane slots
 #ifndef T3M_NW
 #define T3M_NW 8  // compute warps: rows w + T3M_NW h of the 16-row tile
 #endif
@@ -57,8 +64,8 @@ struct T3mLayout {
     static constexpr int G_OFF = W_BYTES, P_OFF = W_BYTES + G_BYTES;
     static constexpr int V_SLOT = TB_EX * TB_EY;  // w_k of a plane with its ring, 68 x 18 from x0-2, y0-1
     static constexpr int V_OFF = T3M_S * STAGE;
-    static constexpr int BAR_OFF = V_OFF + 2 * V_SLOT * 8;
-    static constexpr int NBAR = 2 * T3M_S + 2;
+    static constexpr int BAR_OFF = V_OFF + T3M_NV * V_SLOT * 8;
+    static constexpr int NBAR = 2 * T3M_S + T3M_NV;
     static constexpr int ITEMQ_OFF = BAR_OFF + NBAR * 8;
     static constexpr int BYTES = ITEMQ_OFF + ((T3M_S * 4 + 15) & ~15);
 };
@@ -103,6 +110,11 @@ ES_DEV void t3m_produce(const Geom &g, const TbItems &its, const TbMaps &mp, cha
     if (q >= (uint32_t)T3M_S) mbar_wait(&B.empty[s], ((q / T3M_S) - 1) & 1);
     itemq[s] = -1;
     mbar_arrive(&B.full[s]);
+}
+
+// one step's V slot (u % T3M_NV): wait until every warp has finished step u - 1
+ES_DEV void t3m_v_ready(uint64_t *vfull, uint32_t u) {
+    if (u > 0) mbar_wait(&vfull[(u - 1) % T3M_NV], ((u - 1) / T3M_NV) & 1);
 }
 
 // w_k at one ring point (x, y) of plane j: tb_point_scalar's expression with
@@ -174,30 +186,36 @@ ES_DEV void t3m_edge(const Geom &g, const SeriesParams *P, int k, const TbItems 
             warp_arrive(&B.empty[s % T3M_S]);
             ++s;  // s: stage of plane j
         }
-        for (int j = it.mb - 1; j <= it.me; ++j, ++s, ++u) {
-            mbar_wait(&B.full[(s + 1) % T3M_S], ((s + 1) / T3M_S) & 1);
-            const char *st = stage(s);
-            const double *Wn = reinterpret_cast<const double *>(stage(s + 1));
-            double ep[3], wv[3] = {0.0, 0.0, 0.0};
+        for (int j = it.mb - 1; j <= it.me + T3M_LAG - 1; ++j, ++u) {
+            double wv[3] = {0.0, 0.0, 0.0};
+            if (j <= it.me) {  // (LAG 2: the compute warps' extra C-only step has no plane)
+                mbar_wait(&B.full[(s + 1) % T3M_S], ((s + 1) / T3M_S) & 1);
+                const char *st = stage(s);
+                const double *Wn = reinterpret_cast<const double *>(stage(s + 1));
+                double ep[3];
 #pragma unroll
-            for (int h = 0; h < 3; ++h) ep[h] = Wn[wo[h]];
-            if (j >= 0 && j < its.L) {
+                for (int h = 0; h < 3; ++h) ep[h] = Wn[wo[h]];
+                if (j >= 0 && j < its.L) {
 #pragma unroll
-                for (int h = 0; h < 3; ++h)
-                    if (h < 2 || col)
-                        wv[h] = t3m_ring_point<GD, NEU>(g, st, it.x0, it.y0, px[h], py[h], em[h], ep[h], alpha, beta_k);
+                    for (int h = 0; h < 3; ++h)
+                        if (h < 2 || col)
+                            wv[h] = t3m_ring_point<GD, NEU>(g, st, it.x0, it.y0, px[h], py[h], em[h], ep[h], alpha, beta_k);
+                }
+#pragma unroll
+                for (int h = 0; h < 3; ++h) {
+                    em[h] = ec[h];
+                    ec[h] = ep[h];
+                }
             }
-            tm_v_ready(B.vfull, u);
-            double *V = vrow + (u & 1) * Lt::V_SLOT;
+            t3m_v_ready(B.vfull, u);
+            double *V = vrow + (u % T3M_NV) * Lt::V_SLOT;
             V[vo[0]] = wv[0];
             V[vo[1]] = wv[1];
             if (col) V[vo[2]] = wv[2];
-            warp_arrive(&B.vfull[u & 1]);
-            warp_arrive(&B.empty[s % T3M_S]);
-#pragma unroll
-            for (int h = 0; h < 3; ++h) {
-                em[h] = ec[h];
-                ec[h] = ep[h];
+            warp_arrive(&B.vfull[u % T3M_NV]);
+            if (j <= it.me) {
+                warp_arrive(&B.empty[s % T3M_S]);
+                ++s;
             }
         }
         warp_arrive(&B.empty[s % T3M_S]);  // plane me + 1
@@ -340,10 +358,10 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
                 }
             }
             // ---- w_{k+1}(j-1), p_{k+1}(j-1) (+ node k+1 norms)
-            tm_v_ready(B.vfull, u);
+            t3m_v_ready(B.vfull, u);
             const int jc = j - 1;
             if (two && jc >= it.mb && jc < it.me) {
-                const double *Vc = vrow + ((u - 1) & 1) * Lt::V_SLOT;  // w_k(j-1) with its ring
+                const double *Vc = vrow + ((u - 1) % T3M_NV) * Lt::V_SLOT;  // w_k(j-1) with its ring
                 const double *Gp = reinterpret_cast<const double *>(smem + ((s - 1) % T3M_S) * Lt::STAGE + Lt::G_OFF);
                 double2 pkp[R];  // p_k(j-1)
 #pragma unroll
@@ -400,10 +418,10 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
                 }
             }
             // ---- publish w_k(j): the x/y neighbours of the next step's C part
-            double *Vn = vrow + (u & 1) * Lt::V_SLOT;
+            double *Vn = vrow + (u % T3M_NV) * Lt::V_SLOT;
 #pragma unroll
             for (int h = 0; h < R; ++h) *reinterpret_cast<double2 *>(Vn + ov[h]) = wk[h];
-            warp_arrive(&B.vfull[u & 1]);
+            warp_arrive(&B.vfull[u % T3M_NV]);
             warp_arrive(&B.empty[(s - 1) % T3M_S]);  // plane j - 1: its g' was last read above
             ++j;
             ++s;
@@ -442,6 +460,240 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
     }
 }
 
+// T3M_LAG == 2: the C part of step j works on plane j - 2, so it depends on
+// nothing the step's A part computes -- the two fp64 chains of a step are
+// independent and interleave.  w_k of planes j-3 .. j (four register roles),
+// p_k(j-2) re-derived from its P stage, g'(j-2) and P(j-2) held until step j,
+// three V slots.
+template <bool GD, bool NEU>
+ES_DEV void t3m_compute2(const Geom &g, const SeriesParams *P, int k, bool two, const TbItems &its, char *smem) {
+    using Lt = T3mLayout<GD>;
+    constexpr int R = T3M_RPW;
+    const T3mBars<GD> B(smem);
+    const volatile int *itemq = reinterpret_cast<const volatile int *>(smem + Lt::ITEMQ_OFF);
+    double *vrow = reinterpret_cast<double *>(smem + Lt::V_OFF);
+    const int w = threadIdx.x >> 5, q = threadIdx.x & 31;  // rows w + T3M_NW h; pair x0 + 2q
+    const int64_t nx = g.nx, plane = g.nx * g.ny;
+    const double wx = g.wx, wy = g.wy, wz = g.wz;
+    const int pass = P->state->pass;
+    double *const w1_dst = P->wbuf[pass & 1];
+    double *const pk_dst = P->pbuf[k & 1], *const pk1_dst = P->pbuf[(k + 1) & 1];
+    double *const part = P->part;
+    const bool store_pk = tb_store_pk(*P, two);
+    const double alpha = P->alpha, beta_k = sub(-P->shift, P->xi[k - 1]), dk = P->dd[k];
+    const double dk1 = two ? P->dd[k + 1] : 0.0, beta_k1 = two ? sub(-P->shift, P->xi[k]) : 0.0;
+    const double pscale = k == 1 ? P->dd[0] : 1.0;
+    const int64_t half = (int64_t)P->nslices * P->ntiles * 2;
+    int ow[R], og[R], op[R], ov[R];
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        const int r = w + T3M_NW * h;
+        ow[h] = (r + 2) * TB_WX + 2 * q + 4;
+        og[h] = (r + 1) * TB_GX + 2 * q + 2;
+        op[h] = r * 64 + 2 * q;
+        ov[h] = (r + 1) * TB_EX + 2 * q + 2;
+    }
+    uint32_t s = 0, u = 0;
+    double2 W0[R], W1[R], W2[R], W3[R], U0[R], U1[R], U2[R], U3[R];
+    for (;;) {
+        mbar_wait(&B.full[s % T3M_S], (s / T3M_S) & 1);
+        const int i = itemq[s % T3M_S];
+        if (i < 0) break;
+        const TbItem it = tb_item_at(its, i);
+        const int64_t xa = it.x0 + 2 * q;
+        int64_t ya[R];
+        bool in0[R], in1[R];
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+            ya[h] = it.y0 + w + T3M_NW * h;
+            in0[h] = xa < nx && ya[h] < g.ny;
+            in1[h] = xa + 1 < nx && ya[h] < g.ny;
+        }
+        const int ylast = it.y0 + w + T3M_NW * (R - 1);
+        const bool xedge = it.x0 == 0 || it.x0 + 64 >= nx;
+        const bool yedge = it.y0 + w == 0 || ylast >= g.ny - 1;
+        const bool special = NEU ? (xedge || yedge) : (it.x0 + 64 > nx || ylast >= g.ny);
+        double acc_w0[R], acc_p0[R], acc_w1[R], acc_p1[R];
+#pragma unroll
+        for (int h = 0; h < R; ++h) acc_w0[h] = acc_p0[h] = acc_w1[h] = acc_p1[h] = 0.0;
+        {
+            const double *S0 = reinterpret_cast<const double *>(smem + (s % T3M_S) * Lt::STAGE);
+            mbar_wait(&B.full[(s + 1) % T3M_S], ((s + 1) / T3M_S) & 1);
+            const double *S1 = reinterpret_cast<const double *>(smem + ((s + 1) % T3M_S) * Lt::STAGE);
+#pragma unroll
+            for (int h = 0; h < R; ++h) {
+                W0[h] = *reinterpret_cast<const double2 *>(S0 + ow[h]);
+                W1[h] = *reinterpret_cast<const double2 *>(S1 + ow[h]);
+                U0[h] = U1[h] = U2[h] = make_double2(0.0, 0.0);
+            }
+            ++s;  // s: stage of plane j
+        }
+        const int64_t off0 = (int64_t)(it.mb - 1) * plane + it.y0 * nx + xa + (int64_t)w * nx;  // row 0, plane j
+        const int64_t drow = (int64_t)T3M_NW * nx;
+        double *pk_row = pk_dst + off0, *wk_row = w1_dst + off0;
+        double *wn_row = w1_dst + off0 - 2 * plane, *pn_row = pk1_dst + off0 - 2 * plane;
+        int j = it.mb - 1;
+        // roles: vm, vc, vp = w_{k-1}(j-1, j, j+1); um, uc, up, wk = w_k(j-3, j-2, j-1, j)
+        auto step = [&](double2 (&vm)[R], double2 (&vc)[R], double2 (&vp)[R], double2 (&um)[R], double2 (&uc)[R],
+                        double2 (&up)[R], double2 (&wk)[R]) -> bool {
+            const bool a_part = j <= it.me;  // the last step (plane me + 1) is C only
+            if (a_part) mbar_wait(&B.full[(s + 1) % T3M_S], ((s + 1) / T3M_S) & 1);
+            t3m_v_ready(B.vfull, u);  // every warp finished step u - 1 (V(u-2) complete, slot u % 3 free)
+            // ---- C part: w_{k+1}(j-2), p_{k+1}(j-2) -- independent of this step's A part
+            const int jc = j - 2;
+            if (two && jc >= it.mb && jc < it.me) {
+                const double *Vc = vrow + ((u - 2) % T3M_NV) * Lt::V_SLOT;  // w_k(j-2) with its ring
+                const char *sc = smem + ((s - 2) % T3M_S) * Lt::STAGE;      // g', P of plane j-2
+                const double *Gp = reinterpret_cast<const double *>(sc + Lt::G_OFF);
+                const double *Pp = reinterpret_cast<const double *>(sc + Lt::P_OFF);
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                    const double2 cc = uc[h];
+                    const double2 ym = *reinterpret_cast<const double2 *>(Vc + ov[h] - TB_EX);
+                    const double2 yp = *reinterpret_cast<const double2 *>(Vc + ov[h] + TB_EX);
+                    double xm = Vc[ov[h] - 1], xp = Vc[ov[h] + 2];
+                    double ym0 = ym.x, ym1 = ym.y, yp0 = yp.x, yp1 = yp.y;
+                    double2 zm = um[h], zp = up[h];
+                    if (NEU) {
+                        if (special) {
+                            if (xa == 0) xm = cc.x;
+                            if (xa + 1 == nx - 1) xp = cc.y;
+                            if (ya[h] == 0) {
+                                ym0 = cc.x;
+                                ym1 = cc.y;
+                            }
+                            if (ya[h] == g.ny - 1) {
+                                yp0 = cc.x;
+                                yp1 = cc.y;
+                            }
+                        }
+                        if (jc == 0) zm = cc;              // plane -1 mirrors plane 0
+                        if (jc == its.L - 1) zp = cc;      // plane L mirrors plane L - 1
+                    }
+                    double l0 = lap7(cc.x, xm, cc.y, ym0, yp0, zm.x, zp.x, wx, wy, wz);
+                    double l1 = lap7(cc.y, cc.x, xp, ym1, yp1, zm.y, zp.y, wx, wy, wz);
+                    if constexpr (GD) {
+                        const double2 gv = *reinterpret_cast<const double2 *>(Gp + og[h]);
+                        l0 = sub(l0, mul(gv.x, cc.x));
+                        l1 = sub(l1, mul(gv.y, cc.y));
+                    }
+                    const double2 po = *reinterpret_cast<const double2 *>(Pp + op[h]);
+                    // p_k(j-2): the A part's expression on the same operands (bitwise)
+                    const double2 pkc = make_double2(add(mul(pscale, po.x), mul(dk, cc.x)),
+                                                     add(mul(pscale, po.y), mul(dk, cc.y)));
+                    const double2 wn = make_double2(add(mul(alpha, l0), mul(beta_k1, cc.x)),
+                                                    add(mul(alpha, l1), mul(beta_k1, cc.y)));
+                    const double2 pn = make_double2(add(pkc.x, mul(dk1, wn.x)), add(pkc.y, mul(dk1, wn.y)));
+                    if (in0[h]) {
+                        *reinterpret_cast<double2 *>(wn_row + h * drow) = wn;
+                        *reinterpret_cast<double2 *>(pn_row + h * drow) = pn;
+                        acc_w1[h] = add(acc_w1[h], add(mul(wn.x, wn.x), mul(wn.y, wn.y)));
+                        acc_p1[h] = add(acc_p1[h], add(mul(pn.x, pn.x), mul(pn.y, pn.y)));
+                    }
+                }
+            }
+            // ---- A part: w_k(j), p_k(j)
+            if (a_part) {
+                const char *st = smem + (s % T3M_S) * Lt::STAGE;
+                const double *Wn = reinterpret_cast<const double *>(smem + ((s + 1) % T3M_S) * Lt::STAGE);
+#pragma unroll
+                for (int h = 0; h < R; ++h) vp[h] = *reinterpret_cast<const double2 *>(Wn + ow[h]);
+                if (j >= 0 && j < its.L) {
+                    const double *Wc = reinterpret_cast<const double *>(st);
+                    const double *Gc = reinterpret_cast<const double *>(st + Lt::G_OFF);
+#pragma unroll
+                    for (int h = 0; h < R; ++h) {
+                        const double2 ym = *reinterpret_cast<const double2 *>(Wc + ow[h] - TB_WX);
+                        const double2 yp = *reinterpret_cast<const double2 *>(Wc + ow[h] + TB_WX);
+                        double xm = Wc[ow[h] - 1], xp = Wc[ow[h] + 2];
+                        double ym0 = ym.x, ym1 = ym.y, yp0 = yp.x, yp1 = yp.y;
+                        if (NEU && special) {
+                            if (xa == 0) xm = vc[h].x;
+                            if (xa + 1 == nx - 1) xp = vc[h].y;
+                            if (ya[h] == 0) {
+                                ym0 = vc[h].x;
+                                ym1 = vc[h].y;
+                            }
+                            if (ya[h] == g.ny - 1) {
+                                yp0 = vc[h].x;
+                                yp1 = vc[h].y;
+                            }
+                        }
+                        double l0 = lap7(vc[h].x, xm, vc[h].y, ym0, yp0, vm[h].x, vp[h].x, wx, wy, wz);
+                        double l1 = lap7(vc[h].y, vc[h].x, xp, ym1, yp1, vm[h].y, vp[h].y, wx, wy, wz);
+                        if constexpr (GD) {
+                            const double2 gv = *reinterpret_cast<const double2 *>(Gc + og[h]);
+                            l0 = sub(l0, mul(gv.x, vc[h].x));
+                            l1 = sub(l1, mul(gv.y, vc[h].y));
+                        }
+                        wk[h] = make_double2(add(mul(alpha, l0), mul(beta_k, vc[h].x)),
+                                             add(mul(alpha, l1), mul(beta_k, vc[h].y)));
+                        if (!NEU && special) wk[h] = make_double2(in0[h] ? wk[h].x : 0.0, in1[h] ? wk[h].y : 0.0);
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < R; ++h) wk[h] = make_double2(0.0, 0.0);
+                }
+                if (j >= it.mb && j < it.me) {
+                    const double *Pc = reinterpret_cast<const double *>(st + Lt::P_OFF);
+#pragma unroll
+                    for (int h = 0; h < R; ++h) {
+                        const double2 po = *reinterpret_cast<const double2 *>(Pc + op[h]);
+                        const double2 pk = make_double2(add(mul(pscale, po.x), mul(dk, wk[h].x)),
+                                                        add(mul(pscale, po.y), mul(dk, wk[h].y)));
+                        if (in0[h]) {
+                            if (store_pk) *reinterpret_cast<double2 *>(pk_row + h * drow) = pk;
+                            if (!two) *reinterpret_cast<double2 *>(wk_row + h * drow) = wk[h];
+                            acc_w0[h] = add(acc_w0[h], add(mul(wk[h].x, wk[h].x), mul(wk[h].y, wk[h].y)));
+                            acc_p0[h] = add(acc_p0[h], add(mul(pk.x, pk.x), mul(pk.y, pk.y)));
+                        }
+                    }
+                }
+            }
+            // ---- publish w_k(j) (x/y neighbours of the C part two steps on)
+            double *Vn = vrow + (u % T3M_NV) * Lt::V_SLOT;
+#pragma unroll
+            for (int h = 0; h < R; ++h) *reinterpret_cast<double2 *>(Vn + ov[h]) = wk[h];
+            warp_arrive(&B.vfull[u % T3M_NV]);
+            if (j >= it.mb) warp_arrive(&B.empty[(s - 2) % T3M_S]);  // plane j - 2: g', P last read above
+            ++j;
+            ++u;
+            if (a_part) ++s;
+            pk_row += plane;
+            wk_row += plane;
+            wn_row += plane;
+            pn_row += plane;
+            return j <= it.me + 1;
+        };
+        for (;;) {
+            if (!step(W0, W1, W2, U0, U1, U2, U3)) break;
+            if (!step(W1, W2, W3, U1, U2, U3, U0)) break;
+            if (!step(W2, W3, W0, U2, U3, U0, U1)) break;
+            if (!step(W3, W0, W1, U3, U0, U1, U2)) break;
+        }
+        // s: stage of plane me + 1 (the C-only last step did not advance it); planes me, me + 1 still held
+        warp_arrive(&B.empty[(s - 1) % T3M_S]);
+        warp_arrive(&B.empty[s % T3M_S]);
+        ++s;
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+            const double w0 = warp_sum(acc_w0[h]), p0 = warp_sum(acc_p0[h]);
+            const double w1 = warp_sum(acc_w1[h]), p1 = warp_sum(acc_p1[h]);
+            const int r = w + T3M_NW * h;
+            if (q == 0 && it.y0 + (r & ~7) < g.ny) {
+                const int64_t e =
+                    ((int64_t)it.chunk * its.ntiles8 + it.tile8 + (r >> 3) * its.tiles_x) * TMA_CONSUMER_WARPS + (r & 7);
+                double *d0p = part + e * 2;
+                d0p[0] = w0;
+                d0p[1] = p0;
+                double *d1p = part + half + e * 2;
+                d1p[0] = w1;
+                d1p[1] = p1;
+            }
+        }
+    }
+}
+
 template <bool GD, bool NEU>
 ES_DEV void t3m_pass(const SeriesParams *P, int k, bool two, char *smem) {
     using Lt = T3mLayout<GD>;
@@ -457,7 +709,7 @@ ES_DEV void t3m_pass(const SeriesParams *P, int k, bool two, char *smem) {
             mbar_init(&B.full[s], 1);
             mbar_init(&B.empty[s], T3M_NW + 2);
         }
-        for (int s = 0; s < 2; ++s) mbar_init(&B.vfull[s], T3M_NW + 2);
+        for (int s = 0; s < T3M_NV; ++s) mbar_init(&B.vfull[s], T3M_NW + 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -472,7 +724,10 @@ ES_DEV void t3m_pass(const SeriesParams *P, int k, bool two, char *smem) {
     } else if (warp >= T3M_NW) {
         t3m_edge<GD, NEU>(g, P, k, its, smem, warp - T3M_NW);
     } else {
-        t3m_compute<GD, NEU>(g, P, k, two, its, smem);
+        if constexpr (T3M_LAG == 2)
+            t3m_compute2<GD, NEU>(g, P, k, two, its, smem);
+        else
+            t3m_compute<GD, NEU>(g, P, k, two, its, smem);
     }
 }
 
