@@ -34,6 +34,8 @@
 // Neumann (mirrored ghosts), no coefficient or the staged sampled D, no g'.
 #pragma once
 
+#include <type_traits>
+
 #include "stencil_tb2d.cuh"
 
 namespace es {
@@ -285,7 +287,8 @@ ES_DEV void tm_compute(const Geom &g, const SeriesParams *P, int k, bool two, co
         double *pk_row = pk_dst + off0, *wk_row = w1_dst + off0;
         double *wn_row = w1_dst + off0 - nx, *pn_row = pk1_dst + off0 - nx;
         int t = it.mb - 1;
-        auto step = [&](double2 (&vm)[PP], double2 (&vc)[PP], double2 (&vp)[PP], double2 (&um)[PP],
+        // full (a compile-time tag): every lane of this warp holds domain columns -- no per-lane guards
+        auto step = [&](auto full, double2 (&vm)[PP], double2 (&vc)[PP], double2 (&vp)[PP], double2 (&um)[PP],
                         double2 (&uc)[PP], double2 (&wk)[PP], double2 (&pk_prev)[PP], double2 (&pk)[PP]) -> bool {
             const char *st = smem + (q % TM_S) * Lt::STAGE;  // row t
             const char *sn = smem + ((q + 1) % TM_S) * Lt::STAGE + 8 * (4 + e0);  // row t + 1, this lane's pair 0
@@ -326,7 +329,7 @@ ES_DEV void tm_compute(const Geom &g, const SeriesParams *P, int k, bool two, co
                     const double2 po = *reinterpret_cast<const double2 *>(Pc + 64 * h);
                     pk[h] = make_double2(add(mul(pscale, po.x), mul(dk, wk[h].x)),
                                          add(mul(pscale, po.y), mul(dk, wk[h].y)));
-                    if (in0[h]) {
+                    if (decltype(full)::value || in0[h]) {
                         if (store_pk) *reinterpret_cast<double2 *>(pk_row + 64 * h) = pk[h];
                         if (!two) *reinterpret_cast<double2 *>(wk_row + 64 * h) = wk[h];  // next pass starts from w_k
                         acc_w0[h] = add(acc_w0[h], add(mul(wk[h].x, wk[h].x), mul(wk[h].y, wk[h].y)));
@@ -363,7 +366,7 @@ ES_DEV void tm_compute(const Geom &g, const SeriesParams *P, int k, bool two, co
                                                     add(mul(alpha, l1), mul(beta_k1, uc[h].y)));
                     const double2 pn =
                         make_double2(add(pk_prev[h].x, mul(dk1, wn.x)), add(pk_prev[h].y, mul(dk1, wn.y)));
-                    if (in0[h]) {
+                    if (decltype(full)::value || in0[h]) {
                         *reinterpret_cast<double2 *>(wn_row + 64 * h) = wn;
                         *reinterpret_cast<double2 *>(pn_row + 64 * h) = pn;
                         acc_w1[h] = add(acc_w1[h], add(mul(wn.x, wn.x), mul(wn.y, wn.y)));
@@ -394,11 +397,17 @@ ES_DEV void tm_compute(const Geom &g, const SeriesParams *P, int k, bool two, co
             pn_row += nx;
             return t <= it.me;
         };
-        for (;;) {
-            if (!step(W0, W1, W2, U0, U1, U2, K0, K1)) break;
-            if (!step(W1, W2, W0, U1, U2, U0, K1, K2)) break;
-            if (!step(W2, W0, W1, U2, U0, U1, K2, K0)) break;
-        }
+        auto march = [&](auto full) {
+            for (;;) {
+                if (!step(full, W0, W1, W2, U0, U1, U2, K0, K1)) break;
+                if (!step(full, W1, W2, W0, U1, U2, U0, K1, K2)) break;
+                if (!step(full, W2, W0, W1, U2, U0, U1, K2, K0)) break;
+            }
+        };
+        if (xw + 64 * PP <= nx)
+            march(std::true_type{});
+        else
+            march(std::false_type{});
         warp_arrive(&B.empty[(q - 1) % TM_S]);  // rows me, me + 1
         warp_arrive(&B.empty[q % TM_S]);
         ++q;

@@ -31,6 +31,8 @@
 // homogeneous Dirichlet or Neumann, with or without g'.
 #pragma once
 
+#include <type_traits>
+
 #include "stencil_tb2m.cuh"  // tm_v_ready; stencil_tb.cuh
 
 namespace es {
@@ -296,7 +298,8 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
         double *pk_row = pk_dst + off0, *wk_row = w1_dst + off0;
         double *wn_row = w1_dst + off0 - plane, *pn_row = pk1_dst + off0 - plane;
         int j = it.mb - 1;
-        auto step = [&](double2 (&vm)[R], double2 (&vc)[R], double2 (&vp)[R], double2 (&um)[R], double2 (&uc)[R],
+        // FULL (a compile-time tag): every lane of this warp holds domain points -- no per-lane guards
+        auto step = [&](auto full, double2 (&vm)[R], double2 (&vc)[R], double2 (&vp)[R], double2 (&um)[R], double2 (&uc)[R],
                         double2 (&wk)[R], double2 (&pk_prev)[R], double2 (&pk)[R]) -> bool {
             const char *st = smem + (s % T3M_S) * Lt::STAGE;  // plane j
             const double *Wn = reinterpret_cast<const double *>(smem + ((s + 1) % T3M_S) * Lt::STAGE);
@@ -349,7 +352,7 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
                     // pscale is 1.0 after the first pass, and 1.0 * x == x bit for bit
                     pk[h] = make_double2(add(mul(pscale, po.x), mul(dk, wk[h].x)),
                                          add(mul(pscale, po.y), mul(dk, wk[h].y)));
-                    if (in0[h]) {
+                    if (decltype(full)::value || in0[h]) {
                         if (store_pk) *reinterpret_cast<double2 *>(pk_row + h * drow) = pk[h];
                         if (!two) *reinterpret_cast<double2 *>(wk_row + h * drow) = wk[h];  // the next pass starts from w_k
                         acc_w0[h] = add(acc_w0[h], add(mul(wk[h].x, wk[h].x), mul(wk[h].y, wk[h].y)));
@@ -409,7 +412,7 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
                                                     add(mul(alpha, l1), mul(beta_k1, cc.y)));
                     const double2 pn =
                         make_double2(add(pkp[h].x, mul(dk1, wn.x)), add(pkp[h].y, mul(dk1, wn.y)));
-                    if (in0[h]) {
+                    if (decltype(full)::value || in0[h]) {
                         *reinterpret_cast<double2 *>(wn_row + h * drow) = wn;
                         *reinterpret_cast<double2 *>(pn_row + h * drow) = pn;
                         acc_w1[h] = add(acc_w1[h], add(mul(wn.x, wn.x), mul(wn.y, wn.y)));
@@ -432,11 +435,17 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
             pn_row += plane;
             return j <= it.me;
         };
-        for (;;) {
-            if (!step(W0, W1, W2, U0, U1, U2, K0, K1)) break;
-            if (!step(W1, W2, W0, U1, U2, U0, K1, K2)) break;
-            if (!step(W2, W0, W1, U2, U0, U1, K2, K0)) break;
-        }
+        auto march = [&](auto full) {
+            for (;;) {
+                if (!step(full, W0, W1, W2, U0, U1, U2, K0, K1)) break;
+                if (!step(full, W1, W2, W0, U1, U2, U0, K1, K2)) break;
+                if (!step(full, W2, W0, W1, U2, U0, U1, K2, K0)) break;
+            }
+        };
+        if (it.x0 + 64 <= nx && ylast < g.ny)
+            march(std::true_type{});
+        else
+            march(std::false_type{});
         warp_arrive(&B.empty[(s - 1) % T3M_S]);  // planes me, me + 1
         warp_arrive(&B.empty[s % T3M_S]);
         ++s;
