@@ -299,7 +299,7 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
         double *wn_row = w1_dst + off0 - plane, *pn_row = pk1_dst + off0 - plane;
         int j = it.mb - 1;
         // FULL (a compile-time tag): every lane of this warp holds domain points -- no per-lane guards
-        auto step = [&](auto full, double2 (&vm)[R], double2 (&vc)[R], double2 (&vp)[R], double2 (&um)[R], double2 (&uc)[R],
+        auto step = [&](auto full, auto steady, double2 (&vm)[R], double2 (&vc)[R], double2 (&vp)[R], double2 (&um)[R], double2 (&uc)[R],
                         double2 (&wk)[R], double2 (&pk_prev)[R], double2 (&pk)[R]) -> bool {
             const char *st = smem + (s % T3M_S) * Lt::STAGE;  // plane j
             const double *Wn = reinterpret_cast<const double *>(smem + ((s + 1) % T3M_S) * Lt::STAGE);
@@ -307,7 +307,7 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
 #pragma unroll
             for (int h = 0; h < R; ++h) vp[h] = *reinterpret_cast<const double2 *>(Wn + ow[h]);
             // ---- w_k(j)
-            if (j >= 0 && j < its.L) {
+            if (decltype(steady)::value || (j >= 0 && j < its.L)) {  // steady: an interior plane / row
                 const double *Wc = reinterpret_cast<const double *>(st);
                 const double *Gc = reinterpret_cast<const double *>(st + Lt::G_OFF);
 #pragma unroll
@@ -344,7 +344,7 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
                 for (int h = 0; h < R; ++h) wk[h] = NEU && j == its.L ? uc[h] : make_double2(0.0, 0.0);  // plane L mirrors L - 1
             }
             // ---- p_k(j) (+ node k norms)
-            if (j >= it.mb && j < it.me) {
+            if (decltype(steady)::value || (j >= it.mb && j < it.me)) {
                 const double *Pc = reinterpret_cast<const double *>(st + Lt::P_OFF);
 #pragma unroll
                 for (int h = 0; h < R; ++h) {
@@ -363,7 +363,7 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
             // ---- w_{k+1}(j-1), p_{k+1}(j-1) (+ node k+1 norms)
             t3m_v_ready(B.vfull, u);
             const int jc = j - 1;
-            if (two && jc >= it.mb && jc < it.me) {
+            if (two && (decltype(steady)::value || (jc >= it.mb && jc < it.me))) {
                 const double *Vc = vrow + ((u - 1) % T3M_NV) * Lt::V_SLOT;  // w_k(j-1) with its ring
                 const double *Gp = reinterpret_cast<const double *>(smem + ((s - 1) % T3M_S) * Lt::STAGE + Lt::G_OFF);
                 double2 pkp[R];  // p_k(j-1)
@@ -437,9 +437,18 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
         };
         auto march = [&](auto full) {
             for (;;) {
-                if (!step(full, W0, W1, W2, U0, U1, U2, K0, K1)) break;
-                if (!step(full, W1, W2, W0, U1, U2, U0, K1, K2)) break;
-                if (!step(full, W2, W0, W1, U2, U0, U1, K2, K0)) break;
+                // three steady steps (interior planes: every part active, no range checks)
+                if constexpr (decltype(full)::value) {
+                    if (j >= it.mb + 1 && j + 2 <= it.me - 1) {
+                        step(full, std::true_type{}, W0, W1, W2, U0, U1, U2, K0, K1);
+                        step(full, std::true_type{}, W1, W2, W0, U1, U2, U0, K1, K2);
+                        step(full, std::true_type{}, W2, W0, W1, U2, U0, U1, K2, K0);
+                        continue;
+                    }
+                }
+                if (!step(full, std::false_type{}, W0, W1, W2, U0, U1, U2, K0, K1)) break;
+                if (!step(full, std::false_type{}, W1, W2, W0, U1, U2, U0, K1, K2)) break;
+                if (!step(full, std::false_type{}, W2, W0, W1, U2, U0, U1, K2, K0)) break;
             }
         };
         if (it.x0 + 64 <= nx && ylast < g.ny)
