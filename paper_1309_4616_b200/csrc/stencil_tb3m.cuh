@@ -49,7 +49,13 @@ namespace es {
 // (two planes of prefetch at 6 stages): measured 1.12 vs 1.00 ms per 512^3 pass
 #define T3M_LAG 1
 #endif
-constexpr int T3M_NV = T3M_LAG + 1;  // shared w_k plane slots
+// T3M_EARLY (LAG 1): publish w_k(j) before the C part, three V slots -- the
+// other warps' wait for plane j then ends when every warp's A part is done
+// (bitwise; measured equal, 945 vs 944 us per 512^3 pass)
+#ifndef T3M_EARLY
+#define T3M_EARLY 0
+#endif
+constexpr int T3M_NV = (T3M_LAG == 2 || T3M_EARLY) ? 3 : 2;  // shared w_k plane slots
 #ifndef T3M_NW
 #define T3M_NW 8  // compute warps: rows w + T3M_NW h of the 16-row tile
 #endif
@@ -362,6 +368,12 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
             }
             // ---- w_{k+1}(j-1), p_{k+1}(j-1) (+ node k+1 norms)
             t3m_v_ready(B.vfull, u);
+            if constexpr (T3M_EARLY) {  // publish w_k(j) now (slot u % 3 held V(u-3), read at step u-2)
+                double *Vn = vrow + (u % T3M_NV) * Lt::V_SLOT;
+#pragma unroll
+                for (int h = 0; h < R; ++h) *reinterpret_cast<double2 *>(Vn + ov[h]) = wk[h];
+                warp_arrive(&B.vfull[u % T3M_NV]);
+            }
             const int jc = j - 1;
             if (two && (decltype(steady)::value || (jc >= it.mb && jc < it.me))) {
                 const double *Vc = vrow + ((u - 1) % T3M_NV) * Lt::V_SLOT;  // w_k(j-1) with its ring
@@ -421,10 +433,12 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
                 }
             }
             // ---- publish w_k(j): the x/y neighbours of the next step's C part
-            double *Vn = vrow + (u % T3M_NV) * Lt::V_SLOT;
+            if constexpr (!T3M_EARLY) {
+                double *Vn = vrow + (u % T3M_NV) * Lt::V_SLOT;
 #pragma unroll
-            for (int h = 0; h < R; ++h) *reinterpret_cast<double2 *>(Vn + ov[h]) = wk[h];
-            warp_arrive(&B.vfull[u % T3M_NV]);
+                for (int h = 0; h < R; ++h) *reinterpret_cast<double2 *>(Vn + ov[h]) = wk[h];
+                warp_arrive(&B.vfull[u % T3M_NV]);
+            }
             warp_arrive(&B.empty[(s - 1) % T3M_S]);  // plane j - 1: its g' was last read above
             ++j;
             ++s;
