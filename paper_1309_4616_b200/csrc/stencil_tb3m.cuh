@@ -4,8 +4,8 @@
 // partial sums p_k, p_{k+1}; 40 B/point for two nodes with g') without its
 // producer/consumer split between the two nodes -- the structure that took
 // the 2D pass from 207 to 158 us (stencil_tb2m.cuh).  Each of the eight
-// compute warps owns rows w and w + 8 of the 64 x 16 tile (T3M_NW = 16: row
-// w; lane q: the pair x0 + 2q, group C's mapping, so the norm partials land in the same
+// compute warps owns rows 2w and 2w + 1 of the 64 x 16 tile (T3M_ADJ; else w
+// and w + 8, group C's rows; lane q: the pair x0 + 2q, so the norm partials land in the same
 // (chunk, 64 x 8 tile, row) entries in the same order) and marches down the
 // item's z chunk; w_{k-1} of planes j-1, j and w_k of planes j-2, j-1, j and
 // p_k of the current plane stay in registers whose roles rotate over a
@@ -60,6 +60,13 @@ constexpr int T3M_NV = (T3M_LAG == 2 || T3M_EARLY) ? 3 : 2;  // shared w_k plane
 #define T3M_NW 8  // compute warps: rows w + T3M_NW h of the 16-row tile
 #endif
 constexpr int T3M_RPW = 16 / T3M_NW;               // rows per compute warp
+// T3M_ADJ: a warp owns adjacent rows (R w + h) instead of rows w + T3M_NW h,
+// so one y neighbour of each row is the other row's register (LAG 1 only;
+// 4 of 16 128-bit shared loads per step saved: 512^3 pass 912 -> 893 us)
+#ifndef T3M_ADJ
+#define T3M_ADJ 1
+#endif
+#define T3M_ROW(w, h) (T3M_ADJ ? T3M_RPW * (w) + (h) : (w) + T3M_NW * (h))
 constexpr int T3M_THREADS = 32 * (T3M_NW + 3);     // + two edge warps + producer
 static_assert(TB_TY == 16, "the plane-marching pass tiles 64 x 16");
 
@@ -254,7 +261,7 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
     int ow[R], og[R], op[R], ov[R];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
-        const int r = w + T3M_NW * h;
+        const int r = T3M_ROW(w, h);
         ow[h] = (r + 2) * TB_WX + 2 * q + 4;
         og[h] = (r + 1) * TB_GX + 2 * q + 2;
         op[h] = r * 64 + 2 * q;
@@ -274,15 +281,15 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
         bool in0[R], in1[R];
 #pragma unroll
         for (int h = 0; h < R; ++h) {
-            ya[h] = it.y0 + w + T3M_NW * h;
+            ya[h] = it.y0 + T3M_ROW(w, h);
             in0[h] = xa < nx && ya[h] < g.ny;
             in1[h] = xa + 1 < nx && ya[h] < g.ny;
         }
         // warp-uniform: does this warp hold a domain-edge column / row (Neumann
         // ghost rules) or points outside the domain (Dirichlet masks)?
         const bool xedge = it.x0 == 0 || it.x0 + 64 >= nx;
-        const int ylast = it.y0 + w + T3M_NW * (R - 1);  // this warp's last row
-        const bool yedge = it.y0 + w == 0 || ylast >= g.ny - 1;
+        const int ylast = it.y0 + T3M_ROW(w, R - 1);  // this warp's last row
+        const bool yedge = it.y0 + T3M_ROW(w, 0) == 0 || ylast >= g.ny - 1;
         const bool special = NEU ? (xedge || yedge) : (it.x0 + 64 > nx || ylast >= g.ny);
         double acc_w0[R], acc_p0[R], acc_w1[R], acc_p1[R];
 #pragma unroll
@@ -299,8 +306,8 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
             }
             ++s;  // s: stage of plane j (plane mb - 2 is released by the first step)
         }
-        const int64_t off0 = (int64_t)(it.mb - 1) * plane + it.y0 * nx + xa + (int64_t)w * nx;  // row 0, plane j
-        const int64_t drow = (int64_t)T3M_NW * nx;
+        const int64_t off0 = (int64_t)(it.mb - 1) * plane + it.y0 * nx + xa + (int64_t)T3M_ROW(w, 0) * nx;  // row h = 0, plane j
+        const int64_t drow = (int64_t)(T3M_ROW(w, 1) - T3M_ROW(w, 0)) * nx;
         double *pk_row = pk_dst + off0, *wk_row = w1_dst + off0;
         double *wn_row = w1_dst + off0 - plane, *pn_row = pk1_dst + off0 - plane;
         int j = it.mb - 1;
@@ -318,8 +325,11 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
                 const double *Gc = reinterpret_cast<const double *>(st + Lt::G_OFF);
 #pragma unroll
                 for (int h = 0; h < R; ++h) {
-                    const double2 ym = *reinterpret_cast<const double2 *>(Wc + ow[h] - TB_WX);
-                    const double2 yp = *reinterpret_cast<const double2 *>(Wc + ow[h] + TB_WX);
+                    // T3M_ADJ: the warp's other row is a y neighbour held in registers
+                    const double2 ym = T3M_ADJ && h > 0 ? vc[h > 0 ? h - 1 : 0]
+                                                        : *reinterpret_cast<const double2 *>(Wc + ow[h] - TB_WX);
+                    const double2 yp = T3M_ADJ && h < R - 1 ? vc[h < R - 1 ? h + 1 : 0]
+                                                            : *reinterpret_cast<const double2 *>(Wc + ow[h] + TB_WX);
                     double xm = Wc[ow[h] - 1], xp = Wc[ow[h] + 2];
                     double ym0 = ym.x, ym1 = ym.y, yp0 = yp.x, yp1 = yp.y;
                     if (NEU && special) {  // the point itself is the ghost at the domain edge
@@ -393,8 +403,10 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
 #pragma unroll
                 for (int h = 0; h < R; ++h) {
                     const double2 cc = uc[h];
-                    const double2 ym = *reinterpret_cast<const double2 *>(Vc + ov[h] - TB_EX);
-                    const double2 yp = *reinterpret_cast<const double2 *>(Vc + ov[h] + TB_EX);
+                    const double2 ym = T3M_ADJ && h > 0 ? uc[h > 0 ? h - 1 : 0]
+                                                        : *reinterpret_cast<const double2 *>(Vc + ov[h] - TB_EX);
+                    const double2 yp = T3M_ADJ && h < R - 1 ? uc[h < R - 1 ? h + 1 : 0]
+                                                            : *reinterpret_cast<const double2 *>(Vc + ov[h] + TB_EX);
                     double xm = Vc[ov[h] - 1], xp = Vc[ov[h] + 2];
                     double ym0 = ym.x, ym1 = ym.y, yp0 = yp.x, yp1 = yp.y;
                     double2 zm = um[h], zp = wk[h];
@@ -477,7 +489,7 @@ ES_DEV void t3m_compute(const Geom &g, const SeriesParams *P, int k, bool two, c
         for (int h = 0; h < R; ++h) {
             const double w0 = warp_sum(acc_w0[h]), p0 = warp_sum(acc_p0[h]);
             const double w1 = warp_sum(acc_w1[h]), p1 = warp_sum(acc_p1[h]);
-            const int r = w + T3M_NW * h;
+            const int r = T3M_ROW(w, h);
             if (q == 0 && it.y0 + (r & ~7) < g.ny) {  // the 64 x 8 tile of row r exists
                 const int64_t e =
                     ((int64_t)it.chunk * its.ntiles8 + it.tile8 + (r >> 3) * its.tiles_x) * TMA_CONSUMER_WARPS + (r & 7);
