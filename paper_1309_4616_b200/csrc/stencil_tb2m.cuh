@@ -105,7 +105,7 @@ ES_DEV void tm_produce(const Geom &g, const Tb2Items &its, const Tb2Maps &mp, ch
         for (int t = it.mb - 2; t <= it.me + 1; ++t, ++q) {
             if (t == max(it.mb - 2, it.me - 3)) inext = work ? (int)atomicAdd(work, 1u) : i + (int)gridDim.x;
             const uint32_t s = q % TM_S;
-            if (q >= (uint32_t)TM_S) mbar_wait(&B.empty[s], ((q / TM_S) - 1) & 1);
+            if (q >= (uint32_t)TM_S) mbar_wait_sleep(&B.empty[s], ((q / TM_S) - 1) & 1);
             itemq[s] = i;
             const bool drow = STAGED && t >= it.mb - 1 && t <= it.me;
             const bool prow = t >= it.mb && t < it.me;
@@ -131,15 +131,19 @@ ES_DEV void tm_produce(const Geom &g, const Tb2Items &its, const Tb2Maps &mp, ch
         i = inext;
     }
     const uint32_t s = q % TM_S;  // end-of-work marker
-    if (q >= (uint32_t)TM_S) mbar_wait(&B.empty[s], ((q / TM_S) - 1) & 1);
+    if (q >= (uint32_t)TM_S) mbar_wait_sleep(&B.empty[s], ((q / TM_S) - 1) & 1);
     itemq[s] = -1;
     mbar_arrive(&B.full[s]);
 }
 
 // one row step's V slot: wait until every warp has finished the previous
 // step (its C part read V(t-2), which this step overwrites)
-ES_DEV void tm_v_ready(uint64_t *vfull, uint32_t u) {
-    if (u > 0) mbar_wait(&vfull[(u - 1) & 1], ((u - 1) >> 1) & 1);
+ES_DEV void tm_v_ready(uint64_t *vfull, uint32_t u, bool sleep = false) {
+    if (u == 0) return;
+    if (sleep)
+        mbar_wait_sleep(&vfull[(u - 1) & 1], ((u - 1) >> 1) & 1);
+    else
+        mbar_wait(&vfull[(u - 1) & 1], ((u - 1) >> 1) & 1);
 }
 
 // The edge warp: w_k at x0 - 1 (lane 0) and x0 + TX (lane 1) of every row,
@@ -159,7 +163,7 @@ ES_DEV void tm_edge(const Geom &g, const SeriesParams *P, int k, const Tb2Items 
     auto stage = [&](uint32_t q) { return smem + (q % TM_S) * Lt::STAGE; };
     uint32_t q = 0, u = 0;
     for (;;) {
-        mbar_wait(&B.full[q % TM_S], (q / TM_S) & 1);
+        mbar_wait_sleep(&B.full[q % TM_S], (q / TM_S) & 1);
         const int i = itemq[q % TM_S];
         if (i < 0) break;
         const Tb2Item it = tm_item_at(its, i);
@@ -169,12 +173,12 @@ ES_DEV void tm_edge(const Geom &g, const SeriesParams *P, int k, const Tb2Items 
         const int go = lane == 0 ? 1 : TM_TX + 2;  // D / V index of x
         double em = 0.0, ec = 0.0;
         if (lane < 2) em = reinterpret_cast<const double *>(stage(q))[wo];
-        mbar_wait(&B.full[(q + 1) % TM_S], ((q + 1) / TM_S) & 1);
+        mbar_wait_sleep(&B.full[(q + 1) % TM_S], ((q + 1) / TM_S) & 1);
         if (lane < 2) ec = reinterpret_cast<const double *>(stage(q + 1))[wo];
         warp_arrive(&B.empty[q % TM_S]);
         ++q;  // q: stage of row t
         for (int t = it.mb - 1; t <= it.me; ++t, ++q, ++u) {
-            mbar_wait(&B.full[(q + 1) % TM_S], ((q + 1) / TM_S) & 1);
+            mbar_wait_sleep(&B.full[(q + 1) % TM_S], ((q + 1) / TM_S) & 1);
             double w = 0.0, ep = 0.0;
             if (lane < 2) {
                 const double *Wc = reinterpret_cast<const double *>(stage(q));
@@ -186,7 +190,7 @@ ES_DEV void tm_edge(const Geom &g, const SeriesParams *P, int k, const Tb2Items 
                     w = add(mul(alpha, lap), mul(beta_k, ec));
                 }
             }
-            tm_v_ready(B.vfull, u);
+            tm_v_ready(B.vfull, u, true);
             if (lane < 2) vrow[(u & 1) * Lt::V_SLOT + go] = w;
             warp_arrive(&B.vfull[u & 1]);
             warp_arrive(&B.empty[q % TM_S]);

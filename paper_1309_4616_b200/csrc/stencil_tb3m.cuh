@@ -109,7 +109,7 @@ ES_DEV void t3m_produce(const Geom &g, const TbItems &its, const TbMaps &mp, cha
         for (int t = it.mb - 2; t <= it.me + 1; ++t, ++q) {
             if (t == max(it.mb - 2, it.me - 3)) inext = work ? (int)atomicAdd(work, 1u) : i + (int)gridDim.x;
             const uint32_t s = q % T3M_S;
-            if (q >= (uint32_t)T3M_S) mbar_wait(&B.empty[s], ((q / T3M_S) - 1) & 1);
+            if (q >= (uint32_t)T3M_S) mbar_wait_sleep(&B.empty[s], ((q / T3M_S) - 1) & 1);
             itemq[s] = i;
             const bool gplane = GD && t >= it.mb - 1 && t <= it.me;
             const bool pplane = t >= it.mb && t < it.me;
@@ -122,14 +122,18 @@ ES_DEV void t3m_produce(const Geom &g, const TbItems &its, const TbMaps &mp, cha
         i = inext;
     }
     const uint32_t s = q % T3M_S;  // end-of-work marker
-    if (q >= (uint32_t)T3M_S) mbar_wait(&B.empty[s], ((q / T3M_S) - 1) & 1);
+    if (q >= (uint32_t)T3M_S) mbar_wait_sleep(&B.empty[s], ((q / T3M_S) - 1) & 1);
     itemq[s] = -1;
     mbar_arrive(&B.full[s]);
 }
 
 // one step's V slot (u % T3M_NV): wait until every warp has finished step u - 1
-ES_DEV void t3m_v_ready(uint64_t *vfull, uint32_t u) {
-    if (u > 0) mbar_wait(&vfull[(u - 1) % T3M_NV], ((u - 1) / T3M_NV) & 1);
+ES_DEV void t3m_v_ready(uint64_t *vfull, uint32_t u, bool sleep = false) {
+    if (u == 0) return;
+    if (sleep)
+        mbar_wait_sleep(&vfull[(u - 1) % T3M_NV], ((u - 1) / T3M_NV) & 1);
+    else
+        mbar_wait(&vfull[(u - 1) % T3M_NV], ((u - 1) / T3M_NV) & 1);
 }
 
 // w_k at one ring point (x, y) of plane j: tb_point_scalar's expression with
@@ -171,7 +175,7 @@ ES_DEV void t3m_edge(const Geom &g, const SeriesParams *P, int k, const TbItems 
     auto stage = [&](uint32_t s) { return smem + (s % T3M_S) * Lt::STAGE; };
     uint32_t s = 0, u = 0;
     for (;;) {
-        mbar_wait(&B.full[s % T3M_S], (s / T3M_S) & 1);
+        mbar_wait_sleep(&B.full[s % T3M_S], (s / T3M_S) & 1);
         const int i = itemq[s % T3M_S];
         if (i < 0) break;
         const TbItem it = tb_item_at(its, i);
@@ -191,7 +195,7 @@ ES_DEV void t3m_edge(const Geom &g, const SeriesParams *P, int k, const TbItems 
         double em[3], ec[3];
         {
             const double *W0 = reinterpret_cast<const double *>(stage(s));
-            mbar_wait(&B.full[(s + 1) % T3M_S], ((s + 1) / T3M_S) & 1);
+            mbar_wait_sleep(&B.full[(s + 1) % T3M_S], ((s + 1) / T3M_S) & 1);
             const double *W1 = reinterpret_cast<const double *>(stage(s + 1));
 #pragma unroll
             for (int h = 0; h < 3; ++h) {
@@ -204,7 +208,7 @@ ES_DEV void t3m_edge(const Geom &g, const SeriesParams *P, int k, const TbItems 
         for (int j = it.mb - 1; j <= it.me + T3M_LAG - 1; ++j, ++u) {
             double wv[3] = {0.0, 0.0, 0.0};
             if (j <= it.me) {  // (LAG 2: the compute warps' extra C-only step has no plane)
-                mbar_wait(&B.full[(s + 1) % T3M_S], ((s + 1) / T3M_S) & 1);
+                mbar_wait_sleep(&B.full[(s + 1) % T3M_S], ((s + 1) / T3M_S) & 1);
                 const char *st = stage(s);
                 const double *Wn = reinterpret_cast<const double *>(stage(s + 1));
                 double ep[3];
@@ -222,7 +226,7 @@ ES_DEV void t3m_edge(const Geom &g, const SeriesParams *P, int k, const TbItems 
                     ec[h] = ep[h];
                 }
             }
-            t3m_v_ready(B.vfull, u);
+            t3m_v_ready(B.vfull, u, true);
             double *V = vrow + (u % T3M_NV) * Lt::V_SLOT;
             V[vo[0]] = wv[0];
             V[vo[1]] = wv[1];
