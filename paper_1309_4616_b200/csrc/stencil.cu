@@ -834,7 +834,11 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
         pl.items = (int64_t)((d->nx + tx - 1) / tx) * ((d->ny + chunk2 - 1) / chunk2);
     }
     if (S.tb) {
-        pl.chunk = std::max(1, env_int("ES_TBCHUNK", 32));
+        // plane-marching pass (one domain, no coefficient): z chunks of 64
+        // (halo planes 2 per 64, ~14 items per CTA at 512^3: 896-909 vs
+        // 918-922 us per pass at 32); the group A / C kernel keeps 32
+        const bool march3 = !halos && d->coeff_kind == ES_COEFF_NONE && env_int("ES_TB3M", 1);
+        pl.chunk = std::max(1, env_int("ES_TBCHUNK", march3 ? 64 : 32));
         pl.grid.z = (unsigned)((d->lz + pl.chunk - 1) / pl.chunk);
         pl.nchunks = pl.grid.z;
         pl.items = (int64_t)pl.grid.x * pl.grid.y * pl.nchunks;
