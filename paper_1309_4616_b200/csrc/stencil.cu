@@ -834,11 +834,22 @@ static int prepare_series(const es_stencil_desc *d, const double *v, double *p_o
         pl.items = (int64_t)((d->nx + tx - 1) / tx) * ((d->ny + chunk2 - 1) / chunk2);
     }
     if (S.tb) {
-        // plane-marching pass (one domain, no coefficient): z chunks of 64
-        // (halo planes 2 per 64, ~14 items per CTA at 512^3: 896-909 vs
-        // 918-922 us per pass at 32); the group A / C kernel keeps 32
+        // plane-marching pass (one domain, no coefficient, one CTA per SM):
+        // the longest z chunk (two halo planes per chunk) that still leaves
+        // >= 6 items per CTA -- 512^3: 128 planes, 877-880 us per pass
+        // (64: 891-893, 32: 918-922); the group A / C kernel keeps 32
         const bool march3 = !halos && d->coeff_kind == ES_COEFF_NONE && env_int("ES_TB3M", 1);
-        pl.chunk = std::max(1, env_int("ES_TBCHUNK", march3 ? 64 : 32));
+        int zc = 32;
+        if (march3) {
+            const int64_t tiles = ((d->nx + 63) / 64) * ((d->ny + TB_TY - 1) / TB_TY);
+            for (int c : {128, 64}) {
+                if (tiles * ((d->lz + c - 1) / c) >= 6 * (int64_t)sm_count()) {
+                    zc = c;
+                    break;
+                }
+            }
+        }
+        pl.chunk = std::max(1, env_int("ES_TBCHUNK", zc));
         pl.grid.z = (unsigned)((d->lz + pl.chunk - 1) / pl.chunk);
         pl.nchunks = pl.grid.z;
         pl.items = (int64_t)pl.grid.x * pl.grid.y * pl.nchunks;
