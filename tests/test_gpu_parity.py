@@ -1087,6 +1087,31 @@ def test_two_node_pass_bitwise(graph, march, monkeypatch):
         assert torch.equal(got, ref), (dims, bc)
 
 
+@pytest.mark.parametrize("dims,bc,chunk", [((512, 512, 256), "homogeneous", None), ((256, 128, 300), "neumann", "128")])
+def test_two_node_long_chunks_bitwise(dims, bc, chunk, monkeypatch):
+    """The plane-marching pass picks longer z chunks on large grids
+    (csrc/stencil.cu prepare_series: 64 planes for the first grid; the
+    second forces 128 with a ragged last chunk): p and matvec counts equal
+    the one-node series bit for bit, with g' and tol > 0."""
+    if chunk:
+        monkeypatch.setenv("ES_TBCHUNK", chunk)
+    g = es.Grid3D(*dims)
+    op = es.StencilOperator(g, BCS[bc])
+    iv = es.gershgorin_interval(op).widened(30.0)
+    rng = np.random.default_rng(sum(dims))
+    v = torch.from_numpy(rng.standard_normal(g.n)).cuda()
+    gdiag = torch.from_numpy(rng.random(g.n) * 30.0).cuda()
+    it = es.make_interpolant(iv, "phi1", -1e-5, 60, 1e-8)
+    out = {}
+    for tb in ("0", "1"):
+        monkeypatch.setenv("ES_TB", tb)
+        out[tb] = es.newton_apply(op, it, v, 1e-9, gdiag=gdiag)
+    monkeypatch.delenv("ES_TB")
+    (ref, m0), (got, m1) = out["0"], out["1"]
+    assert m1 == m0 and m0 > 4, (m0, m1)
+    assert torch.equal(got, ref)
+
+
 @pytest.mark.parametrize("dims,bc,nodes", [((6, 4, 2), "homogeneous", 7), ((10, 9, 3), "neumann", 8),
                                            ((130, 17, 33), "homogeneous", 9), ((64, 8, 64), "neumann", 2),
                                            ((66, 10, 35), "homogeneous", 3), ((2, 2, 5), "neumann", 6)])
